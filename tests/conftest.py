@@ -1,0 +1,21 @@
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); parity tests through the C-ABI")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _build_native():
+    # builds kurgen/, oracle/ and libkur.so in-tree if missing or stale
+    subprocess.run(["make", "-s", "-C", ROOT, "kurgen/libkurgen.so", "oracle/liboracle.so"], check=True)
+    yield
