@@ -1,0 +1,206 @@
+/* kur.h — C ABI of libkur.so: the B200 hot path of Böhle, Kuehn & Thalhammer,
+ * "On the reliable and efficient numerical integration of the Kuramoto model
+ * and related dynamical systems on graphs" (arXiv 2102.07167).
+ *
+ * Citation shorthand: P:n = line n of the paper's text.
+ *
+ * The problem (eq. KuramotoGraph, uniform scaling M_m = M,
+ * P:404-408; A need not be symmetric):
+ *
+ *     theta_j' = omega_j + (K/N) * sum_k A_jk sin(theta_k - theta_j)
+ *
+ * evaluated through LOCALISED ORDER PARAMETERS (eq.
+ * KuramotoGraphApproach) on a community-permuted adjacency:
+ * z_k = e^{i theta_k} once per stage, per column community b the block sum
+ * S_b = sum_{k in b} z_k, per row
+ *     W_j = sum_{b dense for c(j)} S_b - sum_{k in Z_j} z_k + sum_{k in NZ_j} z_k
+ * (complement lists Z_j in dense blocks; non-zero lists NZ_j in
+ * sparse blocks), and
+ *     RHS_j = omega_j + (K/N) Im(conj(z_j) W_j)
+ * inside fixed-step classical RK4 (reading R8).
+ *
+ * Conventions for every call:
+ *  - Every function returns a kur_status; none aborts, throws or exits.
+ *    On failure a message is kept in a thread-local buffer (kur_last_error).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  All device work is stream-ordered on it; only
+ *    kur_graph_build, kur_graph_destroy, kur_check and kur_graph_permutation
+ *    block the host.
+ *  - Device vectors (theta, omega, dtheta, r_trace, r_psi, local) are
+ *    caller-owned device pointers on the handle's device, fp64, in INTERNAL
+ *    (community-contiguous) order, covering this rank's rows
+ *    [row_begin, row_end) of kur_graph_info.  kur_permute converts between the
+ *    user order and the internal order ("permute these quantities
+ *    accordingly, perform the time integration, and reorder the solution").
+ *  - A handle is not thread-safe; calls on one handle must be serialised.
+ *  - With world > 1, kur_rhs, kur_step and kur_order_parameter are
+ *    collectives: every rank calls them in the same order.
+ */
+#ifndef KUR_H_
+#define KUR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KUR_OK = 0,
+  KUR_ERR_INVALID_ARG = 1,     /* bad scalar (h <= 0, non-finite K, n < 1, threshold outside [0,1]),
+                                  NULL pointer, unsorted list, bad segment kind */
+  KUR_ERR_INDEX_RANGE = 2,     /* a column id outside [0, n) */
+  KUR_ERR_DUPLICATE_INDEX = 3, /* a column listed twice in one segment, or a community given
+                                  two segments in one row */
+  KUR_ERR_PARTITION = 4,       /* a label outside [0, n_comm), or a listed column outside its
+                                  segment's community */
+  KUR_ERR_SIZE_MISMATCH = 5,   /* pointer-array lengths inconsistent (e.g. idx_ptr not monotone) */
+  KUR_ERR_OOM = 6,             /* host or device allocation failed */
+  KUR_ERR_CUDA = 7,            /* a CUDA runtime error (message in kur_last_error) */
+  KUR_ERR_NCCL = 8,            /* an NCCL error (message in kur_last_error) */
+  KUR_ERR_NONFINITE = 9,       /* a non-finite phase was produced by kur_step (see kur_check) */
+  KUR_ERR_UNSUPPORTED = 10     /* valid request this build does not support (message says why) */
+} kur_status;
+
+/* Segment kinds of the row-segmented adjacency pattern. */
+enum { KUR_ONES = 0, KUR_ZEROS = 1 };
+/* kur_graph_desc.flags */
+enum { KUR_FLAG_RPT1 = 1, KUR_FLAG_RPT2 = 2, KUR_FLAG_RPT4 = 4 };
+
+/* Adjacency A in USER numbering, row-segmented by column community.
+ * Row u owns segments seg_ptr[u] .. seg_ptr[u+1]-1; segment s covers column
+ * community seg_comm[s] (strictly increasing within a row) and lists
+ * idx[idx_ptr[s] .. idx_ptr[s+1]-1], user column ids inside that community,
+ * strictly ascending:
+ *   KUR_ONES : the listed columns are exactly the ones of row u in that community;
+ *   KUR_ZEROS: the listed columns are exactly the zeros; every other member is a one.
+ * A community with no segment in row u is all zeros in that row.  The
+ * diagonal A_uu is "neglected": whether or not it is listed, it
+ * never contributes (reading R2).  A plain CSR matrix is the special
+ * case "one KUR_ONES segment per non-empty (row, community)".
+ * Host arrays are only read during kur_graph_build (copied; not retained). */
+typedef struct {
+  int64_t n;                /* N: number of oscillators (the paper's M) */
+  int32_t n_comm;           /* C: number of communities (labels 0..C-1; empty ones allowed) */
+  const int32_t *community; /* [n]     community of user node u (the partition) */
+  const int64_t *seg_ptr;   /* [n+1]   seg_ptr[0] = 0, non-decreasing */
+  const int32_t *seg_comm;  /* [nseg]  column community of each segment */
+  const uint8_t *seg_kind;  /* [nseg]  KUR_ONES or KUR_ZEROS */
+  const int64_t *idx_ptr;   /* [nseg+1] idx_ptr[0] = 0, non-decreasing */
+  const int32_t *idx;       /* [idx_ptr[nseg]] user column ids (may be NULL if empty) */
+  double dense_threshold;   /* block (a,b) is DENSE iff zeros_ab < threshold * entries_ab, counted
+                               over off-diagonal entries; < 0 selects the paper's rule
+                               "precompute when ones outnumber zeros": DENSE iff
+                               zeros < ones, a tie is SPARSE (reading R3).  0 forces all-sparse
+                               (direct CSR); must be <= 1. */
+  int32_t hot_min;          /* tuning: minimum entries of a tile in one column window for the
+                               window to be staged in shared memory; <= 0 selects the default */
+  int32_t flags;            /* 0, or KUR_FLAG_RPT1/2/4: force 1/2/4 rows per thread (tile = 512/1024/2048
+                               rows) instead of the size-based choice; other bits must be 0 */
+} kur_graph_desc;
+
+/* Multi-GPU placement: contiguous ranges of whole communities per rank.
+ * nccl_id points at a 128-byte ncclUniqueId that rank 0 created with
+ * kur_nccl_unique_id and the caller broadcast (e.g. over a torch process
+ * group).  NULL desc = single GPU (the current device). */
+typedef struct {
+  int32_t rank;
+  int32_t world;
+  int32_t device;
+  const void *nccl_id;
+} kur_dist_desc;
+
+typedef struct {
+  int64_t n, n_comm;
+  int32_t rank, world, device, rows_per_tile;
+  int64_t row_begin, row_end;  /* this rank's internal rows */
+  int64_t nnz;                 /* ones of A, diagonal excluded (direct-CSR entry count) */
+  int64_t n_idx;               /* stored list entries (complements + non-zeros), this rank */
+  int64_t n_idx_hot;           /* of which gathered from shared-memory windows (16-bit) */
+  int64_t n_idx_remote;        /* of which gathered from global memory (32-bit) */
+  int64_t n_slots_hot;         /* hot slots incl. padding */
+  int64_t n_slots_remote;      /* remote slots incl. padding */
+  int64_t n_dense_blocks;      /* non-empty blocks handled by precomputed sums */
+  int64_t n_sparse_blocks;     /* non-empty blocks handled by direct summation */
+  int64_t n_tiles, n_hot_parts;
+  int64_t sincos_per_rhs;      /* N sin/cos pairs = the "2M" trig evaluations of P:660 */
+  int64_t bytes_per_rhs;       /* algorithmic HBM bytes of one RHS */
+  int64_t bytes_pool;          /* device bytes of the index pool (incl. padding) */
+  double build_seconds;        /* host time of kur_graph_build */
+} kur_graph_info_t;
+
+typedef struct kur_graph kur_graph; /* opaque; owns all device data and workspace */
+
+/* Builds the block plan (census, dense/sparse rule, permutation, lists) on the
+ * host and uploads it.  Blocks.  See P:524-571. */
+kur_status kur_graph_build(const kur_graph_desc *desc, const kur_dist_desc *dist, void *stream,
+                           kur_graph **out);
+kur_status kur_graph_destroy(kur_graph *g);
+kur_status kur_graph_info(const kur_graph *g, kur_graph_info_t *info);
+
+/* Host copy of the permutation: perm[i] = user id of internal node i (all n). Blocks. */
+kur_status kur_graph_permutation(const kur_graph *g, int32_t *perm);
+
+enum { KUR_USER_TO_INTERNAL = 0, KUR_INTERNAL_TO_USER = 1 };
+/* Device permutation of a full-length fp64 vector (both in and out have n
+ * entries; in != out).  USER_TO_INTERNAL: out[i] = in[perm[i]];
+ * INTERNAL_TO_USER: out[perm[i]] = in[i]. */
+kur_status kur_permute(const kur_graph *g, const double *in, double *out, int32_t dir, void *stream);
+
+/* dtheta = G(theta): one evaluation of the right-hand side (P:443 with the
+ * block-hybrid sums of P:538-570).  theta, omega, dtheta: this rank's rows. */
+kur_status kur_rhs(kur_graph *g, const double *theta, const double *omega, double K, double *dtheta,
+                   void *stream);
+
+/* nsteps classical RK4 steps of size h, theta updated in place (this rank's
+ * rows).  If record_every > 0 and r_trace != NULL, the order parameter
+ * (r, psi) of theta_n is written to r_trace[2*(n/record_every)]
+ * for every n = 0, record_every, 2*record_every, ... <= nsteps
+ * (floor(nsteps/record_every)+1 pairs, replicated on every rank).
+ * A non-finite phase raises a device flag reported by kur_check. */
+kur_status kur_step(kur_graph *g, double *theta, const double *omega, double K, double h,
+                    int64_t nsteps, int32_t record_every, double *r_trace, void *stream);
+
+/* r_psi[2] = (r, psi) of the complex order parameter r e^{i psi} =
+ * (1/N) sum_k e^{i theta_k} (psi = 0 when r = 0).  local (may be
+ * NULL): [n_comm][2] = (r_b, psi_b) of the localised order parameters
+ * S_b / n_b; empty communities give (0, 0). */
+kur_status kur_order_parameter(kur_graph *g, const double *theta, double *r_psi, double *local,
+                               void *stream);
+
+/* Synchronises `stream`; returns KUR_ERR_NONFINITE (and clears the flag) if a
+ * previous kur_step produced a non-finite phase. */
+kur_status kur_check(kur_graph *g, void *stream);
+
+/* ---- Host-only plan introspection (no device needed; tests and tooling) ----
+ * kur_plan_build runs exactly the host builder of kur_graph_build (validation,
+ * census, dense/sparse rule, permutation, tiles, chunked layout) for one rank
+ * and keeps the result on the host.  kur_plan_export DECODES the stored
+ * layout back into plain lists, so a caller can rebuild A from it:
+ *   sizes[0..9] = n, n_comm, n_local, row_begin, n_entries (stored entries of
+ *   this rank, padding excluded), n_dense_pairs (length of D_idx), n_tiles,
+ *   rows_per_tile, nnz, world;
+ *   perm[n]: user id of internal node i; D_ptr[n_comm+1], D_idx: dense column
+ *   communities of each row community (their block sums are added);
+ *   row_ptr[n_local+1], cols[n_entries] (internal column ids), neg[n_entries]
+ *   (1 = complement entry, subtracted; 0 = non-zero entry, added,
+ *   P:538-542) for this rank's rows; shard_row0[world+1]: row ranges of all
+ *   ranks.  Errors as kur_graph_build. */
+typedef struct kur_plan kur_plan;
+kur_status kur_plan_build(const kur_graph_desc *desc, int32_t rank, int32_t world, int32_t sm_count,
+                          kur_plan **out);
+kur_status kur_plan_sizes(const kur_plan *p, int64_t *sizes /* [10] */);
+kur_status kur_plan_export(const kur_plan *p, int32_t *perm, int32_t *D_ptr, int32_t *D_idx, int64_t *row_ptr,
+                           int32_t *cols, int8_t *neg, int32_t *shard_row0);
+kur_status kur_plan_destroy(kur_plan *p);
+
+/* Creates a 128-byte NCCL unique id (rank 0), to be broadcast by the caller. */
+kur_status kur_nccl_unique_id(void *id128);
+
+const char *kur_status_string(kur_status s);
+const char *kur_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KUR_H_ */

@@ -1,0 +1,473 @@
+// api.cpp — the C ABI of libkur.so (include/kur.h): handle ownership, device
+// memory, launch orchestration, error conventions.  Product code.
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <omp.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "kur.h"
+#include "plan.h"
+
+using namespace kur;
+
+namespace {
+thread_local std::string g_last_error;
+
+kur_status fail(kur_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+kur_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(KUR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define KUR_CUDA(call)                                                     \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);                    \
+  } while (0)
+
+template <class T>
+cudaError_t upload(T** dptr, const std::vector<T>& v) {
+  const size_t bytes = sizeof(T) * (v.empty() ? 1 : v.size());
+  cudaError_t e = cudaMalloc((void**)dptr, bytes);
+  if (e != cudaSuccess) return e;
+  if (!v.empty()) e = cudaMemcpy(*dptr, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
+  return e;
+}
+}  // namespace
+
+struct kur_graph {
+  int device = 0;
+  int64_t n = 0, n_local = 0, n_pad = 0;
+  int32_t C = 0;
+  kur_graph_info_t info{};
+  std::vector<int32_t> perm_host;
+  DevPlan dp{};
+  // device allocations
+  TileDesc* d_tiles = nullptr;
+  int32_t* d_order = nullptr;
+  PartInfo* d_parts = nullptr;
+  uint2* d_chunks = nullptr;
+  uint4* d_pool = nullptr;
+  int32_t *d_comm_tile0 = nullptr, *d_D_ptr = nullptr, *d_D_idx = nullptr, *d_csize = nullptr, *d_perm = nullptr;
+  double2 *zA = nullptr, *zB = nullptr, *TA = nullptr, *TB = nullptr, *S = nullptr, *partial = nullptr;
+  double* acc = nullptr;
+  Ctrl* ctrl = nullptr;
+  ncclComm_t comm = nullptr;
+
+  ~kur_graph() {
+    cudaSetDevice(device);
+    void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
+                    d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (comm) ncclCommDestroy(comm);
+  }
+};
+
+extern "C" {
+
+const char* kur_status_string(kur_status s) {
+  switch (s) {
+    case KUR_OK: return "KUR_OK";
+    case KUR_ERR_INVALID_ARG: return "KUR_ERR_INVALID_ARG";
+    case KUR_ERR_INDEX_RANGE: return "KUR_ERR_INDEX_RANGE";
+    case KUR_ERR_DUPLICATE_INDEX: return "KUR_ERR_DUPLICATE_INDEX";
+    case KUR_ERR_PARTITION: return "KUR_ERR_PARTITION";
+    case KUR_ERR_SIZE_MISMATCH: return "KUR_ERR_SIZE_MISMATCH";
+    case KUR_ERR_OOM: return "KUR_ERR_OOM";
+    case KUR_ERR_CUDA: return "KUR_ERR_CUDA";
+    case KUR_ERR_NCCL: return "KUR_ERR_NCCL";
+    case KUR_ERR_NONFINITE: return "KUR_ERR_NONFINITE";
+    case KUR_ERR_UNSUPPORTED: return "KUR_ERR_UNSUPPORTED";
+  }
+  return "KUR_ERR_UNKNOWN";
+}
+
+const char* kur_last_error(void) { return g_last_error.c_str(); }
+
+kur_status kur_nccl_unique_id(void* id128) {
+  if (!id128) return fail(KUR_ERR_INVALID_ARG, "id128 is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(KUR_ERR_NCCL, ncclGetErrorString(r));
+  std::memcpy(id128, &id, sizeof(id));
+  return KUR_OK;
+}
+
+kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist, void* stream,
+                           kur_graph** out) {
+  (void)stream;
+  if (!out) return fail(KUR_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  int32_t rank = 0, world = 1;
+  int device = 0;
+  if (dist) {
+    rank = dist->rank;
+    world = dist->world;
+    device = dist->device;
+  } else {
+    KUR_CUDA(cudaGetDevice(&device));
+  }
+  if (world != 1) return fail(KUR_ERR_UNSUPPORTED, "world > 1 is not supported by this build yet");
+  KUR_CUDA(cudaSetDevice(device));
+  int sm = 148;
+  cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device);
+  HostPlan P;
+  std::string err;
+  kur_status st;
+  try {
+    st = build_plan(desc, rank, world, sm, P, err);
+  } catch (const std::bad_alloc&) {
+    return fail(KUR_ERR_OOM, "host allocation failed in kur_graph_build");
+  }
+  if (st != KUR_OK) return fail(st, err);
+
+  kur_graph* g = new (std::nothrow) kur_graph();
+  if (!g) return fail(KUR_ERR_OOM, "host allocation failed");
+  g->device = device;
+  g->n = P.n;
+  g->C = P.C;
+  g->n_local = P.row_end - P.row_begin;
+  g->n_pad = ((P.n + 1 + WZ - 1) / WZ) * WZ + WZ;  // z[n..n_pad) stay zero (sentinels, window tails)
+  g->perm_host = P.perm;
+  auto bail = [&](cudaError_t e, const char* what) {
+    delete g;
+    return e == cudaErrorMemoryAllocation ? fail(KUR_ERR_OOM, std::string(what) + ": out of device memory")
+                                          : cuda_fail(e, what);
+  };
+  cudaError_t e;
+  std::vector<PartInfo> parts(P.part_window.size());
+  for (size_t i = 0; i < parts.size(); ++i) parts[i] = PartInfo{P.part_window[i], P.part_neg[i]};
+  std::vector<int32_t> csize((size_t)P.C);
+  for (int32_t c = 0; c < P.C; ++c) csize[(size_t)c] = P.comm_off[(size_t)c + 1] - P.comm_off[(size_t)c];
+  if ((e = upload(&g->d_tiles, P.tiles)) != cudaSuccess) return bail(e, "tiles");
+  if ((e = upload(&g->d_order, P.tile_order)) != cudaSuccess) return bail(e, "order");
+  if ((e = upload(&g->d_parts, parts)) != cudaSuccess) return bail(e, "parts");
+  {
+    std::vector<uint2> ch(P.chunks.size());
+    for (size_t i = 0; i < ch.size(); ++i) ch[i] = make_uint2(P.chunks[i].ofs, P.chunks[i].ng);
+    if ((e = upload(&g->d_chunks, ch)) != cudaSuccess) return bail(e, "chunks");
+  }
+  {
+    const size_t bytes = sizeof(Unit) * P.pool.size();
+    if ((e = cudaMalloc((void**)&g->d_pool, bytes)) != cudaSuccess) return bail(e, "pool");
+    if ((e = cudaMemcpy(g->d_pool, P.pool.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+      return bail(e, "pool copy");
+    std::vector<Unit>().swap(P.pool);
+  }
+  if ((e = upload(&g->d_comm_tile0, P.comm_tile0)) != cudaSuccess) return bail(e, "comm_tile0");
+  if ((e = upload(&g->d_D_ptr, P.D_ptr)) != cudaSuccess) return bail(e, "D_ptr");
+  if ((e = upload(&g->d_D_idx, P.D_idx)) != cudaSuccess) return bail(e, "D_idx");
+  if ((e = upload(&g->d_csize, csize)) != cudaSuccess) return bail(e, "comm sizes");
+  if ((e = upload(&g->d_perm, P.perm)) != cudaSuccess) return bail(e, "perm");
+  const size_t zbytes = sizeof(double2) * (size_t)g->n_pad;
+  if ((e = cudaMalloc((void**)&g->zA, zbytes)) != cudaSuccess) return bail(e, "zA");
+  if ((e = cudaMalloc((void**)&g->zB, zbytes)) != cudaSuccess) return bail(e, "zB");
+  if ((e = cudaMemset(g->zA, 0, zbytes)) != cudaSuccess) return bail(e, "zA");
+  if ((e = cudaMemset(g->zB, 0, zbytes)) != cudaSuccess) return bail(e, "zB");
+  const size_t cb = sizeof(double2) * (size_t)std::max<int32_t>(P.C, 1);
+  if ((e = cudaMalloc((void**)&g->TA, cb)) != cudaSuccess) return bail(e, "TA");
+  if ((e = cudaMalloc((void**)&g->TB, cb)) != cudaSuccess) return bail(e, "TB");
+  if ((e = cudaMalloc((void**)&g->S, cb)) != cudaSuccess) return bail(e, "S");
+  const int32_t ntiles_all = P.comm_tile0[(size_t)P.C];
+  if ((e = cudaMalloc((void**)&g->partial, sizeof(double2) * (size_t)std::max<int32_t>(ntiles_all, 1))) != cudaSuccess)
+    return bail(e, "partial");
+  if ((e = cudaMalloc((void**)&g->acc, sizeof(double) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess)
+    return bail(e, "acc");
+  if ((e = cudaMalloc((void**)&g->ctrl, sizeof(Ctrl))) != cudaSuccess) return bail(e, "ctrl");
+  if ((e = cudaMemset(g->ctrl, 0, sizeof(Ctrl))) != cudaSuccess) return bail(e, "ctrl");
+  if ((e = cudaMemset(g->TA, 0, cb)) != cudaSuccess) return bail(e, "TA");
+  if ((e = cudaMemset(g->TB, 0, cb)) != cudaSuccess) return bail(e, "TB");
+  if ((e = cudaMemset(g->S, 0, cb)) != cudaSuccess) return bail(e, "S");
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "build sync");
+
+  DevPlan& dp = g->dp;
+  dp.n = P.n;
+  dp.C = P.C;
+  dp.rpt = P.rpt;
+  dp.cpt = P.chunks_per_tile;
+  dp.ntiles = (int32_t)P.tiles.size();
+  dp.tile_base = P.tile_begin;
+  dp.row_begin = (int32_t)P.row_begin;
+  dp.world = world;
+  dp.tiles = g->d_tiles;
+  dp.order = g->d_order;
+  dp.parts = g->d_parts;
+  dp.chunks = g->d_chunks;
+  dp.pool = g->d_pool;
+  dp.comm_tile0 = g->d_comm_tile0;
+  dp.D_ptr = g->d_D_ptr;
+  dp.D_idx = g->d_D_idx;
+  dp.comm_size = g->d_csize;
+  dp.perm = g->d_perm;
+  dp.partial = g->partial;
+  dp.S = g->S;
+  dp.ctrl = g->ctrl;
+
+  kur_graph_info_t& I = g->info;
+  I.n = P.n;
+  I.n_comm = P.C;
+  I.rank = rank;
+  I.world = world;
+  I.device = device;
+  I.rows_per_tile = P.rows_per_tile;
+  I.row_begin = P.row_begin;
+  I.row_end = P.row_end;
+  I.nnz = P.nnz;
+  I.n_idx_hot = P.n_idx_hot;
+  I.n_idx_remote = P.n_idx_remote;
+  I.n_idx = P.n_idx_hot + P.n_idx_remote;
+  I.n_slots_hot = P.n_slots_hot;
+  I.n_slots_remote = P.n_slots_remote;
+  I.n_dense_blocks = P.n_dense_blocks;
+  I.n_sparse_blocks = P.n_sparse_blocks;
+  I.n_tiles = (int64_t)P.tiles.size();
+  I.n_hot_parts = P.n_hot_parts;
+  I.sincos_per_rhs = g->n_local;
+  // algorithmic bytes of one fused RK stage (= one RHS evaluation), DESIGN.md §5:
+  // index stream (2 B per hot entry, 4 B per remote entry, no padding) plus per
+  // local row z_in 16 + z_out 16 + omega 8 + theta_n 8 + acc 16 = 64 B.
+  I.bytes_per_rhs = 2 * P.n_idx_hot + 4 * P.n_idx_remote + 64 * g->n_local;
+  I.bytes_pool = (int64_t)(sizeof(Unit) * (size_t)std::max<int64_t>(
+                                              (int64_t)(P.n_slots_hot / 8 + P.n_slots_remote / 4), 1));
+  I.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = g;
+  return KUR_OK;
+}
+
+kur_status kur_graph_destroy(kur_graph* g) {
+  if (!g) return fail(KUR_ERR_INVALID_ARG, "graph is NULL");
+  delete g;
+  return KUR_OK;
+}
+
+kur_status kur_graph_info(const kur_graph* g, kur_graph_info_t* info) {
+  if (!g || !info) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  *info = g->info;
+  return KUR_OK;
+}
+
+kur_status kur_graph_permutation(const kur_graph* g, int32_t* perm) {
+  if (!g || !perm) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  std::memcpy(perm, g->perm_host.data(), sizeof(int32_t) * g->perm_host.size());
+  return KUR_OK;
+}
+
+kur_status kur_permute(const kur_graph* g, const double* in, double* out, int32_t dir, void* stream) {
+  if (!g || !in || !out) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  if (in == out) return fail(KUR_ERR_INVALID_ARG, "in and out must differ");
+  if (dir != KUR_USER_TO_INTERNAL && dir != KUR_INTERNAL_TO_USER) return fail(KUR_ERR_INVALID_ARG, "bad dir");
+  KUR_CUDA(cudaSetDevice(g->device));
+  KUR_CUDA(launch_permute(g->d_perm, g->n, in, out, dir, (cudaStream_t)stream));
+  return KUR_OK;
+}
+
+kur_status kur_rhs(kur_graph* g, const double* theta, const double* omega, double K, double* dtheta,
+                   void* stream) {
+  if (!g || !theta || !omega || !dtheta) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
+  KUR_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  StageArgs a{};
+  a.theta = const_cast<double*>(theta);
+  a.omega = omega;
+  a.out = dtheta;
+  a.zout = g->zA;
+  a.Tout = g->TA;
+  a.KN = K / (double)g->n;
+  a.record = REC_NONE;
+  KUR_CUDA(launch_prologue(g->dp, a, s));
+  a.zin = g->zA;
+  a.Tin = g->TA;
+  a.zout = nullptr;
+  a.Tout = nullptr;
+  KUR_CUDA(launch_stage(MODE_RHS, g->dp, a, s));
+  return KUR_OK;
+}
+
+kur_status kur_step(kur_graph* g, double* theta, const double* omega, double K, double h, int64_t nsteps,
+                    int32_t record_every, double* r_trace, void* stream) {
+  if (!g || !theta || !omega) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
+  if (!(h > 0.0) || !std::isfinite(h)) return fail(KUR_ERR_INVALID_ARG, "h must be finite and > 0");
+  if (nsteps < 0) return fail(KUR_ERR_INVALID_ARG, "nsteps must be >= 0");
+  if (record_every < 0) return fail(KUR_ERR_INVALID_ARG, "record_every must be >= 0");
+  KUR_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool rec = record_every > 0 && r_trace;
+  const int64_t cap = rec ? nsteps / record_every + 1 : 0;
+  KUR_CUDA(launch_set_ctrl(g->ctrl, rec ? record_every : 0, (int)cap, rec ? r_trace : nullptr, s));
+  StageArgs a{};
+  a.theta = theta;
+  a.omega = omega;
+  a.acc = g->acc;
+  a.KN = K / (double)g->n;
+  a.h = h;
+  a.zout = g->zA;
+  a.Tout = g->TA;
+  a.record = REC_START;
+  KUR_CUDA(launch_prologue(g->dp, a, s));
+  for (int64_t n = 0; n < nsteps; ++n) {
+    for (int st = MODE_S1; st <= MODE_S4; ++st) {
+      const bool even = (st == MODE_S1 || st == MODE_S3);
+      a.zin = even ? g->zA : g->zB;
+      a.zout = even ? g->zB : g->zA;
+      a.Tin = even ? g->TA : g->TB;
+      a.Tout = even ? g->TB : g->TA;
+      a.record = st == MODE_S4 ? REC_STEP : REC_NONE;
+      KUR_CUDA(launch_stage(st, g->dp, a, s));
+    }
+  }
+  return KUR_OK;
+}
+
+kur_status kur_order_parameter(kur_graph* g, const double* theta, double* r_psi, double* local, void* stream) {
+  if (!g || !theta || !r_psi) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  KUR_CUDA(cudaSetDevice(g->device));
+  StageArgs a{};
+  a.theta = const_cast<double*>(theta);
+  a.zout = g->zA;
+  a.Tout = g->TA;
+  a.op_rpsi = r_psi;
+  a.op_local = local;
+  a.record = REC_NONE;
+  KUR_CUDA(launch_prologue(g->dp, a, (cudaStream_t)stream));
+  return KUR_OK;
+}
+
+kur_status kur_check(kur_graph* g, void* stream) {
+  if (!g) return fail(KUR_ERR_INVALID_ARG, "graph is NULL");
+  KUR_CUDA(cudaSetDevice(g->device));
+  KUR_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  int flag = 0;
+  KUR_CUDA(cudaMemcpy(&flag, &g->ctrl->nonfinite, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) {
+    const int zero = 0;
+    KUR_CUDA(cudaMemcpy(&g->ctrl->nonfinite, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    return fail(KUR_ERR_NONFINITE, "kur_step produced a non-finite phase");
+  }
+  return KUR_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- host-only plan introspection
+struct kur_plan {
+  HostPlan P;
+};
+
+extern "C" {
+
+kur_status kur_plan_build(const kur_graph_desc* desc, int32_t rank, int32_t world, int32_t sm_count,
+                          kur_plan** out) {
+  if (!out) return fail(KUR_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  kur_plan* p = new (std::nothrow) kur_plan();
+  if (!p) return fail(KUR_ERR_OOM, "host allocation failed");
+  std::string err;
+  kur_status st;
+  try {
+    st = build_plan(desc, rank, world, sm_count > 0 ? sm_count : 148, p->P, err);
+  } catch (const std::bad_alloc&) {
+    delete p;
+    return fail(KUR_ERR_OOM, "host allocation failed in kur_plan_build");
+  }
+  if (st != KUR_OK) {
+    delete p;
+    return fail(st, err);
+  }
+  *out = p;
+  return KUR_OK;
+}
+
+kur_status kur_plan_sizes(const kur_plan* p, int64_t* sizes) {
+  if (!p || !sizes) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  const HostPlan& P = p->P;
+  sizes[0] = P.n;
+  sizes[1] = P.C;
+  sizes[2] = P.row_end - P.row_begin;
+  sizes[3] = P.row_begin;
+  sizes[4] = P.n_idx_hot + P.n_idx_remote;
+  sizes[5] = (int64_t)P.D_idx.size();
+  sizes[6] = (int64_t)P.tiles.size();
+  sizes[7] = P.rows_per_tile;
+  sizes[8] = P.nnz;
+  sizes[9] = P.world;
+  return KUR_OK;
+}
+
+kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int32_t* D_idx, int64_t* row_ptr,
+                           int32_t* cols, int8_t* neg, int32_t* shard_row0) {
+  if (!p) return fail(KUR_ERR_INVALID_ARG, "NULL plan");
+  const HostPlan& P = p->P;
+  if (perm) std::memcpy(perm, P.perm.data(), sizeof(int32_t) * P.perm.size());
+  if (D_ptr) std::memcpy(D_ptr, P.D_ptr.data(), sizeof(int32_t) * P.D_ptr.size());
+  if (D_idx && !P.D_idx.empty()) std::memcpy(D_idx, P.D_idx.data(), sizeof(int32_t) * P.D_idx.size());
+  if (shard_row0) std::memcpy(shard_row0, P.shard_row0.data(), sizeof(int32_t) * P.shard_row0.size());
+  if (!row_ptr) return KUR_OK;
+  // decode the chunked layout exactly as the kernels read it
+  const int64_t nl = P.row_end - P.row_begin;
+  struct E { int32_t row, col; int8_t neg; };
+  std::vector<E> ents;
+  for (const TileDesc& T : P.tiles) {
+    for (int h = 0; h < T.nhot + T.nremote; ++h) {
+      const int part = T.part0 + h;
+      const int32_t w = P.part_window[(size_t)part];
+      const bool hot = h < T.nhot;
+      if (hot != (w >= 0)) return fail(KUR_ERR_INVALID_ARG, "plan: part kind mismatch");
+      for (int c = 0; c < P.chunks_per_tile; ++c) {
+        const ChunkDesc cd = P.chunks[(size_t)part * P.chunks_per_tile + (size_t)c];
+        for (uint32_t g = 0; g < cd.ng; ++g) {
+          for (int l = 0; l < 32; ++l) {
+            const Unit& U = P.pool[(size_t)cd.ofs + (size_t)g * 32 + (size_t)l];
+            const int lr = c * 32 + l;
+            const int nper = hot ? 8 : 4;
+            for (int q = 0; q < nper; ++q) {
+              int64_t col;
+              if (hot) {
+                const uint32_t e = (q & 1) ? (U.w[q >> 1] >> 16) : (U.w[q >> 1] & 0xFFFFu);
+                if (e == HOT_SENT) continue;
+                if (e > HOT_SENT) return fail(KUR_ERR_INVALID_ARG, "plan: hot index out of window");
+                col = (int64_t)w * WZ + e;
+              } else {
+                const uint32_t e = U.w[q];
+                if (e == (uint32_t)P.n) continue;
+                col = e;
+              }
+              if (lr >= T.nrows) return fail(KUR_ERR_INVALID_ARG, "plan: entry in an empty lane");
+              if (col < 0 || col >= P.n) return fail(KUR_ERR_INVALID_ARG, "plan: column out of range");
+              ents.push_back(E{(int32_t)(T.row0 + lr - P.row_begin), (int32_t)col, (int8_t)P.part_neg[(size_t)part]});
+            }
+          }
+        }
+      }
+    }
+  }
+  std::vector<int64_t> cnt((size_t)nl + 1, 0);
+  for (const E& e : ents) cnt[(size_t)e.row + 1]++;
+  for (int64_t i = 0; i < nl; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
+  std::memcpy(row_ptr, cnt.data(), sizeof(int64_t) * (size_t)(nl + 1));
+  std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+  for (const E& e : ents) {
+    const int64_t at = fill[(size_t)e.row]++;
+    if (cols) cols[at] = e.col;
+    if (neg) neg[at] = e.neg;
+  }
+  return KUR_OK;
+}
+
+kur_status kur_plan_destroy(kur_plan* p) {
+  delete p;
+  return KUR_OK;
+}
+
+}  // extern "C"

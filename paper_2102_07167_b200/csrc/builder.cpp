@@ -1,0 +1,506 @@
+// builder.cpp — host-side block builder behind kur_graph_build (product code).
+//
+// Steps:
+//  1. validate the row-segmented pattern (error conventions of include/kur.h);
+//  2. per block (row community a x column community b) count the ones over
+//     the off-diagonal entries and decide DENSE iff zeros < ones (P:96, P:14,
+//     P:538-544; tie -> SPARSE, reading R3) or the caller's threshold;
+//     D(a) = dense column communities of a (block sums precomputed);
+//  3. internal numbering = communities contiguous, rows of a
+//     community by decreasing list length;
+//  4. cut community-aligned tiles, pick hot windows per tile, emit the
+//     complement lists Z_j (dense blocks, subtracted) and the
+//     non-zero lists NZ_j (sparse blocks, added) in the chunked
+//     16-bit / 32-bit layout of plan.h.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <omp.h>
+
+#include "plan.h"
+
+namespace kur {
+namespace {
+
+struct Err {
+  std::mutex mu;
+  int64_t where = INT64_MAX;
+  kur_status st = KUR_OK;
+  std::string msg;
+  void set(int64_t w, kur_status s, const std::string& m) {
+    std::lock_guard<std::mutex> g(mu);
+    if (w < where) { where = w; st = s; msg = m; }
+  }
+};
+
+struct Src {  // the caller's description plus derived community data
+  const kur_graph_desc* d;
+  int64_t n;
+  int32_t C;
+  std::vector<int64_t> moff;   // members offsets [C+1]
+  std::vector<int32_t> mem;    // members (ascending user id)
+  std::vector<int64_t> csize;  // community sizes
+  std::vector<uint8_t> dense;  // only via D lists; per-community bitmap built on demand
+};
+
+inline bool has_diag(const int32_t* lst, int64_t len, int32_t u) {
+  return std::binary_search(lst, lst + len, u);
+}
+
+// Enumerate the stored entries of user row u (community a) after the
+// dense/sparse decision: cb(user_col, neg) with neg = 1 for complement
+// (subtracted) entries and 0 for non-zero entries.  Segment order, ascending
+// within a segment.
+template <class F>
+void enumerate_row(const Src& S, const std::vector<int32_t>& D_ptr, const std::vector<int32_t>& D_idx,
+                   int32_t u, F cb) {
+  const kur_graph_desc* d = S.d;
+  const int32_t a = d->community[u];
+  int64_t s = d->seg_ptr[u];
+  const int64_t s1 = d->seg_ptr[u + 1];
+  int32_t di = D_ptr[a];
+  const int32_t d1 = D_ptr[a + 1];
+  while (s < s1 || di < d1) {
+    const int32_t bs = s < s1 ? d->seg_comm[s] : INT32_MAX;
+    const int32_t bd = di < d1 ? D_idx[di] : INT32_MAX;
+    const int32_t b = std::min(bs, bd);
+    const bool dense = (bd == b);
+    const bool seg = (bs == b);
+    const int32_t* lst = seg ? d->idx + d->idx_ptr[s] : nullptr;
+    const int64_t len = seg ? d->idx_ptr[s + 1] - d->idx_ptr[s] : 0;
+    const int kind = seg ? d->seg_kind[s] : -1;
+    const int32_t* m = S.mem.data() + S.moff[b];
+    const int64_t nm = S.moff[b + 1] - S.moff[b];
+    auto complement = [&](int neg) {  // members of b minus lst minus u
+      int64_t z = 0;
+      for (int64_t e = 0; e < nm; ++e) {
+        const int32_t k = m[e];
+        while (z < len && lst[z] < k) ++z;
+        if (z < len && lst[z] == k) continue;
+        if (k != u) cb(k, neg);
+      }
+    };
+    if (dense) {
+      if (seg && kind == KUR_ZEROS) {
+        for (int64_t e = 0; e < len; ++e) if (lst[e] != u) cb(lst[e], 1);
+      } else {
+        complement(1);  // ONES segment or no segment: zeros = complement
+      }
+    } else if (seg) {
+      if (kind == KUR_ONES) {
+        for (int64_t e = 0; e < len; ++e) if (lst[e] != u) cb(lst[e], 0);
+      } else {
+        complement(0);
+      }
+    }
+    if (seg) ++s;
+    if (dense) ++di;
+  }
+}
+
+}  // namespace
+
+kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int sm_count,
+                      HostPlan& P, std::string& err) {
+  // ------------------------------------------------------------ 1. validate
+  if (!d || d->n < 1 || d->n_comm < 1 || !d->community || !d->seg_ptr || !d->idx_ptr) {
+    err = "kur_graph_desc: n >= 1, n_comm >= 1 and non-NULL community/seg_ptr/idx_ptr required";
+    return KUR_ERR_INVALID_ARG;
+  }
+  if (d->n >= INT32_MAX - 2 * WZ) { err = "n too large for int32 internal ids"; return KUR_ERR_UNSUPPORTED; }
+  const int force_rpt = d->flags & 7;
+  if ((d->flags & ~7) || (force_rpt != 0 && force_rpt != 1 && force_rpt != 2 && force_rpt != 4)) {
+    err = "flags: only KUR_FLAG_RPT1/2/4 (1, 2, 4) are defined";
+    return KUR_ERR_INVALID_ARG;
+  }
+  const double thr = d->dense_threshold;
+  if (std::isnan(thr) || thr > 1.0) { err = "dense_threshold must be <= 1 (or < 0 for the paper rule)"; return KUR_ERR_INVALID_ARG; }
+  if (world < 1 || rank < 0 || rank >= world) { err = "bad rank/world"; return KUR_ERR_INVALID_ARG; }
+  const int64_t n = d->n;
+  const int32_t C = d->n_comm;
+  if (d->seg_ptr[0] != 0) { err = "seg_ptr[0] must be 0"; return KUR_ERR_SIZE_MISMATCH; }
+  const int64_t nseg = d->seg_ptr[n];
+  if (nseg < 0) { err = "seg_ptr[n] < 0"; return KUR_ERR_SIZE_MISMATCH; }
+  if (nseg > 0 && (!d->seg_comm || !d->seg_kind)) { err = "seg_comm/seg_kind NULL"; return KUR_ERR_INVALID_ARG; }
+  if (d->idx_ptr[0] != 0) { err = "idx_ptr[0] must be 0"; return KUR_ERR_SIZE_MISMATCH; }
+  if (d->idx_ptr[nseg] > 0 && !d->idx) { err = "idx NULL"; return KUR_ERR_INVALID_ARG; }
+  Err E;
+#pragma omp parallel for schedule(static)
+  for (int64_t u = 0; u < n; ++u) {
+    if (d->community[u] < 0 || d->community[u] >= C)
+      E.set(u, KUR_ERR_PARTITION, "community label of node " + std::to_string(u) + " outside [0, n_comm)");
+  }
+  if (E.st != KUR_OK) { err = E.msg; return E.st; }
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t u = 0; u < n; ++u) {
+    const int64_t s0 = d->seg_ptr[u], s1 = d->seg_ptr[u + 1];
+    if (s1 < s0 || s1 > nseg) { E.set(u, KUR_ERR_SIZE_MISMATCH, "seg_ptr not monotone at row " + std::to_string(u)); continue; }
+    int32_t pb = -1;
+    for (int64_t s = s0; s < s1; ++s) {
+      const int32_t b = d->seg_comm[s];
+      if (b < 0 || b >= C) { E.set(u, KUR_ERR_PARTITION, "seg_comm outside [0, n_comm) in row " + std::to_string(u)); break; }
+      if (b == pb) { E.set(u, KUR_ERR_DUPLICATE_INDEX, "community given two segments in row " + std::to_string(u)); break; }
+      if (b < pb) { E.set(u, KUR_ERR_INVALID_ARG, "seg_comm not increasing in row " + std::to_string(u)); break; }
+      pb = b;
+      if (d->seg_kind[s] > 1) { E.set(u, KUR_ERR_INVALID_ARG, "bad seg_kind in row " + std::to_string(u)); break; }
+      const int64_t i0 = d->idx_ptr[s], i1 = d->idx_ptr[s + 1];
+      if (i1 < i0) { E.set(u, KUR_ERR_SIZE_MISMATCH, "idx_ptr not monotone in row " + std::to_string(u)); break; }
+      int64_t pk = -1;
+      bool bad = false;
+      for (int64_t e = i0; e < i1; ++e) {
+        const int32_t k = d->idx[e];
+        if (k < 0 || k >= n) { E.set(u, KUR_ERR_INDEX_RANGE, "column id outside [0, n) in row " + std::to_string(u)); bad = true; break; }
+        if (d->community[k] != b) { E.set(u, KUR_ERR_PARTITION, "column outside its segment's community in row " + std::to_string(u)); bad = true; break; }
+        if (k == pk) { E.set(u, KUR_ERR_DUPLICATE_INDEX, "column listed twice in row " + std::to_string(u)); bad = true; break; }
+        if (k < pk) { E.set(u, KUR_ERR_INVALID_ARG, "segment list not ascending in row " + std::to_string(u)); bad = true; break; }
+        pk = k;
+      }
+      if (bad) break;
+    }
+  }
+  if (E.st != KUR_OK) { err = E.msg; return E.st; }
+
+  // ------------------------------------------------------------ communities
+  Src S;
+  S.d = d;
+  S.n = n;
+  S.C = C;
+  S.moff.assign((size_t)C + 1, 0);
+  for (int64_t u = 0; u < n; ++u) S.moff[(size_t)d->community[u] + 1]++;
+  for (int32_t c = 0; c < C; ++c) S.moff[(size_t)c + 1] += S.moff[(size_t)c];
+  S.csize.resize((size_t)C);
+  for (int32_t c = 0; c < C; ++c) S.csize[(size_t)c] = S.moff[(size_t)c + 1] - S.moff[(size_t)c];
+  S.mem.resize((size_t)n);
+  {
+    std::vector<int64_t> fill(S.moff.begin(), S.moff.end() - 1);
+    for (int64_t u = 0; u < n; ++u) S.mem[(size_t)fill[(size_t)d->community[u]]++] = (int32_t)u;
+  }
+
+  // ------------------------------------------------------------ 2. census + rule
+  std::vector<std::vector<int32_t>> Dl((size_t)C);
+  std::atomic<int64_t> nnz{0}, ndense{0}, nsparse{0};
+#pragma omp parallel
+  {
+    std::vector<int64_t> ones((size_t)C, 0);
+    std::vector<uint8_t> seen((size_t)C, 0);
+    std::vector<int32_t> touched;
+#pragma omp for schedule(dynamic, 1)
+    for (int32_t a = 0; a < C; ++a) {
+      touched.clear();
+      for (int64_t mi = S.moff[(size_t)a]; mi < S.moff[(size_t)a + 1]; ++mi) {
+        const int32_t u = S.mem[(size_t)mi];
+        for (int64_t s = d->seg_ptr[u]; s < d->seg_ptr[u + 1]; ++s) {
+          const int32_t b = d->seg_comm[s];
+          const int32_t* lst = d->idx + d->idx_ptr[s];
+          const int64_t len = d->idx_ptr[s + 1] - d->idx_ptr[s];
+          const int64_t lnd = len - ((b == a && has_diag(lst, len, u)) ? 1 : 0);
+          const int64_t o = d->seg_kind[s] == KUR_ONES ? lnd : S.csize[(size_t)b] - (b == a ? 1 : 0) - lnd;
+          if (!seen[(size_t)b]) { seen[(size_t)b] = 1; touched.push_back(b); }
+          ones[(size_t)b] += o;
+        }
+      }
+      std::sort(touched.begin(), touched.end());
+      int64_t lnnz = 0, ld = 0, ls = 0;
+      for (int32_t b : touched) {
+        const int64_t na = S.csize[(size_t)a], nb = S.csize[(size_t)b];
+        const int64_t total = na * nb - (a == b ? na : 0);
+        const int64_t o = ones[(size_t)b];
+        const int64_t z = total - o;
+        bool dense;
+        if (thr < 0) dense = z < o;  // paper rule P:96 (tie -> sparse)
+        else dense = (double)z < thr * (double)total;
+        if (total == 0) dense = false;
+        if (dense) { Dl[(size_t)a].push_back(b); ++ld; }
+        else if (o > 0) ++ls;
+        lnnz += o;
+        ones[(size_t)b] = 0;
+        seen[(size_t)b] = 0;
+      }
+      nnz += lnnz;
+      ndense += ld;
+      nsparse += ls;
+    }
+  }
+  P.D_ptr.assign((size_t)C + 1, 0);
+  for (int32_t a = 0; a < C; ++a) P.D_ptr[(size_t)a + 1] = P.D_ptr[(size_t)a] + (int32_t)Dl[(size_t)a].size();
+  P.D_idx.clear();
+  for (int32_t a = 0; a < C; ++a) P.D_idx.insert(P.D_idx.end(), Dl[(size_t)a].begin(), Dl[(size_t)a].end());
+
+  // ------------------------------------------------------------ 3. lengths + order
+  std::vector<int64_t> rlen((size_t)n, 0);
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t u = 0; u < n; ++u) {
+    const int32_t a = d->community[u];
+    int64_t s = d->seg_ptr[u];
+    const int64_t s1 = d->seg_ptr[u + 1];
+    int32_t di = P.D_ptr[(size_t)a];
+    const int32_t d1 = P.D_ptr[(size_t)a + 1];
+    int64_t L = 0;
+    while (s < s1 || di < d1) {
+      const int32_t bs = s < s1 ? d->seg_comm[s] : INT32_MAX;
+      const int32_t bd = di < d1 ? P.D_idx[(size_t)di] : INT32_MAX;
+      const int32_t b = std::min(bs, bd);
+      const bool dense = bd == b, seg = bs == b;
+      const int64_t nb_off = S.csize[(size_t)b] - (b == a ? 1 : 0);
+      int64_t lnd = 0;
+      int kind = -1;
+      if (seg) {
+        const int32_t* lst = d->idx + d->idx_ptr[s];
+        const int64_t len = d->idx_ptr[s + 1] - d->idx_ptr[s];
+        lnd = len - ((b == a && has_diag(lst, len, (int32_t)u)) ? 1 : 0);
+        kind = d->seg_kind[s];
+      }
+      if (dense) L += (seg && kind == KUR_ZEROS) ? lnd : nb_off - lnd;
+      else if (seg) L += kind == KUR_ONES ? lnd : nb_off - lnd;
+      if (seg) ++s;
+      if (dense) ++di;
+    }
+    rlen[(size_t)u] = L;
+  }
+  P.n = n;
+  P.C = C;
+  P.rank = rank;
+  P.world = world;
+  P.nnz = nnz.load();
+  P.n_dense_blocks = ndense.load();
+  P.n_sparse_blocks = nsparse.load();
+  P.perm.resize((size_t)n);
+  P.comm_off.assign((size_t)C + 1, 0);
+  for (int32_t c = 0; c <= C; ++c) P.comm_off[(size_t)c] = (int32_t)S.moff[(size_t)c];
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int32_t a = 0; a < C; ++a) {
+    int32_t* p = P.perm.data() + S.moff[(size_t)a];
+    const int64_t na = S.csize[(size_t)a];
+    std::copy(S.mem.begin() + S.moff[(size_t)a], S.mem.begin() + S.moff[(size_t)a + 1], p);
+    std::stable_sort(p, p + na, [&](int32_t x, int32_t y) { return rlen[(size_t)x] > rlen[(size_t)y]; });
+  }
+  std::vector<int32_t> inv((size_t)n);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) inv[(size_t)P.perm[(size_t)i]] = (int32_t)i;
+
+  // ------------------------------------------------------------ 4. tiles
+  // rows per thread: the largest rpt keeping >= 4 CTAs per SM worth of tiles
+  int rpt = force_rpt ? force_rpt : 1;
+  for (int r = MAX_RPT; r >= 1 && !force_rpt; r >>= 1) {
+    int64_t nt = 0;
+    for (int32_t c = 0; c < C; ++c) nt += (S.csize[(size_t)c] + 512 * r - 1) / (512 * r);
+    if (nt >= 4LL * sm_count || r == 1) { rpt = r; break; }
+  }
+  P.rpt = rpt;
+  P.rows_per_tile = NTHREADS * rpt;
+  P.chunks_per_tile = NWARPS * rpt;
+  const int RT = P.rows_per_tile, CPT = P.chunks_per_tile;
+  std::vector<TileDesc> all;
+  P.comm_tile0.assign((size_t)C + 1, 0);
+  for (int32_t c = 0; c < C; ++c) {
+    P.comm_tile0[(size_t)c] = (int32_t)all.size();
+    for (int64_t r0 = S.moff[(size_t)c]; r0 < S.moff[(size_t)c + 1]; r0 += RT) {
+      TileDesc t{};
+      t.row0 = (int32_t)r0;
+      t.nrows = (int32_t)std::min<int64_t>(RT, S.moff[(size_t)c + 1] - r0);
+      t.comm = c;
+      all.push_back(t);
+    }
+  }
+  P.comm_tile0[(size_t)C] = (int32_t)all.size();
+  const int64_t ntiles_all = (int64_t)all.size();
+  // per-tile work estimate (entries), then shards of whole communities
+  std::vector<int64_t> twork((size_t)ntiles_all, 0);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < ntiles_all; ++t) {
+    int64_t w = 0;
+    for (int32_t r = 0; r < all[(size_t)t].nrows; ++r) w += rlen[(size_t)P.perm[(size_t)(all[(size_t)t].row0 + r)]] + 8;
+    twork[(size_t)t] = w;
+  }
+  std::vector<int64_t> cwork((size_t)C, 0);
+  for (int32_t c = 0; c < C; ++c)
+    for (int32_t t = P.comm_tile0[(size_t)c]; t < P.comm_tile0[(size_t)c + 1]; ++t) cwork[(size_t)c] += twork[(size_t)t];
+  std::vector<int32_t> comm_b((size_t)world + 1, 0);
+  {
+    const double totw = (double)std::accumulate(cwork.begin(), cwork.end(), (int64_t)0);
+    int64_t acc = 0;
+    int32_t c = 0;
+    for (int32_t r = 1; r < world; ++r) {
+      const double target = totw * r / world;
+      while (c < C && (double)(acc + cwork[(size_t)c] / 2) < target) acc += cwork[(size_t)c++];
+      comm_b[(size_t)r] = std::max(c, comm_b[(size_t)r - 1]);
+    }
+    comm_b[(size_t)world] = C;
+  }
+  P.shard_row0.resize((size_t)world + 1);
+  P.shard_tile0.resize((size_t)world + 1);
+  for (int32_t r = 0; r <= world; ++r) {
+    P.shard_row0[(size_t)r] = P.comm_off[(size_t)comm_b[(size_t)r]];
+    P.shard_tile0[(size_t)r] = P.comm_tile0[(size_t)comm_b[(size_t)r]];
+  }
+  P.comm_begin = comm_b[(size_t)rank];
+  P.comm_end = comm_b[(size_t)rank + 1];
+  P.row_begin = P.shard_row0[(size_t)rank];
+  P.row_end = P.shard_row0[(size_t)rank + 1];
+  P.tile_begin = P.shard_tile0[(size_t)rank];
+  P.tile_end = P.shard_tile0[(size_t)rank + 1];
+  const int32_t nt = P.tile_end - P.tile_begin;
+
+  // ------------------------------------------------------------ 5. layout
+  // key = window<<44 | neg<<43 | local_row<<32 | internal column
+  const int64_t hot_min = d->hot_min > 0 ? d->hot_min : DEFAULT_HOT_MIN;
+  const uint32_t SENT_REMOTE = (uint32_t)n;  // z[n] is kept zero
+  constexpr uint64_t COLM = 0x7FFFFFFFULL;
+  struct TileOut {
+    std::vector<Unit> units;
+    std::vector<int32_t> windows, negs;  // per part (window -1 = remote)
+    std::vector<ChunkDesc> chunks;       // per part x CPT (ofs relative to the tile)
+    int32_t nhot = 0, nremote = 0;
+    int64_t hot = 0, rem = 0, shot = 0, srem = 0;
+  };
+  std::vector<TileOut> outs((size_t)nt);
+#pragma omp parallel
+  {
+    std::vector<uint64_t> keys, remk;
+    std::vector<int32_t> cnt;
+    std::vector<size_t> rb;
+#pragma omp for schedule(dynamic, 1)
+    for (int32_t lt = 0; lt < nt; ++lt) {
+      const TileDesc& T = all[(size_t)(P.tile_begin + lt)];
+      TileOut& O = outs[(size_t)lt];
+      keys.clear();
+      for (int32_t lr = 0; lr < T.nrows; ++lr) {
+        const int32_t u = P.perm[(size_t)(T.row0 + lr)];
+        enumerate_row(S, P.D_ptr, P.D_idx, u, [&](int32_t k, int neg) {
+          const uint64_t c = (uint64_t)(uint32_t)inv[(size_t)k];
+          keys.push_back(((c >> WZ_SHIFT) << 44) | ((uint64_t)neg << 43) | ((uint64_t)lr << 32) | c);
+        });
+      }
+      std::sort(keys.begin(), keys.end());
+      // one part = entries src[k0..k1) of one (window|remote, sign), sorted by (row, column)
+      auto emit_part = [&](int32_t window, int32_t neg, const uint64_t* src, size_t k0, size_t k1) {
+        const bool hot = window >= 0;
+        const int E = hot ? 8 : 4;
+        const int32_t part = (int32_t)O.windows.size();
+        O.windows.push_back(window);
+        O.negs.push_back(neg);
+        O.chunks.resize((size_t)(part + 1) * CPT, ChunkDesc{0, 0});
+        cnt.assign((size_t)RT, 0);
+        for (size_t k = k0; k < k1; ++k) cnt[(size_t)((src[k] >> 32) & 0x7FF)]++;
+        rb.assign((size_t)RT + 1, 0);
+        for (int r = 0; r < RT; ++r) rb[(size_t)r + 1] = rb[(size_t)r] + (size_t)cnt[(size_t)r];
+        for (int c = 0; c < CPT; ++c) {
+          int mx = 0;
+          for (int l = 0; l < 32; ++l) mx = std::max(mx, cnt[(size_t)(c * 32 + l)]);
+          const uint32_t ng = (uint32_t)((mx + E - 1) / E);
+          ChunkDesc& cd = O.chunks[(size_t)part * CPT + c];
+          cd.ofs = (uint32_t)O.units.size();
+          cd.ng = ng;
+          const size_t u0 = O.units.size();
+          O.units.resize(u0 + (size_t)ng * 32);
+          for (uint32_t g = 0; g < ng; ++g) {
+            for (int l = 0; l < 32; ++l) {
+              const int r = c * 32 + l;
+              Unit& U = O.units[u0 + (size_t)g * 32 + (size_t)l];
+              if (hot) {
+                uint16_t v[8];
+                for (int q = 0; q < 8; ++q) {
+                  const int e = (int)g * 8 + q;
+                  v[q] = e < cnt[(size_t)r]
+                             ? (uint16_t)((src[k0 + rb[(size_t)r] + (size_t)e] & COLM) - (uint64_t)window * WZ)
+                             : (uint16_t)HOT_SENT;
+                }
+                std::memcpy(U.w, v, 16);
+              } else {
+                for (int q = 0; q < 4; ++q) {
+                  const int e = (int)g * 4 + q;
+                  U.w[q] = e < cnt[(size_t)r] ? (uint32_t)(src[k0 + rb[(size_t)r] + (size_t)e] & COLM) : SENT_REMOTE;
+                }
+              }
+            }
+          }
+          if (hot) O.shot += (int64_t)ng * 256; else O.srem += (int64_t)ng * 128;
+        }
+        if (hot) O.hot += (int64_t)(k1 - k0); else O.rem += (int64_t)(k1 - k0);
+      };
+      remk.clear();
+      size_t i = 0;
+      while (i < keys.size()) {
+        const uint64_t w = keys[i] >> 44;
+        size_t j = i;
+        while (j < keys.size() && (keys[j] >> 44) == w) ++j;
+        if ((int64_t)(j - i) >= hot_min) {
+          size_t m = i;  // split by sign (bit 43): non-zeros first, then complements
+          while (m < j && !((keys[m] >> 43) & 1)) ++m;
+          if (m > i) { emit_part((int32_t)w, 0, keys.data(), i, m); O.nhot++; }
+          if (j > m) { emit_part((int32_t)w, 1, keys.data(), m, j); O.nhot++; }
+        } else {
+          for (size_t k = i; k < j; ++k) remk.push_back(keys[k] & ((1ULL << 44) - 1));
+        }
+        i = j;
+      }
+      if (!remk.empty()) {
+        std::sort(remk.begin(), remk.end());  // (sign, row, column)
+        size_t m = 0;
+        while (m < remk.size() && !((remk[m] >> 43) & 1)) ++m;
+        if (m > 0) { emit_part(-1, 0, remk.data(), 0, m); O.nremote++; }
+        if (remk.size() > m) { emit_part(-1, 1, remk.data(), m, remk.size()); O.nremote++; }
+      }
+    }
+  }
+  // ------------------------------------------------------------ 6. concatenate
+  P.tiles.resize((size_t)nt);
+  int64_t units = 0, parts = 0;
+  for (int32_t lt = 0; lt < nt; ++lt) {
+    units += (int64_t)outs[(size_t)lt].units.size();
+    parts += (int64_t)outs[(size_t)lt].windows.size();
+  }
+  if (units >= (int64_t)UINT32_MAX) { err = "index pool exceeds 64 GB"; return KUR_ERR_UNSUPPORTED; }
+  P.pool.resize((size_t)std::max<int64_t>(units, 1));
+  P.part_window.assign((size_t)std::max<int64_t>(parts, 1), -1);
+  P.part_neg.assign((size_t)std::max<int64_t>(parts, 1), 0);
+  P.chunks.assign((size_t)std::max<int64_t>(parts, 1) * CPT, ChunkDesc{0, 0});
+  int64_t uo = 0, po = 0;
+  P.n_idx_hot = P.n_idx_remote = P.n_slots_hot = P.n_slots_remote = P.n_hot_parts = 0;
+  std::vector<int64_t> uofs((size_t)nt), pofs((size_t)nt);
+  for (int32_t lt = 0; lt < nt; ++lt) {
+    uofs[(size_t)lt] = uo;
+    pofs[(size_t)lt] = po;
+    const TileOut& O = outs[(size_t)lt];
+    TileDesc T = all[(size_t)(P.tile_begin + lt)];
+    T.part0 = (int32_t)po;
+    T.nhot = O.nhot;
+    T.nremote = O.nremote;
+    P.tiles[(size_t)lt] = T;
+    uo += (int64_t)O.units.size();
+    po += (int64_t)O.windows.size();
+    P.n_idx_hot += O.hot;
+    P.n_idx_remote += O.rem;
+    P.n_slots_hot += O.shot;
+    P.n_slots_remote += O.srem;
+    P.n_hot_parts += O.nhot;
+  }
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int32_t lt = 0; lt < nt; ++lt) {
+    TileOut& O = outs[(size_t)lt];
+    if (!O.units.empty()) std::memcpy(P.pool.data() + uofs[(size_t)lt], O.units.data(), O.units.size() * sizeof(Unit));
+    for (size_t p = 0; p < O.windows.size(); ++p) {
+      P.part_window[(size_t)pofs[(size_t)lt] + p] = O.windows[p];
+      P.part_neg[(size_t)pofs[(size_t)lt] + p] = O.negs[p];
+      for (int c = 0; c < CPT; ++c) {
+        ChunkDesc cd = O.chunks[p * CPT + (size_t)c];
+        if (cd.ng) cd.ofs += (uint32_t)uofs[(size_t)lt];
+        else cd.ofs = 0;
+        P.chunks[((size_t)pofs[(size_t)lt] + p) * CPT + (size_t)c] = cd;
+      }
+    }
+    std::vector<Unit>().swap(O.units);
+  }
+  // launch order: decreasing work (longest-processing-time first)
+  P.tile_order.resize((size_t)nt);
+  std::iota(P.tile_order.begin(), P.tile_order.end(), 0);
+  std::stable_sort(P.tile_order.begin(), P.tile_order.end(), [&](int32_t x, int32_t y) {
+    return twork[(size_t)(P.tile_begin + x)] > twork[(size_t)(P.tile_begin + y)];
+  });
+  return KUR_OK;
+}
+
+}  // namespace kur

@@ -1,0 +1,430 @@
+// kernels.cu — sm_100a fp64 kernels of the localised-order-parameter RHS and
+// the fused classical RK4 stages (product code).
+//
+// One CTA (16 warps, 512 threads) owns one community-aligned tile of
+// 512*RPT rows; lane l of warp w owns rows (w + 16 r)*32 + l.
+//
+//   k_prologue  z = e^{i theta} (= (cos, sin), P:443 / "2M" trig of P:660),
+//               per-tile partial sums of z; the last CTA reduces the partials
+//               to the block sums S_b, T_a = sum_{b in D(a)} S_b,
+//               and the order parameter r e^{i psi} = (1/N) sum_b S_b
+//               (P:236-239).
+//   k_stage     W_j = T_{c(j)} - sum_{Z_j} z_k + sum_{NZ_j} z_k:
+//               hot parts gather z from a 64 KB shared-memory window,
+//               remote parts from global memory; then
+//               k_j = omega_j + (K/N) Im(conj z_j W_j)
+//               and, fused, the RK4 stage update (acc, theta_next), the next
+//               stage's z and its per-tile partials; the last CTA forms the
+//               next S_b, T_a and (r, psi) exactly as k_prologue does.
+// All reductions are fixed-shape (no floating-point atomics): bitwise
+// reproducible run to run.
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace kur {
+namespace {
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void warp_sum2(double& x, double& y) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    x += __shfl_xor_sync(0xffffffffu, x, o);
+    y += __shfl_xor_sync(0xffffffffu, y, o);
+  }
+}
+
+// Fixed-shape block reduction of (x, y) over NTHREADS threads; result valid in warp 0.
+__device__ __forceinline__ void block_sum2(double& x, double& y, double2* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_sum2(x, y);
+  if (lane == 0) red[warp] = make_double2(x, y);
+  __syncthreads();
+  if (warp == 0) {
+    const double2 v = lane < NWARPS ? red[lane] : make_double2(0.0, 0.0);
+    x = v.x;
+    y = v.y;
+#pragma unroll
+    for (int o = NWARPS / 2; o > 0; o >>= 1) {
+      x += __shfl_xor_sync(0xffffffffu, x, o);
+      y += __shfl_xor_sync(0xffffffffu, y, o);
+    }
+  }
+}
+
+// Sum of the 8 window-local z entries named by one 16-byte unit (P:557-570:
+// complement or non-zero entries; the part's sign is applied by the caller).
+__device__ __forceinline__ void hot8(const uint4 v, const double2* zs, double& x0, double& y0,
+                                     double& x1, double& y1) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double2 a = zs[w[q] & 0xFFFFu];
+    const double2 b = zs[w[q] >> 16];
+    x0 += a.x;
+    y0 += a.y;
+    x1 += b.x;
+    y1 += b.y;
+  }
+}
+
+__device__ __forceinline__ void rem4(const uint4 v, const double2* __restrict__ z, double& x0,
+                                     double& y0, double& x1, double& y1) {
+  const double2 a = __ldg(z + v.x);
+  const double2 b = __ldg(z + v.y);
+  const double2 c = __ldg(z + v.z);
+  const double2 d = __ldg(z + v.w);
+  x0 += a.x;
+  y0 += a.y;
+  x1 += b.x;
+  y1 += b.y;
+  x0 += c.x;
+  y0 += c.y;
+  x1 += d.x;
+  y1 += d.y;
+}
+
+// Hot part of one chunk: ng groups of 32 units starting at q (lane-offset applied).
+__device__ __forceinline__ void run_hot(const uint4* __restrict__ q, uint32_t ng, const double2* zs,
+                                        double& sx, double& sy) {
+  double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
+  uint32_t g = 0;
+  for (; g + 4 <= ng; g += 4) {
+    const uint4 v0 = ldg_stream(q + (size_t)(g + 0) * 32);
+    const uint4 v1 = ldg_stream(q + (size_t)(g + 1) * 32);
+    const uint4 v2 = ldg_stream(q + (size_t)(g + 2) * 32);
+    const uint4 v3 = ldg_stream(q + (size_t)(g + 3) * 32);
+    hot8(v0, zs, x0, y0, x1, y1);
+    hot8(v1, zs, x0, y0, x1, y1);
+    hot8(v2, zs, x0, y0, x1, y1);
+    hot8(v3, zs, x0, y0, x1, y1);
+  }
+  for (; g < ng; ++g) hot8(ldg_stream(q + (size_t)g * 32), zs, x0, y0, x1, y1);
+  sx = x0 + x1;
+  sy = y0 + y1;
+}
+
+__device__ __forceinline__ void run_remote(const uint4* __restrict__ q, uint32_t ng,
+                                           const double2* __restrict__ z, double& sx, double& sy) {
+  double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
+  uint32_t g = 0;
+  for (; g + 2 <= ng; g += 2) {
+    const uint4 v0 = ldg_stream(q + (size_t)(g + 0) * 32);
+    const uint4 v1 = ldg_stream(q + (size_t)(g + 1) * 32);
+    rem4(v0, z, x0, y0, x1, y1);
+    rem4(v1, z, x0, y0, x1, y1);
+  }
+  for (; g < ng; ++g) rem4(ldg_stream(q + (size_t)g * 32), z, x0, y0, x1, y1);
+  sx = x0 + x1;
+  sy = y0 + y1;
+}
+
+// Executed by every thread of the LAST CTA of a grid: S_b from the per-tile
+// partials, T_a, the order parameter and its recording.
+__device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = warp; c < dp.C; c += NWARPS) {  // S_b = sum of its tiles' partials
+    const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
+    double x = 0.0, y = 0.0;
+    for (int t = t0 + lane; t < t1; t += 32) {
+      const double2 v = __ldcg(dp.partial + t);
+      x += v.x;
+      y += v.y;
+    }
+    warp_sum2(x, y);
+    if (lane == 0) dp.S[c] = make_double2(x, y);
+  }
+  __threadfence_block();
+  __syncthreads();
+  for (int c = tid; c < dp.C; c += NTHREADS) {  // T_a = sum over dense column communities
+    double x = 0.0, y = 0.0;
+    for (int i = dp.D_ptr[c]; i < dp.D_ptr[c + 1]; ++i) {
+      const double2 v = __ldcg(dp.S + dp.D_idx[i]);
+      x += v.x;
+      y += v.y;
+    }
+    a.Tout[c] = make_double2(x, y);
+    if (a.op_local) {  // localised order parameters S_b / n_b
+      const double2 v = __ldcg(dp.S + c);
+      const double nb = (double)dp.comm_size[c];
+      const double cx = nb > 0 ? v.x / nb : 0.0, cy = nb > 0 ? v.y / nb : 0.0;
+      const double r = sqrt(cx * cx + cy * cy);
+      a.op_local[2 * c] = r;
+      a.op_local[2 * c + 1] = r == 0.0 ? 0.0 : atan2(cy, cx);
+    }
+  }
+  if (warp == 0) {  // r e^{i psi} = (1/N) sum_b S_b
+    double x = 0.0, y = 0.0;
+    for (int c = lane; c < dp.C; c += 32) {
+      const double2 v = __ldcg(dp.S + c);
+      x += v.x;
+      y += v.y;
+    }
+    warp_sum2(x, y);
+    if (lane == 0) {
+      const double cm = x / (double)dp.n, sm = y / (double)dp.n;
+      const double r = sqrt(cm * cm + sm * sm);
+      const double psi = r == 0.0 ? 0.0 : atan2(sm, cm);
+      Ctrl* ct = dp.ctrl;
+      ct->rpsi[0] = r;
+      ct->rpsi[1] = psi;
+      if (a.op_rpsi) {
+        a.op_rpsi[0] = r;
+        a.op_rpsi[1] = psi;
+      }
+      if (a.record != REC_NONE) {
+        if (a.record == REC_START) ct->step = 0;
+        else ct->step += 1;
+        const long long nstep = ct->step;
+        if (ct->record_every > 0 && ct->r_trace && nstep % ct->record_every == 0) {
+          const long long i = nstep / ct->record_every;
+          if (i < ct->nrec_cap) {
+            ct->r_trace[2 * i] = r;
+            ct->r_trace[2 * i + 1] = psi;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Writes the tile partial, then lets the last CTA of the grid finish.
+__device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const StageArgs& a, int lt,
+                                                        double x, double y, double2* red) {
+  __shared__ bool s_last;
+  block_sum2(x, y, red);
+  if (threadIdx.x == 0) {
+    dp.partial[dp.tile_base + lt] = make_double2(x, y);
+    s_last = false;
+    if (dp.world == 1) {  // world > 1: the reduction runs after the exchange
+      __threadfence();
+      const unsigned int t = atomicAdd(&dp.ctrl->ticket, 1u);
+      s_last = (t == gridDim.x - 1);
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  finish_reduce(dp, a);
+  if (threadIdx.x == 0) dp.ctrl->ticket = 0;
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const StageArgs a) {
+  __shared__ double2 red[NWARPS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lt = dp.order[blockIdx.x];
+  const TileDesc T = dp.tiles[lt];
+  double x = 0.0, y = 0.0;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int lr = (warp + NWARPS * r) * 32 + lane;
+    if (lr < T.nrows) {
+      const int row = T.row0 + lr;
+      double s, c;
+      sincos(a.theta[row - dp.row_begin], &s, &c);
+      a.zout[row] = make_double2(c, s);
+      x += c;
+      y += s;
+    }
+  }
+  tile_partial_and_finish(dp, a, lt, x, y, red);
+}
+
+template <int MODE, int RPT>
+__global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const StageArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* zs = reinterpret_cast<double2*>(smem_raw);
+  __shared__ double2 red[NWARPS];
+  __shared__ int s_nonfinite;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lt = dp.order[blockIdx.x];
+  const TileDesc T = dp.tiles[lt];
+  if (tid == 0) {
+    zs[WZ] = make_double2(0.0, 0.0);  // sentinel slot of padded entries
+    s_nonfinite = 0;
+  }
+  double ax[RPT], ay[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) ax[r] = ay[r] = 0.0;
+
+  // ---- hot parts: z window staged in shared memory
+  int loaded = -1;
+  for (int h = 0; h < T.nhot; ++h) {
+    const int p = T.part0 + h;
+    const PartInfo pi = dp.parts[p];
+    if (pi.window != loaded) {
+      __syncthreads();
+      const double2* src = a.zin + (size_t)pi.window * WZ;
+#pragma unroll
+      for (int i = 0; i < WZ / NTHREADS; ++i) zs[tid + i * NTHREADS] = __ldg(src + tid + i * NTHREADS);
+      __syncthreads();
+      loaded = pi.window;
+    }
+    const uint2* ch = dp.chunks + (size_t)p * dp.cpt;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const uint2 c = ch[warp + NWARPS * r];
+      double sx, sy;
+      run_hot(dp.pool + c.x + lane, c.y, zs, sx, sy);
+      if (pi.neg) {
+        ax[r] -= sx;
+        ay[r] -= sy;
+      } else {
+        ax[r] += sx;
+        ay[r] += sy;
+      }
+    }
+  }
+  // ---- remote parts: z gathered from global memory (L2-resident)
+  for (int h = 0; h < T.nremote; ++h) {
+    const int p = T.part0 + T.nhot + h;
+    const PartInfo pi = dp.parts[p];
+    const uint2* ch = dp.chunks + (size_t)p * dp.cpt;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const uint2 c = ch[warp + NWARPS * r];
+      double sx, sy;
+      run_remote(dp.pool + c.x + lane, c.y, a.zin, sx, sy);
+      if (pi.neg) {
+        ax[r] -= sx;
+        ay[r] -= sy;
+      } else {
+        ax[r] += sx;
+        ay[r] += sy;
+      }
+    }
+  }
+
+  // ---- finalize: k_j = omega_j + (K/N) Im(conj z_j W_j), fused RK4 stage
+  const double2 Tc = a.Tin[T.comm];
+  double px = 0.0, py = 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int lr = (warp + NWARPS * r) * 32 + lane;
+    if (lr < T.nrows) {
+      const int row = T.row0 + lr;
+      const int li = row - dp.row_begin;
+      const double wx = Tc.x + ax[r], wy = Tc.y + ay[r];
+      const double2 zj = a.zin[row];
+      const double k = a.omega[li] + a.KN * (zj.x * wy - zj.y * wx);
+      if (MODE == MODE_RHS) {
+        a.out[li] = k;
+      } else {
+        const double thn = a.theta[li];
+        double ts;
+        if (MODE == MODE_S1) {
+          a.acc[li] = k;
+          ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
+        } else if (MODE == MODE_S2) {
+          a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
+          ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
+        } else if (MODE == MODE_S3) {
+          a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
+          ts = __dadd_rn(thn, __dmul_rn(a.h, k));
+        } else {  // MODE_S4: theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
+          ts = __dadd_rn(thn, __dmul_rn(a.h / 6.0, __dadd_rn(a.acc[li], k)));
+          a.theta[li] = ts;
+          bad |= !isfinite(ts);
+        }
+        double s, c;
+        sincos(ts, &s, &c);
+        a.zout[row] = make_double2(c, s);
+        px += c;
+        py += s;
+      }
+    }
+  }
+  if (MODE == MODE_RHS) return;
+  if (MODE == MODE_S4 && bad) s_nonfinite = 1;
+  __syncthreads();
+  if (MODE == MODE_S4 && tid == 0 && s_nonfinite) dp.ctrl->nonfinite = 1;
+  tile_partial_and_finish(dp, a, lt, px, py, red);
+}
+
+__global__ void k_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace) {
+  c->record_every = record_every;
+  c->nrec_cap = nrec_cap;
+  c->r_trace = r_trace;
+}
+
+__global__ void k_permute(const int32_t* __restrict__ perm, int64_t n, const double* __restrict__ in,
+                          double* __restrict__ out, int dir) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (dir == KUR_USER_TO_INTERNAL) out[i] = in[perm[i]];
+  else out[perm[i]] = in[i];
+}
+
+template <int MODE, int RPT>
+cudaError_t launch_stage_t(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
+  static bool attr_set = false;
+  const size_t smem = stage_smem_bytes();
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_stage<MODE, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k_stage<MODE, RPT><<<dp.ntiles, NTHREADS, smem, s>>>(dp, a);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
+  switch (dp.rpt) {
+    case 1: return launch_stage_t<MODE, 1>(dp, a, s);
+    case 2: return launch_stage_t<MODE, 2>(dp, a, s);
+    case 4: return launch_stage_t<MODE, 4>(dp, a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+size_t stage_smem_bytes() { return sizeof(double2) * (WZ + 1); }
+
+cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
+  if (dp.ntiles <= 0) return cudaSuccess;
+  switch (dp.rpt) {
+    case 1: k_prologue<1><<<dp.ntiles, NTHREADS, 0, s>>>(dp, a); break;
+    case 2: k_prologue<2><<<dp.ntiles, NTHREADS, 0, s>>>(dp, a); break;
+    case 4: k_prologue<4><<<dp.ntiles, NTHREADS, 0, s>>>(dp, a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
+  if (dp.ntiles <= 0) return cudaSuccess;
+  switch (mode) {
+    case MODE_RHS: return launch_stage_m<MODE_RHS>(dp, a, s);
+    case MODE_S1: return launch_stage_m<MODE_S1>(dp, a, s);
+    case MODE_S2: return launch_stage_m<MODE_S2>(dp, a, s);
+    case MODE_S3: return launch_stage_m<MODE_S3>(dp, a, s);
+    case MODE_S4: return launch_stage_m<MODE_S4>(dp, a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, cudaStream_t s) {
+  k_set_ctrl<<<1, 1, 0, s>>>(c, record_every, nrec_cap, r_trace);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute(const int32_t* perm, int64_t n, const double* in, double* out, int dir,
+                           cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int bs = 256;
+  k_permute<<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(perm, n, in, out, dir);
+  return cudaGetLastError();
+}
+
+}  // namespace kur

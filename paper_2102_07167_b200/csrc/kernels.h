@@ -1,0 +1,74 @@
+// kernels.h — device-side plan + launchers (product code; used by api.cpp).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "plan.h"
+
+namespace kur {
+
+struct Ctrl {             // device-resident control block
+  unsigned int ticket;    // last-block detection
+  int nonfinite;          // set by RK stage 4 when a phase is not finite
+  int record_every;       // > 0: record (r, psi) of theta_n when n % record_every == 0
+  int nrec_cap;           // capacity of r_trace in pairs
+  long long step;         // n of the current theta_n inside kur_step
+  double* r_trace;        // [nrec_cap][2]
+  double rpsi[2];         // last computed (r, psi)
+};
+
+struct PartInfo {         // 8 bytes; device array [n_parts]
+  int32_t window;         // window id (hot) or -1 (remote)
+  int32_t neg;            // 1: entries are complements (subtracted), 0: non-zeros (added)
+};
+
+struct DevPlan {
+  int64_t n;              // global N
+  int32_t C;
+  int32_t rpt, cpt;       // rows per thread, chunks per tile
+  int32_t ntiles;         // local tiles (one CTA each)
+  int32_t tile_base;      // global id of local tile 0
+  int32_t row_begin;      // internal id of local row 0
+  int32_t world;
+  const TileDesc* tiles;      // [ntiles]
+  const int32_t* order;       // [ntiles] launch order
+  const PartInfo* parts;      // [n_parts]
+  const uint2* chunks;        // [n_parts * cpt]
+  const uint4* pool;          // index units
+  const int32_t* comm_tile0;  // [C+1] global tile ids
+  const int32_t* D_ptr;       // [C+1]
+  const int32_t* D_idx;
+  const int32_t* comm_size;   // [C]
+  const int32_t* perm;        // [n] internal -> user
+  double2* partial;           // [ntiles_all] per-tile sums of z (global tile ids)
+  double2* S;                 // [C] block sums S_b of the last reduction
+  Ctrl* ctrl;
+};
+
+enum StageMode { MODE_RHS = 0, MODE_S1 = 1, MODE_S2 = 2, MODE_S3 = 3, MODE_S4 = 4 };
+enum RecordMode { REC_NONE = 0, REC_START = 1, REC_STEP = 2 };
+
+struct StageArgs {
+  double* theta;          // local rows: theta (prologue/RHS) or theta_n (RK stages; S4 writes theta_{n+1})
+  const double* omega;    // local rows
+  double* acc;            // local rows: k1 + 2k2 + 2k3 (RK)
+  double* out;            // local rows: dtheta (MODE_RHS)
+  const double2* zin;     // [n (+pad)] z of the stage state (global rows)
+  double2* zout;          // [n (+pad)] z of the next stage state
+  const double2* Tin;     // [C] T_a = sum_{b in D(a)} S_b of the stage state
+  double2* Tout;          // [C] T of the next stage state
+  double KN;              // K / N
+  double h;               // step
+  double* op_rpsi;        // kur_order_parameter outputs (device) or NULL
+  double* op_local;
+  int record;             // RecordMode
+};
+
+cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
+cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaStream_t s);
+cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, cudaStream_t s);
+cudaError_t launch_permute(const int32_t* perm, int64_t n, const double* in, double* out, int dir,
+                           cudaStream_t s);
+size_t stage_smem_bytes();
+
+}  // namespace kur

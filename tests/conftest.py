@@ -17,5 +17,5 @@ def pytest_configure(config):
 @pytest.fixture(scope="session", autouse=True)
 def _build_native():
     # builds kurgen/, oracle/ and libkur.so in-tree if missing or stale
-    subprocess.run(["make", "-s", "-C", ROOT, "kurgen/libkurgen.so", "oracle/liboracle.so"], check=True)
+    subprocess.run(["make", "-s", "-C", ROOT, "all"], check=True)
     yield

@@ -1,0 +1,219 @@
+"""Host-side builder tests (no GPU): the block plan decoded back from the
+stored layout must reproduce A exactly, the
+dense/sparse rule must follow P:96 (reading R3), the permutation must make
+communities contiguous, and every error convention of
+include/kur.h must be reachable."""
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+import kurgen
+from paper_2102_07167_b200 import kur
+
+
+def reconstruct(inst, plan):
+    """Dense 0/1 matrix in USER numbering rebuilt from the exported plan rows."""
+    n = inst.n
+    perm = plan["perm"]
+    lab_int = inst.community[perm]
+    rows = np.zeros((plan["n_local"], n), np.int64)
+    for lj in range(plan["n_local"]):
+        j = plan["row_begin"] + lj
+        a = lab_int[j]
+        for b in plan["D_idx"][plan["D_ptr"][a]:plan["D_ptr"][a + 1]]:
+            rows[lj, lab_int == b] += 1
+        s, e = plan["row_ptr"][lj], plan["row_ptr"][lj + 1]
+        np.add.at(rows[lj], plan["cols"][s:e], np.where(plan["neg"][s:e] == 1, -1, 1))
+    return rows
+
+
+def check_plan(inst, A, **kw):
+    world = kw.pop("world", 1)
+    covered = []
+    for rank in range(world):
+        plan = kur.plan_export(inst, rank=rank, world=world, **kw)
+        perm = plan["perm"]
+        assert sorted(perm.tolist()) == list(range(inst.n))
+        lab_int = inst.community[perm]
+        assert np.all(np.diff(lab_int) >= 0), "communities must be contiguous"
+        rows = reconstruct(inst, plan)
+        for lj in range(plan["n_local"]):
+            j = plan["row_begin"] + lj
+            u = perm[j]
+            got = rows[lj].copy()
+            want = A[u, perm].astype(np.int64)
+            got[j] = want[j] = 0  # diagonal never contributes (reading R2)
+            assert np.array_equal(got, want), (rank, j)
+        covered.append((plan["row_begin"], plan["row_begin"] + plan["n_local"]))
+        sr = plan["shard_row0"]
+        if world > 1:  # shards are whole communities
+            for b in sr[1:-1]:
+                assert b == 0 or b == inst.n or lab_int[b - 1] != lab_int[b]
+    covered.sort()
+    assert covered[0][0] == 0 and covered[-1][1] == inst.n
+    for (a0, a1), (b0, b1) in zip(covered, covered[1:]):
+        assert a1 == b0
+    return plan
+
+
+@pytest.mark.parametrize("kind", ["ones", "zeros", "auto", "random"])
+@pytest.mark.parametrize("thr", [-1.0, 0.0, 0.5, 1.0])
+def test_roundtrip_encodings_thresholds(kind, thr):
+    A, labels = kurgen.random_dense(90, 4, seed=7, p_in=0.8, p_out=0.15, symmetric=False)
+    inst = kurgen.from_dense(A, labels, kind=kind, seed=2)
+    check_plan(inst, A, dense_threshold=thr)
+
+
+@pytest.mark.parametrize("hot_min", [1, 1 << 30, 0])
+def test_roundtrip_hot_and_remote(hot_min):
+    inst = kurgen.sbm([700, 300, 5000, 1, 20], np.array(
+        [[0.97, 0.3, 0.001, 0.0, 0.9], [0.3, 0.6, 0.0, 0.5, 0.0], [0.001, 0.0, 0.02, 0.0, 0.3],
+         [0.0, 0.5, 0.0, 0.0, 0.0], [0.9, 0.0, 0.3, 0.0, 1.0]]), 13)
+    A = inst.dense()
+    check_plan(inst, A, hot_min=hot_min)
+
+
+def test_roundtrip_empty_singleton_one_community():
+    A, labels = kurgen.random_dense(40, 1, seed=1, p_in=0.6)
+    check_plan(kurgen.from_dense(A, labels), A)
+    labels = np.array([0] * 10 + [2] * 25 + [4] * 1, np.int32)  # communities 1 and 3 empty
+    A, _ = kurgen.random_dense(36, 1, seed=3, p_in=0.5, symmetric=False)
+    check_plan(kurgen.from_dense(A, labels, kind="random"), A)
+    n = 17  # no edges at all
+    check_plan(kurgen.from_dense(np.zeros((n, n), np.uint8), np.arange(n) % 3), np.zeros((n, n), np.uint8))
+
+
+def test_roundtrip_many_tiles_ragged():
+    # > 512 rows per community so tiles split, ragged last chunk, several windows
+    inst = kurgen.sbm([1300, 4100, 77, 2600], np.array(
+        [[0.95, 0.001, 0.0, 0.6], [0.001, 0.99, 0.01, 0.0], [0.0, 0.01, 0.3, 0.0], [0.6, 0.0, 0.0, 0.08]]), 5)
+    A = inst.dense()
+    plan = check_plan(inst, A)
+    assert plan["n_tiles"] > 4
+    plan2 = check_plan(inst, A, sm_count=1)  # fewer SMs -> larger tiles (rows per thread > 1)
+    assert plan2["rows_per_tile"] > 512
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_roundtrip_sharded(world):
+    inst = kurgen.sbm([300, 500, 200, 400, 100], np.array(
+        [[0.9, 0.01, 0.0, 0.0, 0.2], [0.01, 0.95, 0.02, 0.0, 0.0], [0.0, 0.02, 0.7, 0.01, 0.0],
+         [0.0, 0.0, 0.01, 0.99, 0.0], [0.2, 0.0, 0.0, 0.0, 0.3]]), 9)
+    check_plan(inst, inst.dense(), world=world)
+
+
+def _census(A, labels):
+    C = labels.max() + 1
+    dense = set()
+    for a in range(C):
+        ra = np.flatnonzero(labels == a)
+        for b in range(C):
+            cb = np.flatnonzero(labels == b)
+            blk = A[np.ix_(ra, cb)].astype(np.int64)
+            total = len(ra) * len(cb)
+            ones = blk.sum()
+            if a == b:
+                total -= len(ra)
+                ones -= np.trace(blk)
+            zeros = total - ones
+            if total > 0 and zeros < ones:  # P:96, tie -> sparse (R3)
+                dense.add((a, b))
+    return dense
+
+
+def test_paper_rule_matches_census():
+    A, labels = kurgen.random_dense(120, 6, seed=21, p_in=0.5, p_out=0.5, symmetric=False)
+    inst = kurgen.from_dense(A, labels, kind="random", seed=3)
+    plan = kur.plan_export(inst)
+    got = {(a, int(b)) for a in range(inst.n_comm) for b in plan["D_idx"][plan["D_ptr"][a]:plan["D_ptr"][a + 1]]}
+    assert got == _census(A, labels)
+    assert plan["nnz"] == int(A.sum() - np.trace(A))
+
+
+def test_tie_is_sparse():
+    # 2 communities of 2: block (0,1) has exactly 2 ones of 4 -> SPARSE; block (0,0) off-diag all ones -> DENSE
+    A = np.array([[0, 1, 1, 0], [1, 0, 0, 1], [1, 0, 0, 1], [0, 1, 1, 0]], np.uint8)
+    inst = kurgen.from_dense(A, [0, 0, 1, 1])
+    plan = kur.plan_export(inst)
+    D = {a: set(plan["D_idx"][plan["D_ptr"][a]:plan["D_ptr"][a + 1]].tolist()) for a in range(2)}
+    assert D == {0: {0}, 1: {1}}
+
+
+def test_complete_graph_plan_has_no_entries():
+    inst = kurgen.complete_graph(3000, 1)
+    plan = kur.plan_export(inst)
+    assert plan["cols"].size == 0 and plan["D_idx"].tolist() == [0]
+
+
+# ---------------------------------------------------------------- error conventions
+def _build_status(**over):
+    inst = kurgen.from_dense(np.array([[0, 1, 1], [1, 0, 0], [1, 0, 0]], np.uint8), [0, 0, 1], kind="ones")
+    arrays = dict(community=inst.community.copy(), seg_ptr=inst.seg_ptr.copy(), seg_comm=inst.seg_comm.copy(),
+                  seg_kind=inst.seg_kind.copy(), idx_ptr=inst.idx_ptr.copy(), idx=inst.idx.copy())
+    n, C, thr = inst.n, inst.n_comm, over.pop("thr", -1.0)
+    for k, v in over.items():
+        if k == "n":
+            n = v
+        elif k == "C":
+            C = v
+        else:
+            arrays[k] = np.asarray(v, arrays[k].dtype)
+
+    class I:  # noqa: E742
+        pass
+    I.n, I.n_comm = n, C
+    for k, v in arrays.items():
+        setattr(I, k, v)
+    desc, keep = kur._desc_from(I, thr)
+    h = ctypes.c_void_p()
+    st = kur._lib.kur_plan_build(ctypes.byref(desc), 0, 1, 148, ctypes.byref(h))
+    if st == 0:
+        kur._lib.kur_plan_destroy(h)
+    return st
+
+
+def test_error_codes():
+    # row 0: [seg comm0 ONES {1}], [seg comm1 ONES {2}]; row 1: [comm0 {0}]; row 2: [comm0 {0}]
+    assert _build_status() == 0
+    assert _build_status(idx=[1, 5, 0, 0]) == 2          # KUR_ERR_INDEX_RANGE
+    assert _build_status(community=[0, 0, 7]) == 4      # KUR_ERR_PARTITION (label)
+    assert _build_status(idx=[2, 2, 0, 0]) == 4         # column outside its segment's community
+    assert _build_status(seg_comm=[0, 0, 0, 0]) == 3    # community given two segments in a row
+    assert _build_status(seg_kind=[0, 3, 0, 0]) == 1    # bad kind -> INVALID_ARG
+    assert _build_status(thr=1.5) == 1                  # threshold > 1
+    assert _build_status(n=0) == 1                      # n < 1
+    assert _build_status(idx_ptr=[0, 1, 0, 3, 4]) == 5  # idx_ptr not monotone -> SIZE_MISMATCH
+
+
+def test_duplicate_and_unsorted_lists():
+    A = np.ones((4, 4), np.uint8)
+    inst = kurgen.from_dense(A, [0, 0, 0, 0], kind="ones")
+    bad = inst.idx.copy()
+    bad[1] = bad[0]  # duplicate inside row 0's segment
+    inst.idx = bad
+    with pytest.raises(kur.KurError) as e:
+        kur.plan_export(inst)
+    assert e.value.status == 3
+    inst = kurgen.from_dense(A, [0, 0, 0, 0], kind="ones")
+    bad = inst.idx.copy()
+    bad[0], bad[1] = bad[1], bad[0]
+    inst.idx = bad
+    with pytest.raises(kur.KurError) as e:
+        kur.plan_export(inst)
+    assert e.value.status == 1
+
+
+def test_library_exports_every_declared_symbol():
+    """Every function include/kur.h declares is exported by libkur.so (no compute calls)."""
+    import os
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "kur.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    names = set(re.findall(r"\b(kur_[a-z_0-9]+)\s*\(", hdr))
+    assert {"kur_graph_build", "kur_rhs", "kur_step", "kur_order_parameter"} <= names
+    lib = ctypes.CDLL(kur.LIB_PATH)
+    for name in sorted(names):
+        assert hasattr(lib, name), name
+    assert set(kur.EXPORTED) <= names
+    assert kur._lib.kur_status_string(9) == b"KUR_ERR_NONFINITE"

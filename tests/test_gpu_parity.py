@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path (through the C-ABI binding) against the CPU
+oracle on the same seeded inputs.  Tolerances are BASELINE.json north_star's:
+per RHS and on theta after 10 steps |gpu - oracle| <= 1e-9 + 1e-12 |oracle|;
+the complex order parameter r e^{i psi} within 1e-9 at every recorded step.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import kurgen
+import oracle
+from tests.helpers import R_TOL, Run, close, complex_rpsi
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    torch.cuda.init()
+
+
+# ---------------------------------------------------------------- worked examples
+def test_spec_worked_example_rhs():
+    ex = json.load(open(os.path.join(GOLDEN, "spec_worked_examples.json")))["cases"]
+    for c in ex:
+        if "expected_rhs" not in c:
+            continue
+        n = c["n"]
+        A = np.ones((n, n), np.uint8) - np.eye(n, dtype=np.uint8)
+        inst = kurgen.from_dense(A, np.zeros(n, np.int32), kind="zeros", theta0=np.array(c["theta"]),
+                                 omega=np.array(c["omega"]), K=c["K"])
+        f = Run(inst).rhs()
+        assert np.max(np.abs(f - np.array(c["expected_rhs"]))) <= max(c["tol_abs"], 1e-16), (c["name"], f)
+
+
+def test_order_parameter_examples():
+    for th, r_exp in (([0.0, math.pi], 0.0), ([1.3] * 5, 1.0)):
+        n = len(th)
+        inst = kurgen.complete_graph(n, 1)
+        inst.theta0 = np.array(th)
+        rp = Run(inst).order_parameter()
+        assert abs(rp[0] - r_exp) <= 1e-15
+
+
+# ---------------------------------------------------------------- small random graphs
+SMALL = [
+    dict(n=64, C=1, p_in=0.7, p_out=0.0, sym=False),
+    dict(n=200, C=3, p_in=0.85, p_out=0.05, sym=True),
+    dict(n=333, C=5, p_in=0.6, p_out=0.3, sym=False),
+    dict(n=1500, C=4, p_in=0.9, p_out=0.02, sym=True),
+]
+
+
+@pytest.mark.parametrize("cfg", SMALL)
+@pytest.mark.parametrize("kind", ["ones", "zeros", "random"])
+@pytest.mark.parametrize("thr", [-1.0, 0.0, 1.0])
+def test_rhs_small_random(cfg, kind, thr):
+    A, labels = kurgen.random_dense(cfg["n"], cfg["C"], seed=cfg["n"] + 7, p_in=cfg["p_in"],
+                                    p_out=cfg["p_out"], symmetric=cfg["sym"])
+    inst = kurgen.from_dense(A, labels, kind=kind, seed=3, K=2.5)
+    ref = oracle.rhs(oracle.Graph(inst), inst.theta0, inst.omega, inst.K, mode="naive")
+    got = Run(inst, dense_threshold=thr).rhs()
+    ok, err = close(got, ref, abs_tol=1e-13, rel_tol=1e-12)
+    assert ok, err
+
+
+@pytest.mark.parametrize("hot_min", [1, 1 << 30])
+@pytest.mark.parametrize("rpt", [1, 2, 4])
+def test_rhs_layout_variants(hot_min, rpt):
+    """All-hot / all-remote layouts and 1/2/4 rows per thread give the same RHS."""
+    inst = kurgen.sbm([2100, 700, 5000, 1, 33, 0, 900], np.array(
+        [[0.97, 0.3, 0.001, 0.0, 0.9, 0, 0.0], [0.3, 0.6, 0.0, 0.5, 0.0, 0, 0.01],
+         [0.001, 0.0, 0.02, 0.0, 0.3, 0, 0.0], [0.0, 0.5, 0.0, 0.0, 0.0, 0, 0.0],
+         [0.9, 0.0, 0.3, 0.0, 1.0, 0, 0.0], [0] * 7, [0.0, 0.01, 0.0, 0.0, 0.0, 0, 0.99]]), 13, K=3.0)
+    ref = oracle.rhs(oracle.Graph(inst), inst.theta0, inst.omega, inst.K, mode="naive")
+    got = Run(inst, hot_min=hot_min, rpt=rpt).rhs()
+    ok, err = close(got, ref, abs_tol=1e-13, rel_tol=1e-12)
+    assert ok, err
+
+
+def test_trajectory_small_sbm_and_determinism():
+    inst = kurgen.sbm([1000, 3000, 600], np.array([[0.95, 0.01, 0.7], [0.01, 0.9, 0.0], [0.7, 0.0, 0.3]]), 17,
+                      K=4.0, h=0.01, nsteps=20)
+    th_ref, th10_ref, rt_ref = oracle.rk4(oracle.Graph(inst), inst.theta0, inst.omega, inst.K, inst.h, 20, 1,
+                                          mode="naive")
+    run = Run(inst)
+    th10, _ = run.step(10, 1)
+    th, rt = run.step(20, 1)
+    th_b, rt_b = run.step(20, 1)
+    assert close(th10, th10_ref)[0], close(th10, th10_ref)[1]
+    assert close(th, th_ref)[0]
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(rt_ref))) <= R_TOL
+    assert np.array_equal(th, th_b) and np.array_equal(rt, rt_b), "run-to-run bitwise determinism"
+
+
+def test_step_zero_and_record_every():
+    inst = kurgen.sbm([300, 300], [[0.9, 0.1], [0.1, 0.9]], 3, K=2.0, h=0.02)
+    run = Run(inst)
+    th, rt = run.step(0, 1)
+    assert np.array_equal(th, inst.theta0)
+    r0 = oracle.order_parameter(inst.theta0)
+    assert rt.shape == (1, 2) and abs(rt[0, 0] - r0[0]) <= 1e-14
+    th_ref, _, rt_ref = oracle.rk4(oracle.Graph(inst), inst.theta0, inst.omega, inst.K, inst.h, 7, 3, mode="naive")
+    th, rt = run.step(7, 3)
+    assert rt.shape == rt_ref.shape == (3, 2)
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(rt_ref))) <= R_TOL
+    assert close(th, th_ref)[0]
+
+
+def test_local_order_parameters_and_permute_roundtrip():
+    inst = kurgen.sbm([100, 0, 250, 1], [[0.9, 0, 0.1, 0], [0, 0, 0, 0], [0.1, 0, 0.9, 0], [0, 0, 0, 0]], 4)
+    run = Run(inst)
+    rp, loc = run.order_parameter(local=True)
+    r_ref, psi_ref = oracle.order_parameter(inst.theta0)
+    assert abs(rp[0] * np.exp(1j * rp[1]) - r_ref * np.exp(1j * psi_ref)) <= 1e-14
+    for c in range(4):
+        th = inst.theta0[inst.community == c]
+        zc = np.exp(1j * th).mean() if th.size else 0.0
+        assert abs(loc[c, 0] * np.exp(1j * loc[c, 1]) - zc) <= 1e-14
+    x = torch.from_numpy(inst.theta0).cuda()
+    back = run.g.to_user(run.g.to_internal(x))
+    assert torch.equal(back, x)
+
+
+def test_nonfinite_is_reported():
+    from paper_2102_07167_b200 import kur
+    inst = kurgen.sbm([64], [[0.5]], 2)
+    inst.theta0[5] = np.inf
+    run = Run(inst)
+    th = run.theta_int.clone()
+    with pytest.raises(kur.KurError) as e:
+        kur.step(run.g, th, run.omega_int, 1.0, 0.01, 2, check=True)
+    assert e.value.status == 9
+    kur.check(run.g)  # flag cleared
+
+
+def test_invalid_scalars():
+    from paper_2102_07167_b200 import kur
+    run = Run(kurgen.sbm([10], [[0.5]], 2))
+    th = run.theta_int.clone()
+    for K, h in ((1.0, 0.0), (1.0, -1.0), (float("nan"), 0.1), (1.0, float("inf"))):
+        with pytest.raises(kur.KurError) as e:
+            kur.step(run.g, th, run.omega_int, K, h, 1)
+        assert e.value.status == 1
+
+
+# ---------------------------------------------------------------- BASELINE configs
+def test_config1_full_trajectory():
+    """cfg1: complete graph N=1000, oracle = direct O(N^2) summation."""
+    inst = kurgen.config(1)
+    og = oracle.Graph(inst)
+    run = Run(inst)
+    f_ref = oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode="naive")
+    assert close(run.rhs(), f_ref)[0]
+    th_ref, th10_ref, rt_ref = oracle.rk4(og, inst.theta0, inst.omega, inst.K, inst.h, inst.nsteps, 1, mode="naive")
+    th10, _ = run.step(10, 1)
+    th, rt = run.step(inst.nsteps, 1)
+    assert close(th10, th10_ref)[0]
+    assert close(th, th_ref)[0]
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(rt_ref))) <= R_TOL
+
+
+def test_config2_complete_large():
+    """cfg2: N=2^20 complete graph; oracle = order-parameter form for the
+    trajectory and direct summation on sampled rows of the RHS."""
+    inst = kurgen.config(2)
+    og = oracle.Graph(inst)
+    run = Run(inst)
+    f = run.rhs()
+    f_op = oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode="op")
+    assert close(f, f_op)[0], close(f, f_op)[1]
+    rows = np.concatenate([[0, inst.n - 1], kurgen.raw_bits(1, 9, 30) % np.uint64(inst.n)]).astype(np.int64)
+    f_naive = oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode="naive", rows=rows)
+    assert close(f[rows], f_naive)[0]
+    nst = 20
+    th_ref, th10_ref, rt_ref = oracle.rk4(og, inst.theta0, inst.omega, inst.K, inst.h, nst, inst.record_every,
+                                          mode="op")
+    th, rt = run.step(nst, inst.record_every)
+    assert close(th, th_ref)[0], close(th, th_ref)[1]
+    assert rt.shape == (3, 2)
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(rt_ref))) <= R_TOL
+
+
+def test_config3_rhs_and_10_steps():
+    inst = kurgen.config(3)
+    og = oracle.Graph(inst)
+    run = Run(inst)
+    f_ref = oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode="naive")
+    ok, err = close(run.rhs(), f_ref)
+    assert ok, err
+    th_ref, th10_ref, rt_ref = oracle.rk4(og, inst.theta0, inst.omega, inst.K, inst.h, 10, 1, mode="matvec")
+    th10, rt = run.step(10, 1)
+    ok, err = close(th10, th10_ref)
+    assert ok, err
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(rt_ref))) <= R_TOL
+
+
+def test_config4_rhs_and_10_steps():
+    inst = kurgen.config(4)
+    og = oracle.Graph(inst)
+    run = Run(inst)
+    info = run.g.info
+    assert info["n_dense_blocks"] > 0 and info["n_sparse_blocks"] > 0  # exercises the per-block choice
+    f_ref = oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode="matvec")
+    f = run.rhs()
+    ok, err = close(f, f_ref)
+    assert ok, err
+    rows = (kurgen.raw_bits(4, 9, 256) % np.uint64(inst.n)).astype(np.int64)
+    assert close(f[rows], oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode="naive", rows=rows))[0]
+    th_ref, th10_ref, rt_ref = oracle.rk4(og, inst.theta0, inst.omega, inst.K, inst.h, 10, 1, mode="matvec")
+    th10, rt = run.step(10, 1)
+    ok, err = close(th10, th10_ref)
+    assert ok, err
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(rt_ref))) <= R_TOL
+
+
+def test_config5_sampled_rows_and_invariants():
+    """cfg5 at full size in the bench launch configuration: the RHS on sampled rows
+    (direct summation), the committed oracle trajectory sample (if present), and the
+    conserved mean phase velocity on the whole state."""
+    inst = kurgen.config(5)
+    og = oracle.Graph(inst)
+    run = Run(inst)
+    f = run.rhs()
+    rng_rows = (kurgen.raw_bits(5, 9, 2048) % np.uint64(inst.n)).astype(np.int64)
+    comm0 = np.flatnonzero(inst.community == 0)[:1024].astype(np.int64)
+    rows = np.concatenate([rng_rows, comm0])
+    ok, err = close(f[rows], oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode="naive", rows=rows))
+    assert ok, err
+    d = f - inst.omega
+    assert abs(math.fsum(d)) <= 1e-12 * np.sum(np.abs(d)) + 1e-9
+    th10, rt = run.step(10, 1)
+    res = math.fsum(th10) - math.fsum(inst.theta0) - 10 * inst.h * math.fsum(inst.omega)
+    assert abs(res) <= 1e-10 * inst.n
+    gold = os.path.join(GOLDEN, "cfg5_oracle_trajectory.npz")
+    if os.path.exists(gold):
+        z = np.load(gold)
+        assert str(z["sha256"]) == inst.sha256(), "instance differs from the one the golden file was made from"
+        ok, err = close(th10[z["rows"]], z["theta10"])
+        assert ok, err
+        assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(z["r_trace"]))) <= R_TOL
