@@ -194,6 +194,14 @@ kur_status kur_plan_export(const kur_plan *p, int32_t *perm, int32_t *D_ptr, int
                            int32_t *cols, int8_t *neg, int32_t *shard_row0);
 kur_status kur_plan_destroy(kur_plan *p);
 
+/* Per-launch timing for measurement (bench.py): while enabled, kur_step
+ * records a CUDA event pair around every kernel it launches, on `stream`.
+ * kur_timing_read blocks until the last recorded event, writes out[4] =
+ * {total ms of k_prologue launches, their count, total ms of RK-stage
+ * launches, their count} and clears the record.  Enabling also clears it. */
+kur_status kur_timing(kur_graph *g, int32_t enable);
+kur_status kur_timing_read(kur_graph *g, double *out /* [4] */);
+
 /* Creates a 128-byte NCCL unique id (rank 0), to be broadcast by the caller. */
 kur_status kur_nccl_unique_id(void *id128);
 

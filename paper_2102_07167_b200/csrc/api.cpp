@@ -61,6 +61,21 @@ struct kur_graph {
   double* acc = nullptr;
   Ctrl* ctrl = nullptr;
   ncclComm_t comm = nullptr;
+  // optional per-launch CUDA-event timing (kur_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;        // pool, reused
+  std::vector<int> ev_kind;           // per recorded pair: 0 prologue, 1 stage
+  size_t ev_used = 0;
+  cudaError_t mark(cudaStream_t s) {  // records the next event of the pool on s
+    if (!timing) return cudaSuccess;
+    if (ev_used == ev.size()) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return r;
+      ev.push_back(e);
+    }
+    return cudaEventRecord(ev[ev_used++], s);
+  }
 
   ~kur_graph() {
     cudaSetDevice(device);
@@ -68,6 +83,7 @@ struct kur_graph {
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
     if (comm) ncclCommDestroy(comm);
   }
 };
@@ -315,7 +331,10 @@ kur_status kur_step(kur_graph* g, double* theta, const double* omega, double K, 
   a.zout = g->zA;
   a.Tout = g->TA;
   a.record = REC_START;
+  KUR_CUDA(g->mark(s));
   KUR_CUDA(launch_prologue(g->dp, a, s));
+  KUR_CUDA(g->mark(s));
+  if (g->timing) g->ev_kind.push_back(0);
   for (int64_t n = 0; n < nsteps; ++n) {
     for (int st = MODE_S1; st <= MODE_S4; ++st) {
       const bool even = (st == MODE_S1 || st == MODE_S3);
@@ -324,7 +343,10 @@ kur_status kur_step(kur_graph* g, double* theta, const double* omega, double K, 
       a.Tin = even ? g->TA : g->TB;
       a.Tout = even ? g->TB : g->TA;
       a.record = st == MODE_S4 ? REC_STEP : REC_NONE;
+      KUR_CUDA(g->mark(s));
       KUR_CUDA(launch_stage(st, g->dp, a, s));
+      KUR_CUDA(g->mark(s));
+      if (g->timing) g->ev_kind.push_back(1);
     }
   }
   return KUR_OK;
@@ -341,6 +363,35 @@ kur_status kur_order_parameter(kur_graph* g, const double* theta, double* r_psi,
   a.op_local = local;
   a.record = REC_NONE;
   KUR_CUDA(launch_prologue(g->dp, a, (cudaStream_t)stream));
+  return KUR_OK;
+}
+
+kur_status kur_timing(kur_graph* g, int32_t enable) {
+  if (!g) return fail(KUR_ERR_INVALID_ARG, "graph is NULL");
+  g->timing = enable != 0;
+  g->ev_used = 0;
+  g->ev_kind.clear();
+  return KUR_OK;
+}
+
+kur_status kur_timing_read(kur_graph* g, double* out) {
+  if (!g || !out) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  KUR_CUDA(cudaSetDevice(g->device));
+  double ms[2] = {0.0, 0.0};
+  int64_t cnt[2] = {0, 0};
+  for (size_t i = 0; i < g->ev_kind.size(); ++i) {
+    float t = 0.f;
+    KUR_CUDA(cudaEventSynchronize(g->ev[2 * i + 1]));
+    KUR_CUDA(cudaEventElapsedTime(&t, g->ev[2 * i], g->ev[2 * i + 1]));
+    ms[g->ev_kind[i]] += t;
+    cnt[g->ev_kind[i]] += 1;
+  }
+  out[0] = ms[0];
+  out[1] = (double)cnt[0];
+  out[2] = ms[1];
+  out[3] = (double)cnt[1];
+  g->ev_used = 0;
+  g->ev_kind.clear();
   return KUR_OK;
 }
 

@@ -62,17 +62,20 @@ _lib.kur_rhs.argtypes = [_p, _p, _p, _d, _p, _p]
 _lib.kur_step.argtypes = [_p, _p, _p, _d, _d, _i64, _i32, _p, _p]
 _lib.kur_order_parameter.argtypes = [_p, _p, _p, _p, _p]
 _lib.kur_check.argtypes = [_p, _p]
+_lib.kur_timing.argtypes = [_p, _i32]
+_lib.kur_timing_read.argtypes = [_p, _p]
 _lib.kur_nccl_unique_id.argtypes = [_p]
 _lib.kur_status_string.restype = ctypes.c_char_p
 _lib.kur_status_string.argtypes = [ctypes.c_int]
 _lib.kur_last_error.restype = ctypes.c_char_p
 for _f in ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
-           "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id"):
+           "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id", "kur_timing",
+           "kur_timing_read"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
             "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id",
-            "kur_status_string", "kur_last_error")
+            "kur_status_string", "kur_last_error", "kur_timing", "kur_timing_read")
 
 
 class KurError(RuntimeError):
@@ -225,6 +228,18 @@ def step(g: Graph, theta, omega, K, h, nsteps, record_every=0, r_trace=None, str
     if host:
         th_h.copy_(theta, non_blocking=False)
     return r_trace
+
+
+def timing(g: Graph, enable: bool):
+    """Enable/disable per-launch CUDA-event timing inside kur_step (clears the record)."""
+    _check(_lib.kur_timing(g._h, 1 if enable else 0))
+
+
+def timing_read(g: Graph):
+    """dict(prologue_ms, prologue_n, stage_ms, stage_n) of the launches recorded since enabling."""
+    out = np.zeros(4, np.float64)
+    _check(_lib.kur_timing_read(g._h, _np_ptr(out)))
+    return dict(prologue_ms=float(out[0]), prologue_n=int(out[1]), stage_ms=float(out[2]), stage_n=int(out[3]))
 
 
 def check(g: Graph, stream=None):
