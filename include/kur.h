@@ -64,8 +64,6 @@ typedef enum {
 
 /* Segment kinds of the row-segmented adjacency pattern. */
 enum { KUR_ONES = 0, KUR_ZEROS = 1 };
-/* kur_graph_desc.flags */
-enum { KUR_FLAG_RPT1 = 1, KUR_FLAG_RPT2 = 2, KUR_FLAG_RPT4 = 4 };
 
 /* Adjacency A in USER numbering, row-segmented by column community.
  * Row u owns segments seg_ptr[u] .. seg_ptr[u+1]-1; segment s covers column
@@ -95,8 +93,8 @@ typedef struct {
                                (direct CSR); must be <= 1. */
   int32_t hot_min;          /* tuning: minimum entries of a tile in one column window for the
                                window to be staged in shared memory; <= 0 selects the default */
-  int32_t flags;            /* 0, or KUR_FLAG_RPT1/2/4: force 1/2/4 rows per thread (tile = 512/1024/2048
-                               rows) instead of the size-based choice; other bits must be 0 */
+  int32_t flags;            /* 0 (size-based choice), or a forced tile size in rows: a multiple of 32
+                               in [32, 2048] (tuning / tests) */
 } kur_graph_desc;
 
 /* Multi-GPU placement: contiguous ranges of whole communities per rank.
@@ -123,6 +121,7 @@ typedef struct {
   int64_t n_dense_blocks;      /* non-empty blocks handled by precomputed sums */
   int64_t n_sparse_blocks;     /* non-empty blocks handled by direct summation */
   int64_t n_tiles, n_hot_parts;
+  int64_t n_window_loads;      /* 64 KB z windows staged in shared memory per RHS (all tiles) */
   int64_t sincos_per_rhs;      /* N sin/cos pairs = the "2M" trig evaluations of P:660 */
   int64_t bytes_per_rhs;       /* algorithmic HBM bytes of one RHS */
   int64_t bytes_pool;          /* device bytes of the index pool (incl. padding) */
@@ -177,9 +176,12 @@ kur_status kur_check(kur_graph *g, void *stream);
  * census, dense/sparse rule, permutation, tiles, chunked layout) for one rank
  * and keeps the result on the host.  kur_plan_export DECODES the stored
  * layout back into plain lists, so a caller can rebuild A from it:
- *   sizes[0..9] = n, n_comm, n_local, row_begin, n_entries (stored entries of
+ *   sizes[0..15] = n, n_comm, n_local, row_begin, n_entries (stored entries of
  *   this rank, padding excluded), n_dense_pairs (length of D_idx), n_tiles,
- *   rows_per_tile, nnz, world;
+ *   rows_per_tile, nnz, world, bank conflicts found by the last export (hot
+ *   quarter-warp positions whose slots share a residue mod 8; 0 by
+ *   construction), hot slots, hot entries, remote slots, remote entries,
+ *   window loads per RHS;
  *   perm[n]: user id of internal node i; D_ptr[n_comm+1], D_idx: dense column
  *   communities of each row community (their block sums are added);
  *   row_ptr[n_local+1], cols[n_entries] (internal column ids), neg[n_entries]
@@ -189,7 +191,7 @@ kur_status kur_check(kur_graph *g, void *stream);
 typedef struct kur_plan kur_plan;
 kur_status kur_plan_build(const kur_graph_desc *desc, int32_t rank, int32_t world, int32_t sm_count,
                           kur_plan **out);
-kur_status kur_plan_sizes(const kur_plan *p, int64_t *sizes /* [10] */);
+kur_status kur_plan_sizes(const kur_plan *p, int64_t *sizes /* [16] */);
 kur_status kur_plan_export(const kur_plan *p, int32_t *perm, int32_t *D_ptr, int32_t *D_idx, int64_t *row_ptr,
                            int32_t *cols, int8_t *neg, int32_t *shard_row0);
 kur_status kur_plan_destroy(kur_plan *p);

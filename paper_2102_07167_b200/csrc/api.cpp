@@ -53,7 +53,7 @@ struct kur_graph {
   // device allocations
   TileDesc* d_tiles = nullptr;
   int32_t* d_order = nullptr;
-  PartInfo* d_parts = nullptr;
+  PartDesc* d_parts = nullptr;
   uint2* d_chunks = nullptr;
   uint4* d_pool = nullptr;
   int32_t *d_comm_tile0 = nullptr, *d_D_ptr = nullptr, *d_D_idx = nullptr, *d_csize = nullptr, *d_perm = nullptr;
@@ -161,13 +161,12 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
                                           : cuda_fail(e, what);
   };
   cudaError_t e;
-  std::vector<PartInfo> parts(P.part_window.size());
-  for (size_t i = 0; i < parts.size(); ++i) parts[i] = PartInfo{P.part_window[i], P.part_neg[i]};
+  int64_t pool_bytes = 0;
   std::vector<int32_t> csize((size_t)P.C);
   for (int32_t c = 0; c < P.C; ++c) csize[(size_t)c] = P.comm_off[(size_t)c + 1] - P.comm_off[(size_t)c];
   if ((e = upload(&g->d_tiles, P.tiles)) != cudaSuccess) return bail(e, "tiles");
   if ((e = upload(&g->d_order, P.tile_order)) != cudaSuccess) return bail(e, "order");
-  if ((e = upload(&g->d_parts, parts)) != cudaSuccess) return bail(e, "parts");
+  if ((e = upload(&g->d_parts, P.parts)) != cudaSuccess) return bail(e, "parts");
   {
     std::vector<uint2> ch(P.chunks.size());
     for (size_t i = 0; i < ch.size(); ++i) ch[i] = make_uint2(P.chunks[i].ofs, P.chunks[i].ng);
@@ -175,6 +174,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   }
   {
     const size_t bytes = sizeof(Unit) * P.pool.size();
+    pool_bytes = (int64_t)bytes;
     if ((e = cudaMalloc((void**)&g->d_pool, bytes)) != cudaSuccess) return bail(e, "pool");
     if ((e = cudaMemcpy(g->d_pool, P.pool.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
       return bail(e, "pool copy");
@@ -209,8 +209,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   DevPlan& dp = g->dp;
   dp.n = P.n;
   dp.C = P.C;
-  dp.rpt = P.rpt;
-  dp.cpt = P.chunks_per_tile;
+  dp.rows_per_tile = P.rows_per_tile;
   dp.ntiles = (int32_t)P.tiles.size();
   dp.tile_base = P.tile_begin;
   dp.row_begin = (int32_t)P.row_begin;
@@ -236,6 +235,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   I.world = world;
   I.device = device;
   I.rows_per_tile = P.rows_per_tile;
+  I.n_window_loads = P.n_window_loads;
   I.row_begin = P.row_begin;
   I.row_end = P.row_end;
   I.nnz = P.nnz;
@@ -253,8 +253,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   // index stream (2 B per hot entry, 4 B per remote entry, no padding) plus per
   // local row z_in 16 + z_out 16 + omega 8 + theta_n 8 + acc 16 = 64 B.
   I.bytes_per_rhs = 2 * P.n_idx_hot + 4 * P.n_idx_remote + 64 * g->n_local;
-  I.bytes_pool = (int64_t)(sizeof(Unit) * (size_t)std::max<int64_t>(
-                                              (int64_t)(P.n_slots_hot / 8 + P.n_slots_remote / 4), 1));
+  I.bytes_pool = pool_bytes;
   I.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = g;
   return KUR_OK;
@@ -414,6 +413,7 @@ kur_status kur_check(kur_graph* g, void* stream) {
 // ---------------------------------------------------------------- host-only plan introspection
 struct kur_plan {
   HostPlan P;
+  mutable int64_t conflicts = 0;  // quarter-warp positions with a repeated bank group (export)
 };
 
 extern "C" {
@@ -453,6 +453,12 @@ kur_status kur_plan_sizes(const kur_plan* p, int64_t* sizes) {
   sizes[7] = P.rows_per_tile;
   sizes[8] = P.nnz;
   sizes[9] = P.world;
+  sizes[10] = p->conflicts;
+  sizes[11] = P.n_slots_hot;
+  sizes[12] = P.n_idx_hot;
+  sizes[13] = P.n_slots_remote;
+  sizes[14] = P.n_idx_remote;
+  sizes[15] = P.n_window_loads;
   return KUR_OK;
 }
 
@@ -460,6 +466,7 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
                            int32_t* cols, int8_t* neg, int32_t* shard_row0) {
   if (!p) return fail(KUR_ERR_INVALID_ARG, "NULL plan");
   const HostPlan& P = p->P;
+  p->conflicts = 0;
   if (perm) std::memcpy(perm, P.perm.data(), sizeof(int32_t) * P.perm.size());
   if (D_ptr) std::memcpy(D_ptr, P.D_ptr.data(), sizeof(int32_t) * P.D_ptr.size());
   if (D_idx && !P.D_idx.empty()) std::memcpy(D_idx, P.D_idx.data(), sizeof(int32_t) * P.D_idx.size());
@@ -470,35 +477,52 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
   struct E { int32_t row, col; int8_t neg; };
   std::vector<E> ents;
   for (const TileDesc& T : P.tiles) {
-    for (int h = 0; h < T.nhot + T.nremote; ++h) {
-      const int part = T.part0 + h;
-      const int32_t w = P.part_window[(size_t)part];
-      const bool hot = h < T.nhot;
-      if (hot != (w >= 0)) return fail(KUR_ERR_INVALID_ARG, "plan: part kind mismatch");
-      for (int c = 0; c < P.chunks_per_tile; ++c) {
-        const ChunkDesc cd = P.chunks[(size_t)part * P.chunks_per_tile + (size_t)c];
-        for (uint32_t g = 0; g < cd.ng; ++g) {
-          for (int l = 0; l < 32; ++l) {
-            const Unit& U = P.pool[(size_t)cd.ofs + (size_t)g * 32 + (size_t)l];
-            const int lr = c * 32 + l;
-            const int nper = hot ? 8 : 4;
-            for (int q = 0; q < nper; ++q) {
+    for (int pi = T.part0; pi < T.part0 + T.nparts; ++pi) {
+      const PartDesc& pd = P.parts[(size_t)pi];
+      const bool hot = pd.window >= 0;
+      if (hot != (pi < T.part0 + T.nhot)) return fail(KUR_ERR_INVALID_ARG, "plan: part order");
+      std::vector<uint8_t> seen((size_t)T.nrows, 0);
+      for (uint32_t c = 0; c < pd.nchunks; ++c) {
+        const ChunkDesc cd = P.chunks[(size_t)pd.chunk0 + c];
+        const uint16_t* hdr = reinterpret_cast<const uint16_t*>(&P.pool[(size_t)cd.ofs]);
+        for (int l = 0; l < 32; ++l) {
+          const uint16_t lr = hdr[l];
+          if (lr != EMPTY_LANE) {
+            if (lr >= T.nrows || seen[lr]) return fail(KUR_ERR_INVALID_ARG, "plan: bad chunk header");
+            seen[lr] = 1;
+          }
+          for (uint32_t g = 0; g < cd.ng; ++g) {
+            const Unit& U = P.pool[(size_t)cd.ofs + HDR_UNITS + (size_t)g * 32 + (size_t)l];
+            for (int q = 0; q < (hot ? 8 : 4); ++q) {
               int64_t col;
               if (hot) {
                 const uint32_t e = (q & 1) ? (U.w[q >> 1] >> 16) : (U.w[q >> 1] & 0xFFFFu);
-                if (e == HOT_SENT) continue;
+                if (e >= HOT_SENT && e < HOT_SENT + 8) continue;
                 if (e > HOT_SENT) return fail(KUR_ERR_INVALID_ARG, "plan: hot index out of window");
-                col = (int64_t)w * WZ + e;
+                col = (int64_t)pd.window * WZ + e;
               } else {
                 const uint32_t e = U.w[q];
                 if (e == (uint32_t)P.n) continue;
                 col = e;
               }
-              if (lr >= T.nrows) return fail(KUR_ERR_INVALID_ARG, "plan: entry in an empty lane");
+              if (lr == EMPTY_LANE) return fail(KUR_ERR_INVALID_ARG, "plan: entry in an empty lane");
               if (col < 0 || col >= P.n) return fail(KUR_ERR_INVALID_ARG, "plan: column out of range");
-              ents.push_back(E{(int32_t)(T.row0 + lr - P.row_begin), (int32_t)col, (int8_t)P.part_neg[(size_t)part]});
+              ents.push_back(E{(int32_t)(T.row0 + lr - P.row_begin), (int32_t)col, (int8_t)pd.neg});
             }
           }
+        }
+        if (hot) {  // bank-conflict freedom: distinct slot residues per quarter-warp position
+          for (uint32_t g = 0; g < cd.ng; ++g)
+            for (int q = 0; q < 8; ++q)
+              for (int qw = 0; qw < 4; ++qw) {
+                int mask = 0;
+                for (int l = qw * 8; l < qw * 8 + 8; ++l) {
+                  const Unit& U = P.pool[(size_t)cd.ofs + HDR_UNITS + (size_t)g * 32 + (size_t)l];
+                  const uint32_t e = (q & 1) ? (U.w[q >> 1] >> 16) : (U.w[q >> 1] & 0xFFFFu);
+                  if (mask >> (e & 7) & 1) p->conflicts++;  // NOLINT
+                  mask |= 1 << (e & 7);
+                }
+              }
         }
       }
     }

@@ -16,6 +16,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <numeric>
 #include <omp.h>
@@ -111,9 +112,9 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     return KUR_ERR_INVALID_ARG;
   }
   if (d->n >= INT32_MAX - 2 * WZ) { err = "n too large for int32 internal ids"; return KUR_ERR_UNSUPPORTED; }
-  const int force_rpt = d->flags & 7;
-  if ((d->flags & ~7) || (force_rpt != 0 && force_rpt != 1 && force_rpt != 2 && force_rpt != 4)) {
-    err = "flags: only KUR_FLAG_RPT1/2/4 (1, 2, 4) are defined";
+  const int force_rows = d->flags;
+  if (force_rows != 0 && (force_rows < 32 || force_rows > MAX_TILE_ROWS || force_rows % 32 != 0)) {
+    err = "flags: 0 or a tile size in rows (multiple of 32 in [32, 2048])";
     return KUR_ERR_INVALID_ARG;
   }
   const double thr = d->dense_threshold;
@@ -282,17 +283,16 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   for (int64_t i = 0; i < n; ++i) inv[(size_t)P.perm[(size_t)i]] = (int32_t)i;
 
   // ------------------------------------------------------------ 4. tiles
-  // rows per thread: the largest rpt keeping >= 4 CTAs per SM worth of tiles
-  int rpt = force_rpt ? force_rpt : 1;
-  for (int r = MAX_RPT; r >= 1 && !force_rpt; r >>= 1) {
+  // the largest tile (<= 2048 rows) that still gives >= 2 waves of 2 CTAs/SM
+  int rows_per_tile = force_rows;
+  for (int r = MAX_TILE_ROWS; r >= 32 && !force_rows; r >>= 1) {
     int64_t nt = 0;
-    for (int32_t c = 0; c < C; ++c) nt += (S.csize[(size_t)c] + 512 * r - 1) / (512 * r);
-    if (nt >= 4LL * sm_count || r == 1) { rpt = r; break; }
+    for (int32_t c = 0; c < C; ++c) nt += (S.csize[(size_t)c] + r - 1) / r;
+    rows_per_tile = r;
+    if (nt >= 4LL * sm_count) break;
   }
-  P.rpt = rpt;
-  P.rows_per_tile = NTHREADS * rpt;
-  P.chunks_per_tile = NWARPS * rpt;
-  const int RT = P.rows_per_tile, CPT = P.chunks_per_tile;
+  P.rows_per_tile = rows_per_tile;
+  const int RT = P.rows_per_tile;
   std::vector<TileDesc> all;
   P.comm_tile0.assign((size_t)C + 1, 0);
   for (int32_t c = 0; c < C; ++c) {
@@ -351,17 +351,18 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   constexpr uint64_t COLM = 0x7FFFFFFFULL;
   struct TileOut {
     std::vector<Unit> units;
-    std::vector<int32_t> windows, negs;  // per part (window -1 = remote)
-    std::vector<ChunkDesc> chunks;       // per part x CPT (ofs relative to the tile)
-    int32_t nhot = 0, nremote = 0;
-    int64_t hot = 0, rem = 0, shot = 0, srem = 0;
+    std::vector<PartDesc> parts;    // chunk0 relative to the tile
+    std::vector<ChunkDesc> chunks;  // ofs relative to the tile
+    int32_t nhot = 0;
+    int64_t hot = 0, rem = 0, shot = 0, srem = 0, loads = 0;
   };
   std::vector<TileOut> outs((size_t)nt);
 #pragma omp parallel
   {
     std::vector<uint64_t> keys, remk;
-    std::vector<int32_t> cnt;
-    std::vector<size_t> rb;
+    std::vector<int32_t> rows, rb, cnt;
+    std::vector<uint32_t> pos;  // arranged positions of one quarter: 8 slots each
+    std::vector<uint16_t> lst[8][8];
 #pragma omp for schedule(dynamic, 1)
     for (int32_t lt = 0; lt < nt; ++lt) {
       const TileDesc& T = all[(size_t)(P.tile_begin + lt)];
@@ -378,51 +379,153 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
       // one part = entries src[k0..k1) of one (window|remote, sign), sorted by (row, column)
       auto emit_part = [&](int32_t window, int32_t neg, const uint64_t* src, size_t k0, size_t k1) {
         const bool hot = window >= 0;
-        const int E = hot ? 8 : 4;
-        const int32_t part = (int32_t)O.windows.size();
-        O.windows.push_back(window);
-        O.negs.push_back(neg);
-        O.chunks.resize((size_t)(part + 1) * CPT, ChunkDesc{0, 0});
-        cnt.assign((size_t)RT, 0);
-        for (size_t k = k0; k < k1; ++k) cnt[(size_t)((src[k] >> 32) & 0x7FF)]++;
-        rb.assign((size_t)RT + 1, 0);
-        for (int r = 0; r < RT; ++r) rb[(size_t)r + 1] = rb[(size_t)r] + (size_t)cnt[(size_t)r];
-        for (int c = 0; c < CPT; ++c) {
-          int mx = 0;
-          for (int l = 0; l < 32; ++l) mx = std::max(mx, cnt[(size_t)(c * 32 + l)]);
-          const uint32_t ng = (uint32_t)((mx + E - 1) / E);
-          ChunkDesc& cd = O.chunks[(size_t)part * CPT + c];
-          cd.ofs = (uint32_t)O.units.size();
-          cd.ng = ng;
-          const size_t u0 = O.units.size();
-          O.units.resize(u0 + (size_t)ng * 32);
-          for (uint32_t g = 0; g < ng; ++g) {
-            for (int l = 0; l < 32; ++l) {
-              const int r = c * 32 + l;
-              Unit& U = O.units[u0 + (size_t)g * 32 + (size_t)l];
-              if (hot) {
-                uint16_t v[8];
-                for (int q = 0; q < 8; ++q) {
-                  const int e = (int)g * 8 + q;
-                  v[q] = e < cnt[(size_t)r]
-                             ? (uint16_t)((src[k0 + rb[(size_t)r] + (size_t)e] & COLM) - (uint64_t)window * WZ)
-                             : (uint16_t)HOT_SENT;
-                }
-                std::memcpy(U.w, v, 16);
-              } else {
-                for (int q = 0; q < 4; ++q) {
-                  const int e = (int)g * 4 + q;
-                  U.w[q] = e < cnt[(size_t)r] ? (uint32_t)(src[k0 + rb[(size_t)r] + (size_t)e] & COLM) : SENT_REMOTE;
+        PartDesc pd{window, neg, (uint32_t)O.chunks.size(), 0};
+        // rows with entries, longest first
+        rows.clear();
+        rb.clear();
+        cnt.clear();
+        for (size_t k = k0; k < k1;) {
+          const int32_t lr = (int32_t)((src[k] >> 32) & 0x7FF);
+          size_t j = k;
+          while (j < k1 && (int32_t)((src[j] >> 32) & 0x7FF) == lr) ++j;
+          rows.push_back((int32_t)rows.size());
+          rb.push_back((int32_t)(k - k0));
+          cnt.push_back((int32_t)(j - k));
+          k = j;
+        }
+        std::vector<int32_t> ord(rows.size());
+        std::iota(ord.begin(), ord.end(), 0);
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return cnt[(size_t)x] > cnt[(size_t)y]; });
+        for (size_t c0 = 0; c0 < ord.size(); c0 += 32) {
+          const int nl = (int)std::min<size_t>(32, ord.size() - c0);
+          ChunkDesc cd{(uint32_t)O.units.size(), 0};
+          // header: local row id per lane
+          Unit hdr[HDR_UNITS];
+          uint16_t* h16 = reinterpret_cast<uint16_t*>(hdr);
+          for (int l = 0; l < 32; ++l)
+            h16[l] = l < nl ? (uint16_t)((src[k0 + (size_t)rb[(size_t)ord[c0 + (size_t)l]]] >> 32) & 0x7FF) : EMPTY_LANE;
+          O.units.insert(O.units.end(), hdr, hdr + HDR_UNITS);
+          const size_t gbase = O.units.size();
+          if (hot) {
+            // bank-conflict-free arrangement, one quarter-warp (8 lanes) at a time
+            std::vector<std::vector<uint32_t>> qpos(4);
+            size_t L = 0;
+            for (int q = 0; q < 4; ++q) {
+              int rem[8] = {0}, tot[8] = {0}, c8[8][8];
+              for (int l = 0; l < 8; ++l)
+                for (int r = 0; r < 8; ++r) { lst[l][r].clear(); c8[l][r] = 0; }
+              for (int l = 0; l < 8; ++l) {
+                const int lane = q * 8 + l;
+                if (lane >= nl) continue;
+                const int32_t ri = ord[c0 + (size_t)lane];
+                for (int e = 0; e < cnt[(size_t)ri]; ++e) {
+                  const uint32_t slot = (uint32_t)((src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) - (uint64_t)window * WZ);
+                  lst[l][slot & 7].push_back((uint16_t)slot);
+                  c8[l][slot & 7]++;
+                  rem[l]++;
+                  tot[slot & 7]++;
                 }
               }
+              std::vector<uint32_t>& P8 = qpos[(size_t)q];
+              for (;;) {
+                int any = 0;
+                for (int l = 0; l < 8; ++l) any |= rem[l];
+                if (!any) break;
+                int asg[8], owner[8];
+                for (int i = 0; i < 8; ++i) { asg[i] = -1; owner[i] = -1; }
+                int ordl[8];
+                for (int i = 0; i < 8; ++i) ordl[i] = i;
+                std::sort(ordl, ordl + 8, [&](int x, int y) { return rem[x] > rem[y]; });
+                for (int oi = 0; oi < 8; ++oi) {  // greedy: scarce-residue first
+                  const int l = ordl[oi];
+                  if (!rem[l]) continue;
+                  int best = -1, bs = -1;
+                  for (int r = 0; r < 8; ++r)
+                    if (owner[r] < 0 && c8[l][r] > 0 && tot[r] * 4096 + c8[l][r] > bs) { bs = tot[r] * 4096 + c8[l][r]; best = r; }
+                  if (best >= 0) { asg[l] = best; owner[best] = l; }
+                }
+                // augmenting paths (Kuhn) for lanes still unmatched
+                for (int oi = 0; oi < 8; ++oi) {
+                  const int l = ordl[oi];
+                  if (!rem[l] || asg[l] >= 0) continue;
+                  int seen = 0;
+                  std::function<bool(int)> aug = [&](int x) -> bool {
+                    for (int r = 0; r < 8; ++r) {
+                      if (c8[x][r] <= 0 || (seen >> r & 1)) continue;
+                      seen |= 1 << r;
+                      if (owner[r] < 0 || aug(owner[r])) { owner[r] = x; asg[x] = r; return true; }
+                    }
+                    return false;
+                  };
+                  aug(l);
+                }
+                int used = 0;
+                for (int l = 0; l < 8; ++l) if (asg[l] >= 0) used |= 1 << asg[l];
+                for (int l = 0; l < 8; ++l) {
+                  uint32_t v;
+                  if (asg[l] >= 0) {
+                    const int r = asg[l];
+                    v = lst[l][r].back();
+                    lst[l][r].pop_back();
+                    c8[l][r]--;
+                    rem[l]--;
+                    tot[r]--;
+                  } else {
+                    int r = 0;
+                    while (used >> r & 1) ++r;
+                    used |= 1 << r;
+                    v = HOT_SENT + (uint32_t)r;
+                  }
+                  P8.push_back(v);
+                }
+              }
+              L = std::max(L, P8.size() / 8);
             }
+            const uint32_t ng = (uint32_t)((L + 7) / 8);
+            cd.ng = ng;
+            O.units.resize(gbase + (size_t)ng * 32);
+            for (uint32_t g = 0; g < ng; ++g)
+              for (int lane = 0; lane < 32; ++lane) {
+                const std::vector<uint32_t>& P8 = qpos[(size_t)(lane / 8)];
+                const size_t npos = P8.size() / 8;
+                uint16_t v[8];
+                for (int e = 0; e < 8; ++e) {
+                  const size_t p = (size_t)g * 8 + (size_t)e;
+                  v[e] = p < npos ? (uint16_t)P8[p * 8 + (size_t)(lane & 7)] : (uint16_t)(HOT_SENT + (uint32_t)(lane & 7));
+                }
+                std::memcpy(O.units[gbase + (size_t)g * 32 + (size_t)lane].w, v, 16);
+              }
+            O.shot += (int64_t)ng * 256;
+          } else {
+            int mx = 0;
+            for (int l = 0; l < nl; ++l) mx = std::max(mx, cnt[(size_t)ord[c0 + (size_t)l]]);
+            const uint32_t ng = (uint32_t)((mx + 3) / 4);
+            cd.ng = ng;
+            O.units.resize(gbase + (size_t)ng * 32);
+            for (uint32_t g = 0; g < ng; ++g)
+              for (int lane = 0; lane < 32; ++lane) {
+                Unit& U = O.units[gbase + (size_t)g * 32 + (size_t)lane];
+                for (int e = 0; e < 4; ++e) {
+                  const int p = (int)g * 4 + e;
+                  uint32_t v = SENT_REMOTE;
+                  if (lane < nl) {
+                    const int32_t ri = ord[c0 + (size_t)lane];
+                    if (p < cnt[(size_t)ri]) v = (uint32_t)(src[k0 + (size_t)rb[(size_t)ri] + (size_t)p] & COLM);
+                  }
+                  U.w[e] = v;
+                }
+              }
+            O.srem += (int64_t)ng * 128;
           }
-          if (hot) O.shot += (int64_t)ng * 256; else O.srem += (int64_t)ng * 128;
+          O.chunks.push_back(cd);
+          pd.nchunks++;
         }
+        O.parts.push_back(pd);
         if (hot) O.hot += (int64_t)(k1 - k0); else O.rem += (int64_t)(k1 - k0);
       };
       remk.clear();
       size_t i = 0;
+      int32_t last_w = -1;
       while (i < keys.size()) {
         const uint64_t w = keys[i] >> 44;
         size_t j = i;
@@ -432,6 +535,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
           while (m < j && !((keys[m] >> 43) & 1)) ++m;
           if (m > i) { emit_part((int32_t)w, 0, keys.data(), i, m); O.nhot++; }
           if (j > m) { emit_part((int32_t)w, 1, keys.data(), m, j); O.nhot++; }
+          if ((int32_t)w != last_w) { O.loads++; last_w = (int32_t)w; }
         } else {
           for (size_t k = i; k < j; ++k) remk.push_back(keys[k] & ((1ULL << 44) - 1));
         }
@@ -441,56 +545,59 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
         std::sort(remk.begin(), remk.end());  // (sign, row, column)
         size_t m = 0;
         while (m < remk.size() && !((remk[m] >> 43) & 1)) ++m;
-        if (m > 0) { emit_part(-1, 0, remk.data(), 0, m); O.nremote++; }
-        if (remk.size() > m) { emit_part(-1, 1, remk.data(), m, remk.size()); O.nremote++; }
+        if (m > 0) emit_part(-1, 0, remk.data(), 0, m);
+        if (remk.size() > m) emit_part(-1, 1, remk.data(), m, remk.size());
       }
     }
   }
   // ------------------------------------------------------------ 6. concatenate
   P.tiles.resize((size_t)nt);
-  int64_t units = 0, parts = 0;
+  int64_t units = 0, nparts = 0, nchunks = 0;
   for (int32_t lt = 0; lt < nt; ++lt) {
     units += (int64_t)outs[(size_t)lt].units.size();
-    parts += (int64_t)outs[(size_t)lt].windows.size();
+    nparts += (int64_t)outs[(size_t)lt].parts.size();
+    nchunks += (int64_t)outs[(size_t)lt].chunks.size();
   }
   if (units >= (int64_t)UINT32_MAX) { err = "index pool exceeds 64 GB"; return KUR_ERR_UNSUPPORTED; }
   P.pool.resize((size_t)std::max<int64_t>(units, 1));
-  P.part_window.assign((size_t)std::max<int64_t>(parts, 1), -1);
-  P.part_neg.assign((size_t)std::max<int64_t>(parts, 1), 0);
-  P.chunks.assign((size_t)std::max<int64_t>(parts, 1) * CPT, ChunkDesc{0, 0});
-  int64_t uo = 0, po = 0;
-  P.n_idx_hot = P.n_idx_remote = P.n_slots_hot = P.n_slots_remote = P.n_hot_parts = 0;
-  std::vector<int64_t> uofs((size_t)nt), pofs((size_t)nt);
+  P.parts.assign((size_t)std::max<int64_t>(nparts, 1), PartDesc{-1, 0, 0, 0});
+  P.chunks.assign((size_t)std::max<int64_t>(nchunks, 1), ChunkDesc{0, 0});
+  int64_t uo = 0, po = 0, co = 0;
+  P.n_idx_hot = P.n_idx_remote = P.n_slots_hot = P.n_slots_remote = P.n_hot_parts = P.n_window_loads = 0;
+  std::vector<int64_t> uofs((size_t)nt), pofs((size_t)nt), cofs((size_t)nt);
   for (int32_t lt = 0; lt < nt; ++lt) {
     uofs[(size_t)lt] = uo;
     pofs[(size_t)lt] = po;
+    cofs[(size_t)lt] = co;
     const TileOut& O = outs[(size_t)lt];
     TileDesc T = all[(size_t)(P.tile_begin + lt)];
     T.part0 = (int32_t)po;
+    T.nparts = (int32_t)O.parts.size();
     T.nhot = O.nhot;
-    T.nremote = O.nremote;
     P.tiles[(size_t)lt] = T;
     uo += (int64_t)O.units.size();
-    po += (int64_t)O.windows.size();
+    po += (int64_t)O.parts.size();
+    co += (int64_t)O.chunks.size();
     P.n_idx_hot += O.hot;
     P.n_idx_remote += O.rem;
     P.n_slots_hot += O.shot;
     P.n_slots_remote += O.srem;
     P.n_hot_parts += O.nhot;
+    P.n_window_loads += O.loads;
   }
 #pragma omp parallel for schedule(dynamic, 4)
   for (int32_t lt = 0; lt < nt; ++lt) {
     TileOut& O = outs[(size_t)lt];
     if (!O.units.empty()) std::memcpy(P.pool.data() + uofs[(size_t)lt], O.units.data(), O.units.size() * sizeof(Unit));
-    for (size_t p = 0; p < O.windows.size(); ++p) {
-      P.part_window[(size_t)pofs[(size_t)lt] + p] = O.windows[p];
-      P.part_neg[(size_t)pofs[(size_t)lt] + p] = O.negs[p];
-      for (int c = 0; c < CPT; ++c) {
-        ChunkDesc cd = O.chunks[p * CPT + (size_t)c];
-        if (cd.ng) cd.ofs += (uint32_t)uofs[(size_t)lt];
-        else cd.ofs = 0;
-        P.chunks[((size_t)pofs[(size_t)lt] + p) * CPT + (size_t)c] = cd;
-      }
+    for (size_t p = 0; p < O.parts.size(); ++p) {
+      PartDesc pd = O.parts[p];
+      pd.chunk0 += (uint32_t)cofs[(size_t)lt];
+      P.parts[(size_t)pofs[(size_t)lt] + p] = pd;
+    }
+    for (size_t c = 0; c < O.chunks.size(); ++c) {
+      ChunkDesc cd = O.chunks[c];
+      cd.ofs += (uint32_t)uofs[(size_t)lt];
+      P.chunks[(size_t)cofs[(size_t)lt] + c] = cd;
     }
     std::vector<Unit>().swap(O.units);
   }

@@ -1,8 +1,9 @@
 // kernels.cu — sm_100a fp64 kernels of the localised-order-parameter RHS and
 // the fused classical RK4 stages (product code).
 //
-// One CTA (16 warps, 512 threads) owns one community-aligned tile of
-// 512*RPT rows; lane l of warp w owns rows (w + 16 r)*32 + l.
+// One CTA (16 warps, 512 threads) owns one community-aligned tile of up to
+// 2048 rows whose row sums W_j live in shared memory (plan.h describes the
+// chunked, bank-conflict-free index layout).
 //
 //   k_prologue  z = e^{i theta} (= (cos, sin), P:443 / "2M" trig of P:660),
 //               per-tile partial sums of z; the last CTA reduces the partials
@@ -10,8 +11,9 @@
 //               and the order parameter r e^{i psi} = (1/N) sum_b S_b
 //               (P:236-239).
 //   k_stage     W_j = T_{c(j)} - sum_{Z_j} z_k + sum_{NZ_j} z_k:
-//               hot parts gather z from a 64 KB shared-memory window,
-//               remote parts from global memory; then
+//               hot parts gather z from a 64 KB shared-memory window
+//               (staged by a TMA bulk copy), remote parts from global
+//               memory; then
 //               k_j = omega_j + (K/N) Im(conj z_j W_j)
 //               and, fused, the RK4 stage update (acc, theta_next), the next
 //               stage's z and its per-tile partials; the last CTA forms the
@@ -25,12 +27,53 @@
 namespace kur {
 namespace {
 
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+// Index stream: read once per RHS, never reused within it -> do not allocate
+// in L1 and evict first from L2 (keeps z L2-resident for the remote gathers).
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p, uint64_t pol) {
   uint4 r;
-  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
-      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-      : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
   return r;
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// One thread: TMA bulk copy of `bytes` from global to shared memory, completion on `bar`.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void warp_sum2(double& x, double& y) {
@@ -93,35 +136,35 @@ __device__ __forceinline__ void rem4(const uint4 v, const double2* __restrict__ 
 
 // Hot part of one chunk: ng groups of 32 units starting at q (lane-offset applied).
 __device__ __forceinline__ void run_hot(const uint4* __restrict__ q, uint32_t ng, const double2* zs,
-                                        double& sx, double& sy) {
+                                        uint64_t pol, double& sx, double& sy) {
   double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
   uint32_t g = 0;
   for (; g + 4 <= ng; g += 4) {
-    const uint4 v0 = ldg_stream(q + (size_t)(g + 0) * 32);
-    const uint4 v1 = ldg_stream(q + (size_t)(g + 1) * 32);
-    const uint4 v2 = ldg_stream(q + (size_t)(g + 2) * 32);
-    const uint4 v3 = ldg_stream(q + (size_t)(g + 3) * 32);
+    const uint4 v0 = ldg_stream(q + (size_t)(g + 0) * 32, pol);
+    const uint4 v1 = ldg_stream(q + (size_t)(g + 1) * 32, pol);
+    const uint4 v2 = ldg_stream(q + (size_t)(g + 2) * 32, pol);
+    const uint4 v3 = ldg_stream(q + (size_t)(g + 3) * 32, pol);
     hot8(v0, zs, x0, y0, x1, y1);
     hot8(v1, zs, x0, y0, x1, y1);
     hot8(v2, zs, x0, y0, x1, y1);
     hot8(v3, zs, x0, y0, x1, y1);
   }
-  for (; g < ng; ++g) hot8(ldg_stream(q + (size_t)g * 32), zs, x0, y0, x1, y1);
+  for (; g < ng; ++g) hot8(ldg_stream(q + (size_t)g * 32, pol), zs, x0, y0, x1, y1);
   sx = x0 + x1;
   sy = y0 + y1;
 }
 
 __device__ __forceinline__ void run_remote(const uint4* __restrict__ q, uint32_t ng,
-                                           const double2* __restrict__ z, double& sx, double& sy) {
+                                           const double2* __restrict__ z, uint64_t pol, double& sx, double& sy) {
   double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
   uint32_t g = 0;
   for (; g + 2 <= ng; g += 2) {
-    const uint4 v0 = ldg_stream(q + (size_t)(g + 0) * 32);
-    const uint4 v1 = ldg_stream(q + (size_t)(g + 1) * 32);
+    const uint4 v0 = ldg_stream(q + (size_t)(g + 0) * 32, pol);
+    const uint4 v1 = ldg_stream(q + (size_t)(g + 1) * 32, pol);
     rem4(v0, z, x0, y0, x1, y1);
     rem4(v1, z, x0, y0, x1, y1);
   }
-  for (; g < ng; ++g) rem4(ldg_stream(q + (size_t)g * 32), z, x0, y0, x1, y1);
+  for (; g < ng; ++g) rem4(ldg_stream(q + (size_t)g * 32, pol), z, x0, y0, x1, y1);
   sx = x0 + x1;
   sy = y0 + y1;
 }
@@ -216,131 +259,115 @@ __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const
   if (threadIdx.x == 0) dp.ctrl->ticket = 0;
 }
 
-template <int RPT>
 __global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const StageArgs a) {
   __shared__ double2 red[NWARPS];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int lt = dp.order[blockIdx.x];
   const TileDesc T = dp.tiles[lt];
   double x = 0.0, y = 0.0;
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int lr = (warp + NWARPS * r) * 32 + lane;
-    if (lr < T.nrows) {
-      const int row = T.row0 + lr;
-      double s, c;
-      sincos(a.theta[row - dp.row_begin], &s, &c);
-      a.zout[row] = make_double2(c, s);
-      x += c;
-      y += s;
-    }
+  for (int lr = tid; lr < T.nrows; lr += NTHREADS) {
+    const int row = T.row0 + lr;
+    double s, c;
+    sincos(a.theta[row - dp.row_begin], &s, &c);  // z = e^{i theta}
+    a.zout[row] = make_double2(c, s);
+    x += c;
+    y += s;
   }
   tile_partial_and_finish(dp, a, lt, x, y, red);
 }
 
-template <int MODE, int RPT>
+template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const StageArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* zs = reinterpret_cast<double2*>(smem_raw);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* zs = reinterpret_cast<double2*>(smem_raw);       // [WZ + 8]: window + 8 zero sentinels
+  double2* Ws = zs + (WZ + 8);                              // [rows_per_tile]: W_j of the tile
   __shared__ double2 red[NWARPS];
+  __shared__ __align__(8) uint64_t bar;
   __shared__ int s_nonfinite;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lt = dp.order[blockIdx.x];
   const TileDesc T = dp.tiles[lt];
+  const uint64_t pol = evict_first_policy();
+  for (int r = tid; r < T.nrows; r += NTHREADS) Ws[r] = make_double2(0.0, 0.0);
+  if (tid < 8) zs[WZ + tid] = make_double2(0.0, 0.0);
   if (tid == 0) {
-    zs[WZ] = make_double2(0.0, 0.0);  // sentinel slot of padded entries
     s_nonfinite = 0;
+    mbar_init(&bar, 1);
   }
-  double ax[RPT], ay[RPT];
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) ax[r] = ay[r] = 0.0;
+  __syncthreads();
 
-  // ---- hot parts: z window staged in shared memory
+  // ---- parts: hot ones gather from the staged window, remote ones from global memory
+  uint32_t phase = 0;
   int loaded = -1;
-  for (int h = 0; h < T.nhot; ++h) {
-    const int p = T.part0 + h;
-    const PartInfo pi = dp.parts[p];
-    if (pi.window != loaded) {
-      __syncthreads();
-      const double2* src = a.zin + (size_t)pi.window * WZ;
-#pragma unroll
-      for (int i = 0; i < WZ / NTHREADS; ++i) zs[tid + i * NTHREADS] = __ldg(src + tid + i * NTHREADS);
-      __syncthreads();
-      loaded = pi.window;
+  for (int p = T.part0; p < T.part0 + T.nparts; ++p) {
+    const PartDesc P = dp.parts[p];
+    const bool hot = P.window >= 0;
+    if (hot && P.window != loaded) {  // all reads of the previous window ended at the last barrier
+      if (tid == 0) tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), &bar);
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      loaded = P.window;
     }
-    const uint2* ch = dp.chunks + (size_t)p * dp.cpt;
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const uint2 c = ch[warp + NWARPS * r];
+    // chunks of the part, snake order over the 16 warps (chunks are sorted longest first)
+    for (uint32_t r = 0;; ++r) {
+      const uint32_t c = r * NWARPS + ((r & 1) ? (NWARPS - 1 - warp) : warp);
+      if (c >= P.nchunks) break;
+      const uint2 cd = dp.chunks[P.chunk0 + c];
+      const uint4* q = dp.pool + cd.x;
+      const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
       double sx, sy;
-      run_hot(dp.pool + c.x + lane, c.y, zs, sx, sy);
-      if (pi.neg) {
-        ax[r] -= sx;
-        ay[r] -= sy;
-      } else {
-        ax[r] += sx;
-        ay[r] += sy;
+      if (hot) run_hot(q + HDR_UNITS + lane, cd.y, zs, pol, sx, sy);
+      else run_remote(q + HDR_UNITS + lane, cd.y, a.zin, pol, sx, sy);
+      if (row != EMPTY_LANE) {
+        double2 w = Ws[row];
+        if (P.neg) {
+          w.x -= sx;
+          w.y -= sy;
+        } else {
+          w.x += sx;
+          w.y += sy;
+        }
+        Ws[row] = w;
       }
     }
-  }
-  // ---- remote parts: z gathered from global memory (L2-resident)
-  for (int h = 0; h < T.nremote; ++h) {
-    const int p = T.part0 + T.nhot + h;
-    const PartInfo pi = dp.parts[p];
-    const uint2* ch = dp.chunks + (size_t)p * dp.cpt;
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const uint2 c = ch[warp + NWARPS * r];
-      double sx, sy;
-      run_remote(dp.pool + c.x + lane, c.y, a.zin, sx, sy);
-      if (pi.neg) {
-        ax[r] -= sx;
-        ay[r] -= sy;
-      } else {
-        ax[r] += sx;
-        ay[r] += sy;
-      }
-    }
+    __syncthreads();
   }
 
   // ---- finalize: k_j = omega_j + (K/N) Im(conj z_j W_j), fused RK4 stage
   const double2 Tc = a.Tin[T.comm];
   double px = 0.0, py = 0.0;
   bool bad = false;
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int lr = (warp + NWARPS * r) * 32 + lane;
-    if (lr < T.nrows) {
-      const int row = T.row0 + lr;
-      const int li = row - dp.row_begin;
-      const double wx = Tc.x + ax[r], wy = Tc.y + ay[r];
-      const double2 zj = a.zin[row];
-      const double k = a.omega[li] + a.KN * (zj.x * wy - zj.y * wx);
-      if (MODE == MODE_RHS) {
-        a.out[li] = k;
-      } else {
-        const double thn = a.theta[li];
-        double ts;
-        if (MODE == MODE_S1) {
-          a.acc[li] = k;
-          ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
-        } else if (MODE == MODE_S2) {
-          a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
-          ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
-        } else if (MODE == MODE_S3) {
-          a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
-          ts = __dadd_rn(thn, __dmul_rn(a.h, k));
-        } else {  // MODE_S4: theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
-          ts = __dadd_rn(thn, __dmul_rn(a.h / 6.0, __dadd_rn(a.acc[li], k)));
-          a.theta[li] = ts;
-          bad |= !isfinite(ts);
-        }
-        double s, c;
-        sincos(ts, &s, &c);
-        a.zout[row] = make_double2(c, s);
-        px += c;
-        py += s;
+  for (int lr = tid; lr < T.nrows; lr += NTHREADS) {
+    const int row = T.row0 + lr;
+    const int li = row - dp.row_begin;
+    const double2 w = Ws[lr];
+    const double wx = Tc.x + w.x, wy = Tc.y + w.y;
+    const double2 zj = a.zin[row];
+    const double k = a.omega[li] + a.KN * (zj.x * wy - zj.y * wx);
+    if (MODE == MODE_RHS) {
+      a.out[li] = k;
+    } else {
+      const double thn = a.theta[li];
+      double ts;
+      if (MODE == MODE_S1) {
+        a.acc[li] = k;
+        ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
+      } else if (MODE == MODE_S2) {
+        a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
+        ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
+      } else if (MODE == MODE_S3) {
+        a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
+        ts = __dadd_rn(thn, __dmul_rn(a.h, k));
+      } else {  // MODE_S4: theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
+        ts = __dadd_rn(thn, __dmul_rn(a.h / 6.0, __dadd_rn(a.acc[li], k)));
+        a.theta[li] = ts;
+        bad |= !isfinite(ts);
       }
+      double s, c;
+      sincos(ts, &s, &c);
+      a.zout[row] = make_double2(c, s);
+      px += c;
+      py += s;
     }
   }
   if (MODE == MODE_RHS) return;
@@ -364,41 +391,26 @@ __global__ void k_permute(const int32_t* __restrict__ perm, int64_t n, const dou
   else out[perm[i]] = in[i];
 }
 
-template <int MODE, int RPT>
-cudaError_t launch_stage_t(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
+template <int MODE>
+cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
   static bool attr_set = false;
-  const size_t smem = stage_smem_bytes();
+  const size_t smem = stage_smem_bytes(MAX_TILE_ROWS);
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage<MODE, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_stage<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_stage<MODE, RPT><<<dp.ntiles, NTHREADS, smem, s>>>(dp, a);
+  k_stage<MODE><<<dp.ntiles, NTHREADS, stage_smem_bytes(dp.rows_per_tile), s>>>(dp, a);
   return cudaGetLastError();
-}
-
-template <int MODE>
-cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
-  switch (dp.rpt) {
-    case 1: return launch_stage_t<MODE, 1>(dp, a, s);
-    case 2: return launch_stage_t<MODE, 2>(dp, a, s);
-    case 4: return launch_stage_t<MODE, 4>(dp, a, s);
-    default: return cudaErrorInvalidValue;
-  }
 }
 
 }  // namespace
 
-size_t stage_smem_bytes() { return sizeof(double2) * (WZ + 1); }
+size_t stage_smem_bytes(int rows_per_tile) { return sizeof(double2) * (size_t)(WZ + 8 + rows_per_tile); }
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
   if (dp.ntiles <= 0) return cudaSuccess;
-  switch (dp.rpt) {
-    case 1: k_prologue<1><<<dp.ntiles, NTHREADS, 0, s>>>(dp, a); break;
-    case 2: k_prologue<2><<<dp.ntiles, NTHREADS, 0, s>>>(dp, a); break;
-    case 4: k_prologue<4><<<dp.ntiles, NTHREADS, 0, s>>>(dp, a); break;
-    default: return cudaErrorInvalidValue;
-  }
+  k_prologue<<<dp.ntiles, NTHREADS, 0, s>>>(dp, a);
   return cudaGetLastError();
 }
 

@@ -17,23 +17,18 @@ struct Ctrl {             // device-resident control block
   double rpsi[2];         // last computed (r, psi)
 };
 
-struct PartInfo {         // 8 bytes; device array [n_parts]
-  int32_t window;         // window id (hot) or -1 (remote)
-  int32_t neg;            // 1: entries are complements (subtracted), 0: non-zeros (added)
-};
-
 struct DevPlan {
   int64_t n;              // global N
   int32_t C;
-  int32_t rpt, cpt;       // rows per thread, chunks per tile
+  int32_t rows_per_tile;  // <= MAX_TILE_ROWS
   int32_t ntiles;         // local tiles (one CTA each)
   int32_t tile_base;      // global id of local tile 0
   int32_t row_begin;      // internal id of local row 0
   int32_t world;
   const TileDesc* tiles;      // [ntiles]
   const int32_t* order;       // [ntiles] launch order
-  const PartInfo* parts;      // [n_parts]
-  const uint2* chunks;        // [n_parts * cpt]
+  const PartDesc* parts;      // [n_parts]
+  const uint2* chunks;        // [n_chunks] {header offset, groups}
   const uint4* pool;          // index units
   const int32_t* comm_tile0;  // [C+1] global tile ids
   const int32_t* D_ptr;       // [C+1]
@@ -69,6 +64,6 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
 cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, cudaStream_t s);
 cudaError_t launch_permute(const int32_t* perm, int64_t n, const double* in, double* out, int dir,
                            cudaStream_t s);
-size_t stage_smem_bytes();
+size_t stage_smem_bytes(int rows_per_tile);
 
 }  // namespace kur

@@ -4,23 +4,30 @@
 // Layout in HBM.  Internal numbering: communities contiguous
 // in label order (the permutation P of P:644-650), inside a community rows
 // sorted by decreasing list length.  Rows are cut into community-aligned
-// TILES of rows_per_tile = 512*rpt rows; one CTA (16 warps) owns a tile and
-// lane l of warp w owns rows (w + 16 r)*32 + l, r < rpt ("chunk" = 32 rows).
+// TILES of at most 2048 rows; one CTA (16 warps) owns a tile and keeps the
+// row sums W_j of the tile in shared memory.
 //
 // Per row j the stored list is the complement list Z_j of its dense blocks
 // (subtracted) and the non-zero list NZ_j of its sparse blocks (added)
 // (P:538-570).  The column space is cut into WINDOWS of WZ = 4096 columns
 // (64 KB of z).  For each tile the windows that hold at least hot_min of the
-// tile's entries are HOT: the CTA stages z[window] in shared memory and the
-// entries are stored as 16-bit window-local indices.  All other entries are
-// REMOTE, stored as 32-bit column ids and gathered from global memory.  A
-// PART is one (hot window | remote, sign) pair of a tile, so the sign is
-// uniform inside a part and costs nothing per entry.
+// tile's entries are HOT: the CTA stages z[window] in shared memory (TMA bulk
+// copy) and the entries are 16-bit window-local slots.  All other entries are
+// REMOTE: 32-bit column ids gathered from global memory.  A PART is one
+// (hot window | remote, sign) pair of a tile, so the sign is uniform inside a
+// part and costs nothing per entry.
 //
-// A part's data is a list of 16-byte units; for chunk c of the tile it is
-// ng groups of 32 units, unit (g, lane) holding the entries 8g..8g+7 (hot)
-// or 4g..4g+3 (remote) of the lane's row, padded with a sentinel that points
-// at a zero z entry.
+// Inside a part the rows that have entries are sorted by their entry count
+// (longest first) and cut into CHUNKS of 32 rows, one row per lane, so the
+// rows of a chunk have nearly equal lengths (little padding).  A chunk is a
+// 64-byte header (32 x uint16 local row ids, 0xFFFF = empty lane) followed by
+// ng groups of 32 16-byte units; unit (g, lane) holds the lane's entries at
+// positions 8g..8g+7 (hot) or 4g..4g+3 (remote).  In hot parts the entries of
+// every quarter-warp (lanes 8q..8q+7) at one position have pairwise distinct
+// slot residues mod 8, i.e. they hit distinct 16-byte shared-memory bank
+// groups: every LDS.128 of the gather loop is bank-conflict free.  Padding
+// slots point at zero sentinels WZ + rho (one per residue rho), remote padding
+// at z[n] = 0.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -34,23 +41,33 @@ constexpr int WZ_SHIFT = 12;
 constexpr int WZ = 1 << WZ_SHIFT;  // columns per shared-memory window (64 KB of double2)
 constexpr int NWARPS = 16;         // warps per CTA
 constexpr int NTHREADS = NWARPS * 32;
-constexpr int MAX_RPT = 4;         // rows per thread (tile rows = 512 * rpt)
-constexpr uint32_t HOT_SENT = WZ;  // window-local sentinel slot (always zero)
-constexpr int DEFAULT_HOT_MIN = 1024;
+constexpr uint32_t HOT_SENT = WZ;  // first of the 8 zero sentinel slots WZ..WZ+7
+constexpr int DEFAULT_HOT_MIN = 2048;
+
+constexpr int MAX_TILE_ROWS = 2048;  // W_j of a tile live in shared memory (32 KB)
+constexpr int HDR_UNITS = 4;         // 64-byte chunk header
+constexpr uint16_t EMPTY_LANE = 0xFFFF;
 
 struct TileDesc {   // 32 bytes; device array
   int32_t row0;     // first internal row (global numbering)
   int32_t nrows;    // rows in this tile (<= rows_per_tile)
   int32_t comm;     // community of every row of the tile
   int32_t part0;    // first part of the tile
-  int32_t nhot;     // hot parts (part0 .. part0+nhot-1)
-  int32_t nremote;  // 0..2 remote parts (after the hot parts)
+  int32_t nparts;   // hot parts first (by window), then remote parts
+  int32_t nhot;     // number of hot parts
   int32_t pad0, pad1;
 };
 
-struct ChunkDesc {  // 8 bytes; device array [n_parts * chunks_per_tile]
-  uint32_t ofs;     // offset of the chunk's first unit (16-byte units) in the pool
-  uint32_t ng;      // groups (each group = 32 units)
+struct PartDesc {   // 16 bytes; device array
+  int32_t window;   // window id (hot) or -1 (remote)
+  int32_t neg;      // 1: complement entries (subtracted), 0: non-zero entries (added)
+  uint32_t chunk0;  // first chunk in the chunk table
+  uint32_t nchunks;
+};
+
+struct ChunkDesc {  // 8 bytes; device array
+  uint32_t ofs;     // pool offset (16-byte units) of the chunk header
+  uint32_t ng;      // groups after the header (each group = 32 units)
 };
 
 struct Unit {       // 16 bytes of the pool
@@ -60,7 +77,7 @@ struct Unit {       // 16 bytes of the pool
 struct HostPlan {
   int64_t n = 0;
   int32_t C = 0;
-  int rpt = 1, rows_per_tile = NTHREADS, chunks_per_tile = NWARPS;
+  int rows_per_tile = NTHREADS;
   int32_t rank = 0, world = 1;
   int64_t row_begin = 0, row_end = 0;     // this rank's internal rows
   int32_t tile_begin = 0, tile_end = 0;   // this rank's tiles (global ids)
@@ -70,9 +87,8 @@ struct HostPlan {
   std::vector<int32_t> comm_tile0;  // [C+1] tile offsets (global tile ids)
   std::vector<int32_t> D_ptr, D_idx;  // dense column communities of each row community
   std::vector<TileDesc> tiles;      // this rank's tiles (parts renumbered locally)
-  std::vector<int32_t> part_window; // [n_parts] window id (-1 = remote)
-  std::vector<int32_t> part_neg;    // [n_parts] 1 = complement entries (subtracted)
-  std::vector<ChunkDesc> chunks;    // [n_parts * chunks_per_tile]
+  std::vector<PartDesc> parts;      // this rank's parts
+  std::vector<ChunkDesc> chunks;    // this rank's chunks
   std::vector<Unit> pool;           // index data
   std::vector<int32_t> tile_order;  // launch order (local tile ids, decreasing work)
   std::vector<int32_t> shard_row0;  // [world+1] internal row ranges of all ranks
@@ -80,6 +96,7 @@ struct HostPlan {
   // statistics (this rank)
   int64_t nnz = 0, n_idx_hot = 0, n_idx_remote = 0, n_slots_hot = 0, n_slots_remote = 0;
   int64_t n_dense_blocks = 0, n_sparse_blocks = 0, n_hot_parts = 0;
+  int64_t n_window_loads = 0;       // hot windows staged per RHS (all tiles)
 };
 
 // Builds the plan on the host.  `sm_count` steers the tile size choice.

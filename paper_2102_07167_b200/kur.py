@@ -49,7 +49,7 @@ class GraphInfo(ctypes.Structure):
                 ("rows_per_tile", _i32), ("row_begin", _i64), ("row_end", _i64), ("nnz", _i64),
                 ("n_idx", _i64), ("n_idx_hot", _i64), ("n_idx_remote", _i64), ("n_slots_hot", _i64),
                 ("n_slots_remote", _i64), ("n_dense_blocks", _i64), ("n_sparse_blocks", _i64),
-                ("n_tiles", _i64), ("n_hot_parts", _i64), ("sincos_per_rhs", _i64),
+                ("n_tiles", _i64), ("n_hot_parts", _i64), ("n_window_loads", _i64), ("sincos_per_rhs", _i64),
                 ("bytes_per_rhs", _i64), ("bytes_pool", _i64), ("build_seconds", _d)]
 
 
@@ -163,7 +163,7 @@ class Graph:
         return x_internal_full[self.row_begin:self.row_end]
 
 
-def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, rpt=0, device=None, dist=None, **arrays):
+def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, device=None, dist=None, **arrays):
     """kur_graph_build from a kurgen.Instance (or the same arrays as keywords)."""
     src = arrays if inst is None else dict(
         n=inst.n, n_comm=inst.n_comm, community=inst.community, seg_ptr=inst.seg_ptr,
@@ -179,7 +179,7 @@ def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, rpt=0, device=Non
                      community=_np_ptr(keep["community"]), seg_ptr=_np_ptr(keep["seg_ptr"]),
                      seg_comm=_np_ptr(keep["seg_comm"]), seg_kind=_np_ptr(keep["seg_kind"]),
                      idx_ptr=_np_ptr(keep["idx_ptr"]), idx=_np_ptr(keep["idx"]),
-                     dense_threshold=float(dense_threshold), hot_min=int(hot_min), flags=int(rpt))
+                     dense_threshold=float(dense_threshold), hot_min=int(hot_min), flags=int(tile_rows))
     if device is None:
         device = torch.cuda.current_device()
     dd = None
@@ -267,7 +267,7 @@ for _f in ("kur_plan_build", "kur_plan_sizes", "kur_plan_export", "kur_plan_dest
 EXPORTED = EXPORTED + ("kur_plan_build", "kur_plan_sizes", "kur_plan_export", "kur_plan_destroy")
 
 
-def _desc_from(inst, dense_threshold=-1.0, hot_min=0, rpt=0):
+def _desc_from(inst, dense_threshold=-1.0, hot_min=0, tile_rows=0):
     keep = dict(
         community=np.ascontiguousarray(inst.community, np.int32),
         seg_ptr=np.ascontiguousarray(inst.seg_ptr, np.int64),
@@ -279,19 +279,19 @@ def _desc_from(inst, dense_threshold=-1.0, hot_min=0, rpt=0):
                      seg_ptr=_np_ptr(keep["seg_ptr"]), seg_comm=_np_ptr(keep["seg_comm"]),
                      seg_kind=_np_ptr(keep["seg_kind"]), idx_ptr=_np_ptr(keep["idx_ptr"]),
                      idx=_np_ptr(keep["idx"]), dense_threshold=float(dense_threshold),
-                     hot_min=int(hot_min), flags=int(rpt))
+                     hot_min=int(hot_min), flags=int(tile_rows))
     return desc, keep
 
 
-def plan_export(inst, *, rank=0, world=1, sm_count=148, dense_threshold=-1.0, hot_min=0, rpt=0):
+def plan_export(inst, *, rank=0, world=1, sm_count=148, dense_threshold=-1.0, hot_min=0, tile_rows=0):
     """Host-only: build the block plan and decode its stored layout (see kur.h)."""
-    desc, keep = _desc_from(inst, dense_threshold, hot_min, rpt)
+    desc, keep = _desc_from(inst, dense_threshold, hot_min, tile_rows)
     h = ctypes.c_void_p()
     _check(_lib.kur_plan_build(ctypes.byref(desc), rank, world, sm_count, ctypes.byref(h)))
     try:
-        sz = np.zeros(10, np.int64)
+        sz = np.zeros(16, np.int64)
         _check(_lib.kur_plan_sizes(h, _np_ptr(sz)))
-        n, C, nl, rb, ne, nd, nt, rpt_rows, nnz, w = (int(x) for x in sz)
+        n, C, nl, rb, ne, nd, nt, rpt_rows, nnz, w = (int(x) for x in sz[:10])
         out = dict(n=n, n_comm=C, n_local=nl, row_begin=rb, n_tiles=nt, rows_per_tile=rpt_rows, nnz=nnz,
                    perm=np.empty(n, np.int32), D_ptr=np.empty(C + 1, np.int32),
                    D_idx=np.empty(max(nd, 1), np.int32), row_ptr=np.empty(nl + 1, np.int64),
@@ -302,6 +302,9 @@ def plan_export(inst, *, rank=0, world=1, sm_count=148, dense_threshold=-1.0, ho
         out["D_idx"] = out["D_idx"][:nd]
         out["cols"] = out["cols"][:ne]
         out["neg"] = out["neg"][:ne]
+        _check(_lib.kur_plan_sizes(h, _np_ptr(sz)))
+        out.update(conflicts=int(sz[10]), slots_hot=int(sz[11]), idx_hot=int(sz[12]), slots_remote=int(sz[13]),
+                   idx_remote=int(sz[14]), window_loads=int(sz[15]))
         return out
     finally:
         _lib.kur_plan_destroy(h)

@@ -38,6 +38,7 @@ def check_plan(inst, A, **kw):
         assert sorted(perm.tolist()) == list(range(inst.n))
         lab_int = inst.community[perm]
         assert np.all(np.diff(lab_int) >= 0), "communities must be contiguous"
+        assert plan["conflicts"] == 0, "hot gathers must be bank-conflict free"
         rows = reconstruct(inst, plan)
         for lj in range(plan["n_local"]):
             j = plan["row_begin"] + lj
@@ -92,8 +93,10 @@ def test_roundtrip_many_tiles_ragged():
     A = inst.dense()
     plan = check_plan(inst, A)
     assert plan["n_tiles"] > 4
-    plan2 = check_plan(inst, A, sm_count=1)  # fewer SMs -> larger tiles (rows per thread > 1)
-    assert plan2["rows_per_tile"] > 512
+    plan2 = check_plan(inst, A, sm_count=1)  # fewer SMs -> larger tiles
+    assert plan2["rows_per_tile"] == 2048
+    for tr in (32, 96, 512):
+        assert check_plan(inst, A, tile_rows=tr)["rows_per_tile"] == tr
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -185,6 +188,23 @@ def test_error_codes():
     assert _build_status(thr=1.5) == 1                  # threshold > 1
     assert _build_status(n=0) == 1                      # n < 1
     assert _build_status(idx_ptr=[0, 1, 0, 3, 4]) == 5  # idx_ptr not monotone -> SIZE_MISMATCH
+
+
+def test_bad_tile_rows_flag():
+    A = np.ones((4, 4), np.uint8)
+    inst = kurgen.from_dense(A, [0, 0, 0, 0])
+    for bad in (31, 4096, 100):
+        with pytest.raises(kur.KurError) as e:
+            kur.plan_export(inst, tile_rows=bad)
+        assert e.value.status == 1
+
+
+def test_padding_is_small_on_sbm():
+    """Per-part row sorting + bank-aware arrangement keep hot padding small."""
+    inst = kurgen.sbm([8192, 8192], [[0.98, 2e-4], [2e-4, 0.98]], 77)
+    plan = kur.plan_export(inst)
+    assert plan["conflicts"] == 0
+    assert plan["slots_hot"] <= 1.30 * plan["idx_hot"], (plan["slots_hot"], plan["idx_hot"])
 
 
 def test_duplicate_and_unsorted_lists():

@@ -73,15 +73,15 @@ def test_rhs_small_random(cfg, kind, thr):
 
 
 @pytest.mark.parametrize("hot_min", [1, 1 << 30])
-@pytest.mark.parametrize("rpt", [1, 2, 4])
-def test_rhs_layout_variants(hot_min, rpt):
-    """All-hot / all-remote layouts and 1/2/4 rows per thread give the same RHS."""
+@pytest.mark.parametrize("tile_rows", [32, 512, 2048])
+def test_rhs_layout_variants(hot_min, tile_rows):
+    """All-hot / all-remote layouts and several tile sizes give the same RHS."""
     inst = kurgen.sbm([2100, 700, 5000, 1, 33, 0, 900], np.array(
         [[0.97, 0.3, 0.001, 0.0, 0.9, 0, 0.0], [0.3, 0.6, 0.0, 0.5, 0.0, 0, 0.01],
          [0.001, 0.0, 0.02, 0.0, 0.3, 0, 0.0], [0.0, 0.5, 0.0, 0.0, 0.0, 0, 0.0],
          [0.9, 0.0, 0.3, 0.0, 1.0, 0, 0.0], [0] * 7, [0.0, 0.01, 0.0, 0.0, 0.0, 0, 0.99]]), 13, K=3.0)
     ref = oracle.rhs(oracle.Graph(inst), inst.theta0, inst.omega, inst.K, mode="naive")
-    got = Run(inst, hot_min=hot_min, rpt=rpt).rhs()
+    got = Run(inst, hot_min=hot_min, tile_rows=tile_rows).rhs()
     ok, err = close(got, ref, abs_tol=1e-13, rel_tol=1e-12)
     assert ok, err
 
