@@ -202,7 +202,7 @@ def test_bad_tile_rows_flag():
 def test_padding_is_small_on_sbm():
     """Per-part row sorting + bank-aware arrangement keep hot padding small."""
     inst = kurgen.sbm([8192, 8192], [[0.98, 2e-4], [2e-4, 0.98]], 77)
-    plan = kur.plan_export(inst)
+    plan = kur.plan_export(inst, tile_rows=2048)
     assert plan["conflicts"] == 0
     assert plan["slots_hot"] <= 1.30 * plan["idx_hot"], (plan["slots_hot"], plan["idx_hot"])
 
