@@ -13,6 +13,7 @@
 //     non-zero lists NZ_j (sparse blocks, added) in the chunked
 //     16-bit / 32-bit layout of plan.h.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -99,6 +100,157 @@ void enumerate_row(const Src& S, const std::vector<int32_t>& D_ptr, const std::v
     }
     if (seg) ++s;
     if (dense) ++di;
+  }
+}
+
+
+// Form the chunks of a hot part.  Rows (ord, longest first) are taken in
+// pools of 128; each pool is split greedily into 16 quarter-warps of 8 rows
+// whose per-residue totals (slot mod 8) are balanced, because a quarter's
+// conflict-free schedule needs max(longest row, largest residue total)
+// positions; quarters are then sorted by that bound and grouped 4 per chunk.
+template <class CountFn>
+void plan_pools(const std::vector<int32_t>& ord, const std::vector<int32_t>& cnt,
+                std::vector<std::array<int32_t, 32>>& lanes, CountFn count) {
+  constexpr int POOL = 128, NQ = POOL / 8;
+  for (size_t p0 = 0; p0 < ord.size(); p0 += POOL) {
+    const int np = (int)std::min<size_t>(POOL, ord.size() - p0);
+    const int nq = (np + 7) / 8;
+    int cv[POOL][8];
+    std::memset(cv, 0, sizeof(cv));
+    for (int i = 0; i < np; ++i) count(ord[p0 + (size_t)i], cv[i]);
+    int qt[NQ][8], qf[NQ], qlen[NQ], qm[NQ][8];
+    std::memset(qt, 0, sizeof(qt));
+    std::memset(qf, 0, sizeof(qf));
+    std::memset(qlen, 0, sizeof(qlen));
+    for (int i = 0; i < np; ++i) {
+      int bq = -1;
+      long bmx = 0, bss = 0;
+      for (int q = 0; q < nq; ++q) {
+        if (qf[q] == 8) continue;
+        long mx = std::max(qlen[q], cnt[(size_t)ord[p0 + (size_t)i]]), ss = 0;
+        for (int r = 0; r < 8; ++r) {
+          const long v = qt[q][r] + cv[i][r];
+          mx = std::max(mx, v);
+          ss += v * v;
+        }
+        if (bq < 0 || mx < bmx || (mx == bmx && ss < bss)) { bq = q; bmx = mx; bss = ss; }
+      }
+      for (int r = 0; r < 8; ++r) qt[bq][r] += cv[i][r];
+      qlen[bq] = std::max(qlen[bq], cnt[(size_t)ord[p0 + (size_t)i]]);
+      qm[bq][qf[bq]++] = ord[p0 + (size_t)i];
+    }
+    int qord[NQ], qb[NQ];
+    for (int q = 0; q < nq; ++q) {
+      qord[q] = q;
+      qb[q] = qlen[q];
+      for (int r = 0; r < 8; ++r) qb[q] = std::max(qb[q], qt[q][r]);
+    }
+    std::sort(qord, qord + nq, [&](int x, int y) { return qb[x] > qb[y]; });
+    for (int c = 0; c * 4 < nq; ++c) {
+      std::array<int32_t, 32> a;
+      a.fill(-1);
+      for (int k = 0; k < 4 && c * 4 + k < nq; ++k) {
+        const int q = qord[c * 4 + k];
+        for (int m = 0; m < qf[q]; ++m) a[(size_t)(k * 8 + m)] = qm[q][m];
+      }
+      lanes.push_back(a);
+    }
+  }
+}
+
+// Schedule the entries of one quarter-warp (lst[lane][residue] = window slots)
+// into positions of 8 slots with pairwise distinct residues (one 16-byte bank
+// group per lane: conflict-free LDS.128).  Bipartite edge colouring of the
+// lane x residue multigraph: at each position a matching that covers every
+// "critical" lane / residue (remaining degree = remaining positions), found
+// with augmenting paths, so the schedule length stays at the lower bound
+// max(lane length, residue total) (Koenig's edge-colouring theorem).
+// Unused lanes of a position get the zero sentinel of a free residue.
+void schedule_quarter(std::vector<uint16_t> (&lst)[8][8], std::vector<uint32_t>& P8) {
+  P8.clear();
+  int c8[8][8], rem[8] = {0}, tot[8] = {0};
+  for (int l = 0; l < 8; ++l)
+    for (int r = 0; r < 8; ++r) {
+      c8[l][r] = (int)lst[l][r].size();
+      rem[l] += c8[l][r];
+      tot[r] += c8[l][r];
+    }
+  int Lb = 0;
+  for (int i = 0; i < 8; ++i) Lb = std::max(Lb, std::max(rem[i], tot[i]));
+  int asg[8], owner[8], adj[8];
+  std::function<bool(int, int&, int)> aug_lane = [&](int x, int& seen, int crit_r) -> bool {
+    // residues: critical first, then by remaining total (scarce residues are the bottleneck)
+    int order[8];
+    for (int r = 0; r < 8; ++r) order[r] = r;
+    std::sort(order, order + 8, [&](int u, int v) {
+      const int cu = (crit_r >> u) & 1, cvv = (crit_r >> v) & 1;
+      if (cu != cvv) return cu > cvv;
+      return tot[u] > tot[v];
+    });
+    for (int k = 0; k < 8; ++k) {
+      const int r = order[k];
+      if (!((adj[x] >> r) & 1) || ((seen >> r) & 1)) continue;
+      seen |= 1 << r;
+      if (owner[r] < 0 || aug_lane(owner[r], seen, crit_r)) { owner[r] = x; asg[x] = r; return true; }
+    }
+    return false;
+  };
+  std::function<bool(int, int&)> aug_res = [&](int y, int& seenl) -> bool {
+    for (int x = 0; x < 8; ++x) {
+      if (!((adj[x] >> y) & 1) || ((seenl >> x) & 1)) continue;
+      seenl |= 1 << x;
+      if (asg[x] < 0 || aug_res(asg[x], seenl)) { asg[x] = y; owner[y] = x; return true; }
+    }
+    return false;
+  };
+  for (int pos = 0;; ++pos) {
+    int any = 0;
+    for (int l = 0; l < 8; ++l) any |= rem[l];
+    if (!any) break;
+    const int R = std::max(Lb - pos, 1);
+    int crit_l = 0, crit_r = 0;
+    for (int i = 0; i < 8; ++i) {
+      if (rem[i] >= R) crit_l |= 1 << i;
+      if (tot[i] >= R) crit_r |= 1 << i;
+      asg[i] = owner[i] = -1;
+      adj[i] = 0;
+      for (int r = 0; r < 8; ++r)
+        if (c8[i][r] > 0) adj[i] |= 1 << r;
+    }
+    int lord[8];
+    for (int i = 0; i < 8; ++i) lord[i] = i;
+    std::sort(lord, lord + 8, [&](int u, int v) { return rem[u] > rem[v]; });
+    for (int k = 0; k < 8; ++k) {  // 1) critical lanes
+      const int x = lord[k];
+      if ((crit_l >> x) & 1) { int seen = 0; aug_lane(x, seen, crit_r); }
+    }
+    for (int y = 0; y < 8; ++y)  // 2) critical residues (never unmatches a lane)
+      if (((crit_r >> y) & 1) && owner[y] < 0) { int seenl = 0; aug_res(y, seenl); }
+    for (int k = 0; k < 8; ++k) {  // 3) everybody else, longest first
+      const int x = lord[k];
+      if (rem[x] && asg[x] < 0) { int seen = 0; aug_lane(x, seen, crit_r); }
+    }
+    int used = 0;
+    for (int l = 0; l < 8; ++l)
+      if (asg[l] >= 0) used |= 1 << asg[l];
+    for (int l = 0; l < 8; ++l) {
+      uint32_t v;
+      if (asg[l] >= 0) {
+        const int r = asg[l];
+        v = lst[l][r].back();
+        lst[l][r].pop_back();
+        c8[l][r]--;
+        rem[l]--;
+        tot[r]--;
+      } else {
+        int r = 0;
+        while ((used >> r) & 1) ++r;
+        used |= 1 << r;
+        v = HOT_SENT + (uint32_t)r;
+      }
+      P8.push_back(v);
+    }
   }
 }
 
@@ -396,90 +548,48 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
         std::vector<int32_t> ord(rows.size());
         std::iota(ord.begin(), ord.end(), 0);
         std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return cnt[(size_t)x] > cnt[(size_t)y]; });
-        for (size_t c0 = 0; c0 < ord.size(); c0 += 32) {
-          const int nl = (int)std::min<size_t>(32, ord.size() - c0);
+        auto slot_of = [&](int32_t ri, int e) -> uint32_t {
+          return (uint32_t)((src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) - (uint64_t)window * WZ);
+        };
+        // chunks (lane -> row); hot parts: residue-balanced quarter-warps from 128-row pools
+        std::vector<std::array<int32_t, 32>> lanes;
+        if (hot) {
+          plan_pools(ord, cnt, lanes, [&](int32_t ri, int* cv) {
+            for (int e = 0; e < cnt[(size_t)ri]; ++e) cv[slot_of(ri, e) & 7]++;
+          });
+        } else {
+          for (size_t c0 = 0; c0 < ord.size(); c0 += 32) {
+            std::array<int32_t, 32> a;
+            for (int l = 0; l < 32; ++l) a[(size_t)l] = c0 + (size_t)l < ord.size() ? ord[c0 + (size_t)l] : -1;
+            lanes.push_back(a);
+          }
+        }
+        for (const std::array<int32_t, 32>& lane_row : lanes) {
           ChunkDesc cd{(uint32_t)O.units.size(), 0};
-          // header: local row id per lane
           Unit hdr[HDR_UNITS];
           uint16_t* h16 = reinterpret_cast<uint16_t*>(hdr);
           for (int l = 0; l < 32; ++l)
-            h16[l] = l < nl ? (uint16_t)((src[k0 + (size_t)rb[(size_t)ord[c0 + (size_t)l]]] >> 32) & 0x7FF) : EMPTY_LANE;
+            h16[l] = lane_row[(size_t)l] >= 0 ? (uint16_t)((src[k0 + (size_t)rb[(size_t)lane_row[(size_t)l]]] >> 32) & 0x7FF)
+                                             : EMPTY_LANE;
           O.units.insert(O.units.end(), hdr, hdr + HDR_UNITS);
           const size_t gbase = O.units.size();
           if (hot) {
-            // bank-conflict-free arrangement, one quarter-warp (8 lanes) at a time
+            // bank-conflict-free schedule, one quarter-warp (8 lanes) at a time
             std::vector<std::vector<uint32_t>> qpos(4);
             size_t L = 0;
             for (int q = 0; q < 4; ++q) {
-              int rem[8] = {0}, tot[8] = {0}, c8[8][8];
               for (int l = 0; l < 8; ++l)
-                for (int r = 0; r < 8; ++r) { lst[l][r].clear(); c8[l][r] = 0; }
+                for (int r = 0; r < 8; ++r) lst[l][r].clear();
               for (int l = 0; l < 8; ++l) {
-                const int lane = q * 8 + l;
-                if (lane >= nl) continue;
-                const int32_t ri = ord[c0 + (size_t)lane];
+                const int32_t ri = lane_row[(size_t)(q * 8 + l)];
+                if (ri < 0) continue;
                 for (int e = 0; e < cnt[(size_t)ri]; ++e) {
-                  const uint32_t slot = (uint32_t)((src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) - (uint64_t)window * WZ);
+                  const uint32_t slot = slot_of(ri, e);
                   lst[l][slot & 7].push_back((uint16_t)slot);
-                  c8[l][slot & 7]++;
-                  rem[l]++;
-                  tot[slot & 7]++;
                 }
               }
-              std::vector<uint32_t>& P8 = qpos[(size_t)q];
-              for (;;) {
-                int any = 0;
-                for (int l = 0; l < 8; ++l) any |= rem[l];
-                if (!any) break;
-                int asg[8], owner[8];
-                for (int i = 0; i < 8; ++i) { asg[i] = -1; owner[i] = -1; }
-                int ordl[8];
-                for (int i = 0; i < 8; ++i) ordl[i] = i;
-                std::sort(ordl, ordl + 8, [&](int x, int y) { return rem[x] > rem[y]; });
-                for (int oi = 0; oi < 8; ++oi) {  // greedy: scarce-residue first
-                  const int l = ordl[oi];
-                  if (!rem[l]) continue;
-                  int best = -1, bs = -1;
-                  for (int r = 0; r < 8; ++r)
-                    if (owner[r] < 0 && c8[l][r] > 0 && tot[r] * 4096 + c8[l][r] > bs) { bs = tot[r] * 4096 + c8[l][r]; best = r; }
-                  if (best >= 0) { asg[l] = best; owner[best] = l; }
-                }
-                // augmenting paths (Kuhn) for lanes still unmatched
-                for (int oi = 0; oi < 8; ++oi) {
-                  const int l = ordl[oi];
-                  if (!rem[l] || asg[l] >= 0) continue;
-                  int seen = 0;
-                  std::function<bool(int)> aug = [&](int x) -> bool {
-                    for (int r = 0; r < 8; ++r) {
-                      if (c8[x][r] <= 0 || (seen >> r & 1)) continue;
-                      seen |= 1 << r;
-                      if (owner[r] < 0 || aug(owner[r])) { owner[r] = x; asg[x] = r; return true; }
-                    }
-                    return false;
-                  };
-                  aug(l);
-                }
-                int used = 0;
-                for (int l = 0; l < 8; ++l) if (asg[l] >= 0) used |= 1 << asg[l];
-                for (int l = 0; l < 8; ++l) {
-                  uint32_t v;
-                  if (asg[l] >= 0) {
-                    const int r = asg[l];
-                    v = lst[l][r].back();
-                    lst[l][r].pop_back();
-                    c8[l][r]--;
-                    rem[l]--;
-                    tot[r]--;
-                  } else {
-                    int r = 0;
-                    while (used >> r & 1) ++r;
-                    used |= 1 << r;
-                    v = HOT_SENT + (uint32_t)r;
-                  }
-                  P8.push_back(v);
-                }
-              }
-              L = std::max(L, P8.size() / 8);
+              schedule_quarter(lst, qpos[(size_t)q]);
+              L = std::max(L, qpos[(size_t)q].size() / 8);
             }
             const uint32_t ng = (uint32_t)((L + 7) / 8);
             cd.ng = ng;
@@ -498,7 +608,8 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
             O.shot += (int64_t)ng * 256;
           } else {
             int mx = 0;
-            for (int l = 0; l < nl; ++l) mx = std::max(mx, cnt[(size_t)ord[c0 + (size_t)l]]);
+            for (int l = 0; l < 32; ++l)
+              if (lane_row[(size_t)l] >= 0) mx = std::max(mx, cnt[(size_t)lane_row[(size_t)l]]);
             const uint32_t ng = (uint32_t)((mx + 3) / 4);
             cd.ng = ng;
             O.units.resize(gbase + (size_t)ng * 32);
@@ -508,10 +619,8 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
                 for (int e = 0; e < 4; ++e) {
                   const int p = (int)g * 4 + e;
                   uint32_t v = SENT_REMOTE;
-                  if (lane < nl) {
-                    const int32_t ri = ord[c0 + (size_t)lane];
-                    if (p < cnt[(size_t)ri]) v = (uint32_t)(src[k0 + (size_t)rb[(size_t)ri] + (size_t)p] & COLM);
-                  }
+                  const int32_t ri = lane_row[(size_t)lane];
+                  if (ri >= 0 && p < cnt[(size_t)ri]) v = (uint32_t)(src[k0 + (size_t)rb[(size_t)ri] + (size_t)p] & COLM);
                   U.w[e] = v;
                 }
               }

@@ -204,7 +204,7 @@ def test_padding_is_small_on_sbm():
     inst = kurgen.sbm([8192, 8192], [[0.98, 2e-4], [2e-4, 0.98]], 77)
     plan = kur.plan_export(inst, tile_rows=2048)
     assert plan["conflicts"] == 0
-    assert plan["slots_hot"] <= 1.30 * plan["idx_hot"], (plan["slots_hot"], plan["idx_hot"])
+    assert plan["slots_hot"] <= 1.16 * plan["idx_hot"], (plan["slots_hot"], plan["idx_hot"])
 
 
 def test_duplicate_and_unsorted_lists():
