@@ -180,19 +180,24 @@ def main():
     from paper_2102_07167_b200 import kur
 
     world, rank, local = _dist()
-    if world > 1:
-        raise SystemExit("multi-GPU sharded path not yet available in this build")
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     t0 = time.perf_counter()
     inst = kurgen.config(args.config)
     gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    g = kur.graph_build(inst, device=local)
+    if world > 1:
+        obj = [kur.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        g = kur.graph_build(inst, device=local, dist=(rank, world, obj[0]))
+    else:
+        g = kur.graph_build(inst, device=local)
     build_s = time.perf_counter() - t0
     info = g.info
-    th = g.to_internal(torch.from_numpy(inst.theta0).to(dev))
-    om = g.to_internal(torch.from_numpy(inst.omega).to(dev))
+    th = g.local(g.to_internal(torch.from_numpy(inst.theta0).to(dev))).clone()
+    om = g.local(g.to_internal(torch.from_numpy(inst.omega).to(dev))).clone()
     K, h = inst.K, inst.h
     stream = torch.cuda.current_stream()
 
@@ -217,9 +222,10 @@ def main():
     kur.timing(g, False)
     kur.check(g)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms, tm["stage_ms"]], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(t[0].item())
+        tm["stage_ms"] = float(t[1].item())
     ms_per_step = ms / args.steps
     rhs_per_s = 4.0 * args.steps / (ms / 1e3)
     stage_ms = tm["stage_ms"] / max(tm["stage_n"], 1)
@@ -236,16 +242,14 @@ def main():
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        th_h = g.to_user(th).cpu().pin_memory()
-        om_h = torch.from_numpy(inst.omega).pin_memory()
-        # the API works in internal order: the caller keeps host vectors in that order
-        th_hi = torch.empty(inst.n, dtype=torch.float64).pin_memory()
-        om_hi = torch.empty(inst.n, dtype=torch.float64).pin_memory()
-        th_hi.copy_(g.to_internal(th_h.to(dev)).cpu())
-        om_hi.copy_(g.to_internal(om_h.to(dev)).cpu())
+        # the API works in internal order: the caller keeps its host vectors in that order
+        th_hi = th.cpu().pin_memory()
+        om_hi = om.cpu().pin_memory()
         rt_h = torch.empty((2, 2), dtype=torch.float64).pin_memory()
         kur.step(g, th_hi, om_hi, K, h, 1, 1)  # warm
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         ne = max(3, min(args.steps, 20))
         ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ee0.record(stream)
@@ -255,8 +259,12 @@ def main():
         ee1.record(stream)
         torch.cuda.synchronize()
         e_ms = ee0.elapsed_time(ee1) / ne
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
         e2e = {"value": 4.0 / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * inst.n,
-               "d2h_bytes_per_step": 8 * inst.n + 32, "ms_per_step": e_ms, "steps": ne,
+               "d2h_bytes_per_step": 8 * inst.n + 32 * world, "ms_per_step": e_ms, "steps": ne,
                "path": "kur.step(host pinned theta, omega): H2D + kur_step(nsteps=1) + D2H theta and r"}
 
     cpu = None
@@ -281,7 +289,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 2 + tm["stage_n"] + 0 * tm["prologue_n"],
+            "gpu_launches": 1 + tm["prologue_n"] + tm["stage_n"] + (2 * (tm["prologue_n"] + tm["stage_n"]) if world > 1 else 0),
             "clocks": clk.result(),
             "host": {"gen_s": gen_s, "build_s": build_s, "nproc": os.cpu_count()},
             "plan": {k: info[k] for k in ("n_idx_hot", "n_idx_remote", "n_slots_hot", "n_slots_remote",
@@ -292,6 +300,8 @@ def main():
         }
         print(json.dumps(out), flush=True)
     g.close()
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -97,10 +97,14 @@ typedef struct {
                                in [32, 2048] (tuning / tests) */
 } kur_graph_desc;
 
-/* Multi-GPU placement: contiguous ranges of whole communities per rank.
+/* Multi-GPU placement: contiguous ranges of whole communities per rank,
+ * balanced by stored-entry count (every rank computes the same split).
  * nccl_id points at a 128-byte ncclUniqueId that rank 0 created with
  * kur_nccl_unique_id and the caller broadcast (e.g. over a torch process
- * group).  NULL desc = single GPU (the current device). */
+ * group); each stage then all-gathers the packed [stage phases | tile partials]
+ * of every rank over NCCL.  nccl_id = NULL with world > 1 builds a rank handle
+ * for the single-process group calls (kur_group_*).  NULL desc = single GPU
+ * (the current device). */
 typedef struct {
   int32_t rank;
   int32_t world;
@@ -166,6 +170,17 @@ kur_status kur_step(kur_graph *g, double *theta, const double *omega, double K, 
  * S_b / n_b; empty communities give (0, 0). */
 kur_status kur_order_parameter(kur_graph *g, const double *theta, double *r_psi, double *local,
                                void *stream);
+
+/* Single-process execution of a whole world of rank handles (built with
+ * world > 1 and nccl_id = NULL, ranks 0..world-1, all on one device): the
+ * same kernels as the NCCL path, the all-gather done by device copies, ranks
+ * run one after another on `stream`.  Used to test the sharded path and its
+ * bitwise world-size invariance on one GPU.  Arrays are indexed by rank. */
+kur_status kur_group_rhs(kur_graph *const *g, int32_t world, const double *const *theta,
+                         const double *const *omega, double K, double *const *dtheta, void *stream);
+kur_status kur_group_step(kur_graph *const *g, int32_t world, double *const *theta, const double *const *omega,
+                          double K, double h, int64_t nsteps, int32_t record_every, double *const *r_trace,
+                          void *stream);
 
 /* Synchronises `stream`; returns KUR_ERR_NONFINITE (and clears the flag) if a
  * previous kur_step produced a non-finite phase. */

@@ -61,6 +61,9 @@ struct kur_graph {
   double* acc = nullptr;
   Ctrl* ctrl = nullptr;
   ncclComm_t comm = nullptr;
+  int world = 1;
+  int32_t *d_shard_row0 = nullptr, *d_shard_tile0 = nullptr;
+  double *xsend = nullptr, *xrecv = nullptr;  // world > 1: packed exchange buffers
   // optional per-launch CUDA-event timing (kur_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev;        // pool, reused
@@ -80,7 +83,8 @@ struct kur_graph {
   ~kur_graph() {
     cudaSetDevice(device);
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
-                    d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl};
+                    d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
+                    xsend, xrecv};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -133,7 +137,6 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   } else {
     KUR_CUDA(cudaGetDevice(&device));
   }
-  if (world != 1) return fail(KUR_ERR_UNSUPPORTED, "world > 1 is not supported by this build yet");
   KUR_CUDA(cudaSetDevice(device));
   int sm = 148;
   cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device);
@@ -204,6 +207,30 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   if ((e = cudaMemset(g->TA, 0, cb)) != cudaSuccess) return bail(e, "TA");
   if ((e = cudaMemset(g->TB, 0, cb)) != cudaSuccess) return bail(e, "TB");
   if ((e = cudaMemset(g->S, 0, cb)) != cudaSuccess) return bail(e, "S");
+  g->world = world;
+  int32_t xrows = 0, xtiles = 0;
+  for (int32_t r = 0; r < world; ++r) {
+    xrows = std::max(xrows, P.shard_row0[(size_t)r + 1] - P.shard_row0[(size_t)r]);
+    xtiles = std::max(xtiles, P.shard_tile0[(size_t)r + 1] - P.shard_tile0[(size_t)r]);
+  }
+  const int32_t xstride = std::max(xrows + 2 * xtiles, 1);
+  if ((e = upload(&g->d_shard_row0, P.shard_row0)) != cudaSuccess) return bail(e, "shard_row0");
+  if ((e = upload(&g->d_shard_tile0, P.shard_tile0)) != cudaSuccess) return bail(e, "shard_tile0");
+  if (world > 1) {
+    if ((e = cudaMalloc((void**)&g->xsend, sizeof(double) * (size_t)xstride)) != cudaSuccess) return bail(e, "xsend");
+    if ((e = cudaMalloc((void**)&g->xrecv, sizeof(double) * (size_t)xstride * (size_t)world)) != cudaSuccess)
+      return bail(e, "xrecv");
+    if ((e = cudaMemset(g->xsend, 0, sizeof(double) * (size_t)xstride)) != cudaSuccess) return bail(e, "xsend");
+    if (dist && dist->nccl_id) {
+      ncclUniqueId id;
+      std::memcpy(&id, dist->nccl_id, sizeof(id));
+      ncclResult_t nr = ncclCommInitRank(&g->comm, world, id, rank);
+      if (nr != ncclSuccess) {
+        delete g;
+        return fail(KUR_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(nr));
+      }
+    }
+  }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "build sync");
 
   DevPlan& dp = g->dp;
@@ -214,6 +241,11 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   dp.tile_base = P.tile_begin;
   dp.row_begin = (int32_t)P.row_begin;
   dp.world = world;
+  dp.rank = rank;
+  dp.shard_row0 = g->d_shard_row0;
+  dp.shard_tile0 = g->d_shard_tile0;
+  dp.xrows = xrows;
+  dp.xstride = xstride;
   dp.tiles = g->d_tiles;
   dp.order = g->d_order;
   dp.parts = g->d_parts;
@@ -286,83 +318,194 @@ kur_status kur_permute(const kur_graph* g, const double* in, double* out, int32_
   return KUR_OK;
 }
 
-kur_status kur_rhs(kur_graph* g, const double* theta, const double* omega, double K, double* dtheta,
-                   void* stream) {
-  if (!g || !theta || !omega || !dtheta) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
-  if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
-  KUR_CUDA(cudaSetDevice(g->device));
-  cudaStream_t s = (cudaStream_t)stream;
-  StageArgs a{};
-  a.theta = const_cast<double*>(theta);
-  a.omega = omega;
-  a.out = dtheta;
-  a.zout = g->zA;
-  a.Tout = g->TA;
-  a.KN = K / (double)g->n;
-  a.record = REC_NONE;
-  KUR_CUDA(launch_prologue(g->dp, a, s));
-  a.zin = g->zA;
-  a.Tin = g->TA;
-  a.zout = nullptr;
-  a.Tout = nullptr;
-  KUR_CUDA(launch_stage(MODE_RHS, g->dp, a, s));
+}  // extern "C"
+
+// ---------------------------------------------------------------- orchestration
+// One "phase" = k_prologue or one k_stage over every rank in `gs`.  With
+// world > 1 the fused kernel packs [stage theta | tile partials] into xsend;
+// the packed buffers are all-gathered (NCCL across processes, or device copies
+// when all ranks live in this process: kur_group_*), then k_unpack fills z of
+// the remote rows and all partials and k_finish forms S_b, T_a, (r, psi) in the
+// same fixed order on every rank (bitwise identical for any world size).
+namespace {
+
+struct RankIO {
+  double* theta;
+  const double* omega;
+  double* out;      // dtheta (RHS)
+  double* op_rpsi;  // order parameter outputs
+  double* op_local;
+};
+
+kur_status exchange(const std::vector<kur_graph*>& gs, cudaStream_t s) {
+  kur_graph* g0 = gs[0];
+  if (g0->world == 1) return KUR_OK;
+  if (g0->comm) {
+    ncclResult_t r = ncclAllGather(g0->xsend, g0->xrecv, (size_t)g0->dp.xstride, ncclDouble, g0->comm, s);
+    if (r != ncclSuccess) return fail(KUR_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    return KUR_OK;
+  }
+  if ((int)gs.size() != g0->world)
+    return fail(KUR_ERR_UNSUPPORTED, "this handle has world > 1 without NCCL: use the kur_group_* calls");
+  const size_t bytes = sizeof(double) * (size_t)g0->dp.xstride;
+  for (kur_graph* dst : gs)
+    for (kur_graph* src : gs)
+      KUR_CUDA(cudaMemcpyAsync(dst->xrecv + (size_t)src->dp.rank * g0->dp.xstride, src->xsend, bytes,
+                               cudaMemcpyDeviceToDevice, s));
   return KUR_OK;
 }
 
-kur_status kur_step(kur_graph* g, double* theta, const double* omega, double K, double h, int64_t nsteps,
-                    int32_t record_every, double* r_trace, void* stream) {
-  if (!g || !theta || !omega) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
-  if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
-  if (!(h > 0.0) || !std::isfinite(h)) return fail(KUR_ERR_INVALID_ARG, "h must be finite and > 0");
-  if (nsteps < 0) return fail(KUR_ERR_INVALID_ARG, "nsteps must be >= 0");
-  if (record_every < 0) return fail(KUR_ERR_INVALID_ARG, "record_every must be >= 0");
-  KUR_CUDA(cudaSetDevice(g->device));
-  cudaStream_t s = (cudaStream_t)stream;
-  const bool rec = record_every > 0 && r_trace;
-  const int64_t cap = rec ? nsteps / record_every + 1 : 0;
-  KUR_CUDA(launch_set_ctrl(g->ctrl, rec ? record_every : 0, (int)cap, rec ? r_trace : nullptr, s));
-  StageArgs a{};
-  a.theta = theta;
-  a.omega = omega;
-  a.acc = g->acc;
-  a.KN = K / (double)g->n;
-  a.h = h;
-  a.zout = g->zA;
-  a.Tout = g->TA;
-  a.record = REC_START;
-  KUR_CUDA(g->mark(s));
-  KUR_CUDA(launch_prologue(g->dp, a, s));
-  KUR_CUDA(g->mark(s));
-  if (g->timing) g->ev_kind.push_back(0);
-  for (int64_t n = 0; n < nsteps; ++n) {
-    for (int st = MODE_S1; st <= MODE_S4; ++st) {
-      const bool even = (st == MODE_S1 || st == MODE_S3);
-      a.zin = even ? g->zA : g->zB;
-      a.zout = even ? g->zB : g->zA;
-      a.Tin = even ? g->TA : g->TB;
-      a.Tout = even ? g->TB : g->TA;
-      a.record = st == MODE_S4 ? REC_STEP : REC_NONE;
-      KUR_CUDA(g->mark(s));
-      KUR_CUDA(launch_stage(st, g->dp, a, s));
-      KUR_CUDA(g->mark(s));
-      if (g->timing) g->ev_kind.push_back(1);
+enum { PH_PROLOGUE = -1 };
+
+// mode: PH_PROLOGUE or a StageMode.  zin/zout/Tin/Tout select the ping-pong buffers.
+kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vector<RankIO>& io, double K,
+                     double h, int record, bool z_from_A, cudaStream_t s) {
+  const int world = gs[0]->world;
+  std::vector<StageArgs> args(gs.size());
+  for (size_t r = 0; r < gs.size(); ++r) {
+    kur_graph* g = gs[r];
+    StageArgs& a = args[r];
+    a = StageArgs{};
+    a.theta = io[r].theta;
+    a.omega = io[r].omega;
+    a.out = io[r].out;
+    a.acc = g->acc;
+    a.KN = K / (double)g->n;
+    a.h = h;
+    a.record = record;
+    a.op_rpsi = io[r].op_rpsi;
+    a.op_local = io[r].op_local;
+    a.xsend = world > 1 ? g->xsend : nullptr;
+    if (mode == PH_PROLOGUE) {
+      a.zout = g->zA;
+      a.Tout = g->TA;
+    } else {
+      a.zin = z_from_A ? g->zA : g->zB;
+      a.zout = z_from_A ? g->zB : g->zA;
+      a.Tin = z_from_A ? g->TA : g->TB;
+      a.Tout = z_from_A ? g->TB : g->TA;
     }
+    KUR_CUDA(g->mark(s));
+    if (mode == PH_PROLOGUE) KUR_CUDA(launch_prologue(g->dp, a, s));
+    else KUR_CUDA(launch_stage(mode, g->dp, a, s));
+    KUR_CUDA(g->mark(s));
+    if (g->timing) g->ev_kind.push_back(mode == PH_PROLOGUE ? 0 : 1);
+  }
+  if (world == 1 || mode == MODE_RHS) return KUR_OK;
+  kur_status st = exchange(gs, s);
+  if (st != KUR_OK) return st;
+  for (size_t r = 0; r < gs.size(); ++r) {
+    KUR_CUDA(launch_unpack(gs[r]->dp, gs[r]->xrecv, args[r].zout, s));
+    KUR_CUDA(launch_finish(gs[r]->dp, args[r], s));
   }
   return KUR_OK;
 }
 
+kur_status check_group(const std::vector<kur_graph*>& gs) {
+  if (gs.empty() || !gs[0]) return fail(KUR_ERR_INVALID_ARG, "graph is NULL");
+  for (kur_graph* g : gs)
+    if (!g || g->device != gs[0]->device || g->world != gs[0]->world)
+      return fail(KUR_ERR_INVALID_ARG, "group handles must share world size and device");
+  if (gs.size() > 1) {
+    for (size_t r = 0; r < gs.size(); ++r)
+      if (gs[r]->dp.rank != (int)r || gs[r]->comm) return fail(KUR_ERR_INVALID_ARG, "group handles must be ranks 0..world-1 without NCCL");
+  }
+  return KUR_OK;
+}
+
+kur_status rhs_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO>& io, double K, cudaStream_t s) {
+  if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
+  for (size_t r = 0; r < io.size(); ++r)
+    if (gs[r]->n_local > 0 && (!io[r].theta || !io[r].omega || !io[r].out))
+      return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  KUR_CUDA(cudaSetDevice(gs[0]->device));
+  kur_status st = run_phase(gs, PH_PROLOGUE, io, K, 0.0, REC_NONE, true, s);
+  if (st != KUR_OK) return st;
+  return run_phase(gs, MODE_RHS, io, K, 0.0, REC_NONE, true, s);
+}
+
+kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO>& io, double K, double h,
+                     int64_t nsteps, int32_t record_every, const std::vector<double*>& r_trace, cudaStream_t s) {
+  if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
+  if (!(h > 0.0) || !std::isfinite(h)) return fail(KUR_ERR_INVALID_ARG, "h must be finite and > 0");
+  if (nsteps < 0) return fail(KUR_ERR_INVALID_ARG, "nsteps must be >= 0");
+  if (record_every < 0) return fail(KUR_ERR_INVALID_ARG, "record_every must be >= 0");
+  for (size_t r = 0; r < io.size(); ++r)
+    if (gs[r]->n_local > 0 && (!io[r].theta || !io[r].omega)) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  KUR_CUDA(cudaSetDevice(gs[0]->device));
+  for (size_t r = 0; r < gs.size(); ++r) {
+    const bool rec = record_every > 0 && r_trace[r];
+    const int64_t cap = rec ? nsteps / record_every + 1 : 0;
+    KUR_CUDA(launch_set_ctrl(gs[r]->ctrl, rec ? record_every : 0, (int)cap, rec ? r_trace[r] : nullptr, s));
+  }
+  kur_status st = run_phase(gs, PH_PROLOGUE, io, K, h, REC_START, true, s);
+  if (st != KUR_OK) return st;
+  for (int64_t n = 0; n < nsteps; ++n)
+    for (int m = MODE_S1; m <= MODE_S4; ++m) {
+      st = run_phase(gs, m, io, K, h, m == MODE_S4 ? REC_STEP : REC_NONE, m == MODE_S1 || m == MODE_S3, s);
+      if (st != KUR_OK) return st;
+    }
+  return KUR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+kur_status kur_rhs(kur_graph* g, const double* theta, const double* omega, double K, double* dtheta,
+                   void* stream) {
+  if (!g) return fail(KUR_ERR_INVALID_ARG, "graph is NULL");
+  std::vector<kur_graph*> gs{g};
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
+  return rhs_impl(gs, {RankIO{const_cast<double*>(theta), omega, dtheta, nullptr, nullptr}}, K, (cudaStream_t)stream);
+}
+
+kur_status kur_step(kur_graph* g, double* theta, const double* omega, double K, double h, int64_t nsteps,
+                    int32_t record_every, double* r_trace, void* stream) {
+  if (!g) return fail(KUR_ERR_INVALID_ARG, "graph is NULL");
+  std::vector<kur_graph*> gs{g};
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
+  return step_impl(gs, {RankIO{theta, omega, nullptr, nullptr, nullptr}}, K, h, nsteps, record_every, {r_trace},
+                   (cudaStream_t)stream);
+}
+
 kur_status kur_order_parameter(kur_graph* g, const double* theta, double* r_psi, double* local, void* stream) {
   if (!g || !theta || !r_psi) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  std::vector<kur_graph*> gs{g};
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
   KUR_CUDA(cudaSetDevice(g->device));
-  StageArgs a{};
-  a.theta = const_cast<double*>(theta);
-  a.zout = g->zA;
-  a.Tout = g->TA;
-  a.op_rpsi = r_psi;
-  a.op_local = local;
-  a.record = REC_NONE;
-  KUR_CUDA(launch_prologue(g->dp, a, (cudaStream_t)stream));
-  return KUR_OK;
+  return run_phase(gs, PH_PROLOGUE, {RankIO{const_cast<double*>(theta), nullptr, nullptr, r_psi, local}}, 0.0, 0.0,
+                   REC_NONE, true, (cudaStream_t)stream);
+}
+
+kur_status kur_group_rhs(kur_graph* const* g, int32_t world, const double* const* theta,
+                         const double* const* omega, double K, double* const* dtheta, void* stream) {
+  if (!g || !theta || !omega || !dtheta || world < 1) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  std::vector<kur_graph*> gs(g, g + world);
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
+  std::vector<RankIO> io;
+  for (int r = 0; r < world; ++r) io.push_back(RankIO{const_cast<double*>(theta[r]), omega[r], dtheta[r], nullptr, nullptr});
+  return rhs_impl(gs, io, K, (cudaStream_t)stream);
+}
+
+kur_status kur_group_step(kur_graph* const* g, int32_t world, double* const* theta, const double* const* omega,
+                          double K, double h, int64_t nsteps, int32_t record_every, double* const* r_trace,
+                          void* stream) {
+  if (!g || !theta || !omega || world < 1) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  std::vector<kur_graph*> gs(g, g + world);
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
+  std::vector<RankIO> io;
+  std::vector<double*> rt;
+  for (int r = 0; r < world; ++r) {
+    io.push_back(RankIO{theta[r], omega[r], nullptr, nullptr, nullptr});
+    rt.push_back(r_trace ? r_trace[r] : nullptr);
+  }
+  return step_impl(gs, io, K, h, nsteps, record_every, rt, (cudaStream_t)stream);
 }
 
 kur_status kur_timing(kur_graph* g, int32_t enable) {

@@ -22,6 +22,8 @@
 // reproducible run to run.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace kur {
@@ -37,7 +39,7 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p, uint64_t pol) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p), "l"(pol));
   return r;
@@ -135,19 +137,32 @@ __device__ __forceinline__ void rem4(const uint4 v, const double2* __restrict__ 
 }
 
 // Hot part of one chunk: ng groups of 32 units starting at q (lane-offset applied).
+// Software-pipelined: the next 4 groups are in flight while 4 are gathered.
 __device__ __forceinline__ void run_hot(const uint4* __restrict__ q, uint32_t ng, const double2* zs,
                                         uint64_t pol, double& sx, double& sy) {
   double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
   uint32_t g = 0;
-  for (; g + 4 <= ng; g += 4) {
-    const uint4 v0 = ldg_stream(q + (size_t)(g + 0) * 32, pol);
-    const uint4 v1 = ldg_stream(q + (size_t)(g + 1) * 32, pol);
-    const uint4 v2 = ldg_stream(q + (size_t)(g + 2) * 32, pol);
-    const uint4 v3 = ldg_stream(q + (size_t)(g + 3) * 32, pol);
-    hot8(v0, zs, x0, y0, x1, y1);
-    hot8(v1, zs, x0, y0, x1, y1);
-    hot8(v2, zs, x0, y0, x1, y1);
-    hot8(v3, zs, x0, y0, x1, y1);
+  if (ng >= 4) {
+    uint4 a0 = ldg_stream(q + 0 * 32, pol), a1 = ldg_stream(q + 1 * 32, pol);
+    uint4 a2 = ldg_stream(q + 2 * 32, pol), a3 = ldg_stream(q + 3 * 32, pol);
+    for (g = 4; g + 4 <= ng; g += 4) {
+      const uint4 b0 = ldg_stream(q + (size_t)(g + 0) * 32, pol);
+      const uint4 b1 = ldg_stream(q + (size_t)(g + 1) * 32, pol);
+      const uint4 b2 = ldg_stream(q + (size_t)(g + 2) * 32, pol);
+      const uint4 b3 = ldg_stream(q + (size_t)(g + 3) * 32, pol);
+      hot8(a0, zs, x0, y0, x1, y1);
+      hot8(a1, zs, x0, y0, x1, y1);
+      hot8(a2, zs, x0, y0, x1, y1);
+      hot8(a3, zs, x0, y0, x1, y1);
+      a0 = b0;
+      a1 = b1;
+      a2 = b2;
+      a3 = b3;
+    }
+    hot8(a0, zs, x0, y0, x1, y1);
+    hot8(a1, zs, x0, y0, x1, y1);
+    hot8(a2, zs, x0, y0, x1, y1);
+    hot8(a3, zs, x0, y0, x1, y1);
   }
   for (; g < ng; ++g) hot8(ldg_stream(q + (size_t)g * 32, pol), zs, x0, y0, x1, y1);
   sx = x0 + x1;
@@ -245,6 +260,10 @@ __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const
   block_sum2(x, y, red);
   if (threadIdx.x == 0) {
     dp.partial[dp.tile_base + lt] = make_double2(x, y);
+    if (a.xsend) {
+      a.xsend[dp.xrows + 2 * lt] = x;
+      a.xsend[dp.xrows + 2 * lt + 1] = y;
+    }
     s_last = false;
     if (dp.world == 1) {  // world > 1: the reduction runs after the exchange
       __threadfence();
@@ -268,8 +287,10 @@ __global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const S
   for (int lr = tid; lr < T.nrows; lr += NTHREADS) {
     const int row = T.row0 + lr;
     double s, c;
-    sincos(a.theta[row - dp.row_begin], &s, &c);  // z = e^{i theta}
+    const double th = a.theta[row - dp.row_begin];
+    sincos(th, &s, &c);  // z = e^{i theta}
     a.zout[row] = make_double2(c, s);
+    if (a.xsend) a.xsend[row - dp.row_begin] = th;
     x += c;
     y += s;
   }
@@ -366,6 +387,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
       double s, c;
       sincos(ts, &s, &c);
       a.zout[row] = make_double2(c, s);
+      if (a.xsend) a.xsend[li] = ts;
       px += c;
       py += s;
     }
@@ -375,6 +397,32 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __syncthreads();
   if (MODE == MODE_S4 && tid == 0 && s_nonfinite) dp.ctrl->nonfinite = 1;
   tile_partial_and_finish(dp, a, lt, px, py, red);
+}
+
+// world > 1: z of the non-local rows from the exchanged stage phases (the same
+// sincos the owner evaluated -> bitwise identical), and every tile partial.
+__global__ void k_unpack(const DevPlan dp, const double* __restrict__ xrecv, double2* __restrict__ zout) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < dp.n) {
+    int r = 0;
+    while (dp.shard_row0[r + 1] <= i) ++r;
+    if (r != dp.rank) {
+      double s, c;
+      sincos(xrecv[(size_t)r * dp.xstride + (i - dp.shard_row0[r])], &s, &c);
+      zout[i] = make_double2(c, s);
+    }
+  }
+  const int64_t nt = dp.shard_tile0[dp.world];
+  if (i < nt) {
+    int r = 0;
+    while (dp.shard_tile0[r + 1] <= i) ++r;
+    const double* src = xrecv + (size_t)r * dp.xstride + dp.xrows + 2 * (i - dp.shard_tile0[r]);
+    dp.partial[i] = make_double2(src[0], src[1]);
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_finish(const DevPlan dp, const StageArgs a) {
+  finish_reduce(dp, a);
 }
 
 __global__ void k_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace) {
@@ -424,6 +472,18 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
     case MODE_S4: return launch_stage_m<MODE_S4>(dp, a, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, cudaStream_t s) {
+  const int64_t m = std::max<int64_t>(dp.n, (int64_t)1);
+  const int bs = 256;
+  k_unpack<<<(unsigned)((m + bs - 1) / bs), bs, 0, s>>>(dp, xrecv, zout);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finish(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
+  k_finish<<<1, NTHREADS, 0, s>>>(dp, a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, cudaStream_t s) {

@@ -35,6 +35,11 @@ struct DevPlan {
   const int32_t* D_idx;
   const int32_t* comm_size;   // [C]
   const int32_t* perm;        // [n] internal -> user
+  int32_t rank;
+  int32_t xstride;            // doubles per rank in the exchange buffer (xrows + 2 * xtiles)
+  int32_t xrows;              // max rows of a shard (theta region of the exchange buffer)
+  const int32_t* shard_row0;  // [world+1] internal row range of every rank
+  const int32_t* shard_tile0; // [world+1] tile range of every rank
   double2* partial;           // [ntiles_all] per-tile sums of z (global tile ids)
   double2* S;                 // [C] block sums S_b of the last reduction
   Ctrl* ctrl;
@@ -57,10 +62,16 @@ struct StageArgs {
   double* op_rpsi;        // kur_order_parameter outputs (device) or NULL
   double* op_local;
   int record;             // RecordMode
+  double* xsend;          // world > 1: packed [stage theta of local rows | local tile partials]
 };
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
 cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaStream_t s);
+// world > 1: after the all-gather of the packed buffers (xrecv = world x xstride doubles),
+// z of every non-local row from its exchanged phase, all tile partials; then the
+// fixed-order block-sum reduction by one CTA.
+cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, cudaStream_t s);
+cudaError_t launch_finish(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
 cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, cudaStream_t s);
 cudaError_t launch_permute(const int32_t* perm, int64_t n, const double* in, double* out, int dir,
                            cudaStream_t s);

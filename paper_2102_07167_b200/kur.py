@@ -65,17 +65,20 @@ _lib.kur_check.argtypes = [_p, _p]
 _lib.kur_timing.argtypes = [_p, _i32]
 _lib.kur_timing_read.argtypes = [_p, _p]
 _lib.kur_nccl_unique_id.argtypes = [_p]
+_lib.kur_group_rhs.argtypes = [_p, _i32, _p, _p, _d, _p, _p]
+_lib.kur_group_step.argtypes = [_p, _i32, _p, _p, _d, _d, _i64, _i32, _p, _p]
 _lib.kur_status_string.restype = ctypes.c_char_p
 _lib.kur_status_string.argtypes = [ctypes.c_int]
 _lib.kur_last_error.restype = ctypes.c_char_p
 for _f in ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
            "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id", "kur_timing",
-           "kur_timing_read"):
+           "kur_timing_read", "kur_group_rhs", "kur_group_step"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
             "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id",
-            "kur_status_string", "kur_last_error", "kur_timing", "kur_timing_read")
+            "kur_status_string", "kur_last_error", "kur_timing", "kur_timing_read", "kur_group_rhs",
+            "kur_group_step")
 
 
 class KurError(RuntimeError):
@@ -100,6 +103,8 @@ def _stream(stream):
 
 
 def _dev_vec(x, n, device, name):
+    if n == 0 and isinstance(x, torch.Tensor) and x.numel() == 0:
+        return ctypes.c_void_p(None)  # a rank without rows
     if not isinstance(x, torch.Tensor):
         raise TypeError(f"{name} must be a torch tensor")
     if x.dtype != torch.float64 or not x.is_cuda or not x.is_contiguous() or x.numel() != n:
@@ -185,8 +190,9 @@ def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, devi
     dd = None
     if dist is not None:
         rank, world, nccl_id = dist
-        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
-        dd = DistDesc(rank=rank, world=world, device=device, nccl_id=ctypes.cast(idbuf, _p))
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+        dd = DistDesc(rank=rank, world=world, device=device,
+                      nccl_id=ctypes.cast(idbuf, _p) if idbuf is not None else None)
     h = ctypes.c_void_p()
     with torch.cuda.device(device):
         _check(_lib.kur_graph_build(ctypes.byref(desc), ctypes.byref(dd) if dd is not None else None,
@@ -240,6 +246,41 @@ def timing_read(g: Graph):
     out = np.zeros(4, np.float64)
     _check(_lib.kur_timing_read(g._h, _np_ptr(out)))
     return dict(prologue_ms=float(out[0]), prologue_n=int(out[1]), stage_ms=float(out[2]), stage_n=int(out[3]))
+
+
+def _ptr_array(ptrs):
+    arr = (ctypes.c_void_p * len(ptrs))(*[p.value if isinstance(p, ctypes.c_void_p) else p for p in ptrs])
+    return arr
+
+
+def group_build(inst, world, device=None, **kw):
+    """world rank handles on ONE device for the single-process group calls (kur_group_*)."""
+    return [graph_build(inst, device=device, dist=(r, world, None), **kw) for r in range(world)]
+
+
+def group_rhs(graphs, thetas, omegas, K, outs=None, stream=None):
+    """kur_group_rhs: thetas/omegas/outs are per-rank local-row device tensors."""
+    outs = [torch.empty_like(t) for t in thetas] if outs is None else outs
+    hs = _ptr_array([g._h for g in graphs])
+    th = _ptr_array([_dev_vec(t, g.n_local, g.device, "theta").value for g, t in zip(graphs, thetas)])
+    om = _ptr_array([_dev_vec(o, g.n_local, g.device, "omega").value for g, o in zip(graphs, omegas)])
+    ou = _ptr_array([_dev_vec(o, g.n_local, g.device, "dtheta").value for g, o in zip(graphs, outs)])
+    _check(_lib.kur_group_rhs(hs, len(graphs), th, om, float(K), ou, _stream(stream)))
+    return outs
+
+
+def group_step(graphs, thetas, omegas, K, h, nsteps, record_every=0, stream=None):
+    """kur_group_step: in-place RK4 on per-rank local-row device tensors; returns per-rank r_traces."""
+    dev = f"cuda:{graphs[0].device}"
+    rts = [torch.zeros((int(nsteps) // int(record_every) + 1, 2), dtype=torch.float64, device=dev)
+           if record_every else None for _ in graphs]
+    hs = _ptr_array([g._h for g in graphs])
+    th = _ptr_array([_dev_vec(t, g.n_local, g.device, "theta").value for g, t in zip(graphs, thetas)])
+    om = _ptr_array([_dev_vec(o, g.n_local, g.device, "omega").value for g, o in zip(graphs, omegas)])
+    rt = _ptr_array([r.data_ptr() if r is not None else None for r in rts]) if record_every else None
+    _check(_lib.kur_group_step(hs, len(graphs), th, om, float(K), float(h), int(nsteps), int(record_every), rt,
+                               _stream(stream)))
+    return rts
 
 
 def check(g: Graph, stream=None):
