@@ -67,7 +67,8 @@ struct kur_graph {
   // optional per-launch CUDA-event timing (kur_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev;        // pool, reused
-  std::vector<int> ev_kind;           // per recorded pair: 0 prologue, 1 stage
+  std::vector<std::pair<int, int>> ev_kind;  // per recorded pair: (0 prologue | 1 stage, RHS evaluations)
+  bool small = false;                 // whole kur_step in one single-CTA launch
   size_t ev_used = 0;
   cudaError_t mark(cudaStream_t s) {  // records the next event of the pool on s
     if (!timing) return cudaSuccess;
@@ -242,6 +243,11 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   dp.row_begin = (int32_t)P.row_begin;
   dp.world = world;
   dp.rank = rank;
+  dp.has_parts = 0;
+  for (const TileDesc& T : P.tiles)
+    if (T.nparts > 0) dp.has_parts = 1;
+  // tiny graphs run a whole trajectory in one CTA (launch latency dominates otherwise)
+  g->small = P.small;
   dp.shard_row0 = g->d_shard_row0;
   dp.shard_tile0 = g->d_shard_tile0;
   dp.xrows = xrows;
@@ -389,7 +395,7 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
     if (mode == PH_PROLOGUE) KUR_CUDA(launch_prologue(g->dp, a, s));
     else KUR_CUDA(launch_stage(mode, g->dp, a, s));
     KUR_CUDA(g->mark(s));
-    if (g->timing) g->ev_kind.push_back(mode == PH_PROLOGUE ? 0 : 1);
+    if (g->timing) g->ev_kind.push_back({mode == PH_PROLOGUE ? 0 : 1, mode == PH_PROLOGUE ? 0 : 1});
   }
   if (world == 1 || mode == MODE_RHS) return KUR_OK;
   kur_status st = exchange(gs, s);
@@ -437,6 +443,20 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
     const bool rec = record_every > 0 && r_trace[r];
     const int64_t cap = rec ? nsteps / record_every + 1 : 0;
     KUR_CUDA(launch_set_ctrl(gs[r]->ctrl, rec ? record_every : 0, (int)cap, rec ? r_trace[r] : nullptr, s));
+  }
+  if (gs.size() == 1 && gs[0]->small) {  // tiny graph: one single-CTA launch for the whole trajectory
+    kur_graph* g = gs[0];
+    StageArgs a{};
+    a.theta = io[0].theta;
+    a.omega = io[0].omega;
+    a.acc = g->acc;
+    a.KN = K / (double)g->n;
+    a.h = h;
+    KUR_CUDA(g->mark(s));
+    KUR_CUDA(launch_small(g->dp, a, g->zA, g->zB, g->TA, g->TB, (long long)nsteps, s));
+    KUR_CUDA(g->mark(s));
+    if (g->timing) g->ev_kind.push_back({1, (int)std::min<int64_t>(4 * nsteps, INT32_MAX)});
+    return KUR_OK;
   }
   kur_status st = run_phase(gs, PH_PROLOGUE, io, K, h, REC_START, true, s);
   if (st != KUR_OK) return st;
@@ -525,8 +545,8 @@ kur_status kur_timing_read(kur_graph* g, double* out) {
     float t = 0.f;
     KUR_CUDA(cudaEventSynchronize(g->ev[2 * i + 1]));
     KUR_CUDA(cudaEventElapsedTime(&t, g->ev[2 * i], g->ev[2 * i + 1]));
-    ms[g->ev_kind[i]] += t;
-    cnt[g->ev_kind[i]] += 1;
+    ms[g->ev_kind[i].first] += t;
+    cnt[g->ev_kind[i].first] += g->ev_kind[i].first == 0 ? 1 : g->ev_kind[i].second;
   }
   out[0] = ms[0];
   out[1] = (double)cnt[0];

@@ -436,12 +436,16 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
 
   // ------------------------------------------------------------ 4. tiles
   // the largest tile (<= 2048 rows) that still gives >= 2 waves of 2 CTAs/SM
-  int rows_per_tile = force_rows;
-  for (int r = MAX_TILE_ROWS; r >= 32 && !force_rows; r >>= 1) {
+  // tiny graphs run whole trajectories in one CTA (kur_step), with the largest tiles
+  int64_t total_len = 0;
+#pragma omp parallel for reduction(+ : total_len)
+  for (int64_t u = 0; u < n; ++u) total_len += rlen[(size_t)u];
+  P.small = world == 1 && n <= 8192 && total_len <= (1 << 18);
+  int rows_per_tile = force_rows ? force_rows : (P.small ? MAX_TILE_ROWS : 0);
+  for (int r = MAX_TILE_ROWS; r >= 32 && !rows_per_tile; r >>= 1) {
     int64_t nt = 0;
     for (int32_t c = 0; c < C; ++c) nt += (S.csize[(size_t)c] + r - 1) / r;
-    rows_per_tile = r;
-    if (nt >= 4LL * sm_count) break;
+    if (nt >= 4LL * sm_count || r == 32) { rows_per_tile = r; break; }
   }
   P.rows_per_tile = rows_per_tile;
   const int RT = P.rows_per_tile;

@@ -120,12 +120,20 @@ __device__ __forceinline__ void hot8(const uint4 v, const double2* zs, double& x
   }
 }
 
+// COHERENT: z was written earlier by the same kernel (single-CTA trajectory
+// kernel) -> read through L2 (ld.global.cg) instead of the non-coherent path.
+template <bool COHERENT>
+__device__ __forceinline__ double2 ldz(const double2* p) {
+  return COHERENT ? __ldcg(p) : __ldg(p);
+}
+
+template <bool COHERENT>
 __device__ __forceinline__ void rem4(const uint4 v, const double2* __restrict__ z, double& x0,
                                      double& y0, double& x1, double& y1) {
-  const double2 a = __ldg(z + v.x);
-  const double2 b = __ldg(z + v.y);
-  const double2 c = __ldg(z + v.z);
-  const double2 d = __ldg(z + v.w);
+  const double2 a = ldz<COHERENT>(z + v.x);
+  const double2 b = ldz<COHERENT>(z + v.y);
+  const double2 c = ldz<COHERENT>(z + v.z);
+  const double2 d = ldz<COHERENT>(z + v.w);
   x0 += a.x;
   y0 += a.y;
   x1 += b.x;
@@ -169,6 +177,7 @@ __device__ __forceinline__ void run_hot(const uint4* __restrict__ q, uint32_t ng
   sy = y0 + y1;
 }
 
+template <bool COHERENT>
 __device__ __forceinline__ void run_remote(const uint4* __restrict__ q, uint32_t ng,
                                            const double2* __restrict__ z, uint64_t pol, double& sx, double& sy) {
   double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
@@ -176,10 +185,10 @@ __device__ __forceinline__ void run_remote(const uint4* __restrict__ q, uint32_t
   for (; g + 2 <= ng; g += 2) {
     const uint4 v0 = ldg_stream(q + (size_t)(g + 0) * 32, pol);
     const uint4 v1 = ldg_stream(q + (size_t)(g + 1) * 32, pol);
-    rem4(v0, z, x0, y0, x1, y1);
-    rem4(v1, z, x0, y0, x1, y1);
+    rem4<COHERENT>(v0, z, x0, y0, x1, y1);
+    rem4<COHERENT>(v1, z, x0, y0, x1, y1);
   }
-  for (; g < ng; ++g) rem4(ldg_stream(q + (size_t)g * 32, pol), z, x0, y0, x1, y1);
+  for (; g < ng; ++g) rem4<COHERENT>(ldg_stream(q + (size_t)g * 32, pol), z, x0, y0, x1, y1);
   sx = x0 + x1;
   sy = y0 + y1;
 }
@@ -187,9 +196,12 @@ __device__ __forceinline__ void run_remote(const uint4* __restrict__ q, uint32_t
 // Executed by every thread of the LAST CTA of a grid: S_b from the per-tile
 // partials, T_a, the order parameter and its recording.
 __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
+  __shared__ double2 fred[NWARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int BIG = 64;  // communities with more tiles are reduced by the whole CTA
   for (int c = warp; c < dp.C; c += NWARPS) {  // S_b = sum of its tiles' partials
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
+    if (t1 - t0 > BIG) continue;
     double x = 0.0, y = 0.0;
     for (int t = t0 + lane; t < t1; t += 32) {
       const double2 v = __ldcg(dp.partial + t);
@@ -198,6 +210,19 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
     }
     warp_sum2(x, y);
     if (lane == 0) dp.S[c] = make_double2(x, y);
+  }
+  for (int c = 0; c < dp.C; ++c) {  // large communities (uniform branch): fixed-shape block reduction
+    const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
+    if (t1 - t0 <= BIG) continue;
+    double x = 0.0, y = 0.0;
+    for (int t = t0 + tid; t < t1; t += NTHREADS) {
+      const double2 v = __ldcg(dp.partial + t);
+      x += v.x;
+      y += v.y;
+    }
+    block_sum2(x, y, fred);
+    if (tid == 0) dp.S[c] = make_double2(x, y);
+    __syncthreads();
   }
   __threadfence_block();
   __syncthreads();
@@ -218,15 +243,15 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
       a.op_local[2 * c + 1] = r == 0.0 ? 0.0 : atan2(cy, cx);
     }
   }
-  if (warp == 0) {  // r e^{i psi} = (1/N) sum_b S_b
+  {  // r e^{i psi} = (1/N) sum_b S_b, fixed-shape block reduction
     double x = 0.0, y = 0.0;
-    for (int c = lane; c < dp.C; c += 32) {
+    for (int c = tid; c < dp.C; c += NTHREADS) {
       const double2 v = __ldcg(dp.S + c);
       x += v.x;
       y += v.y;
     }
-    warp_sum2(x, y);
-    if (lane == 0) {
+    block_sum2(x, y, fred);
+    if (tid == 0) {
       const double cm = x / (double)dp.n, sm = y / (double)dp.n;
       const double r = sqrt(cm * cm + sm * sm);
       const double psi = r == 0.0 ? 0.0 : atan2(sm, cm);
@@ -278,13 +303,12 @@ __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const
   if (threadIdx.x == 0) dp.ctrl->ticket = 0;
 }
 
-__global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const StageArgs a) {
-  __shared__ double2 red[NWARPS];
-  const int tid = threadIdx.x;
-  const int lt = dp.order[blockIdx.x];
-  const TileDesc T = dp.tiles[lt];
-  double x = 0.0, y = 0.0;
-  for (int lr = tid; lr < T.nrows; lr += NTHREADS) {
+// a1 for one tile: z = e^{i theta} of its rows; returns this thread's partial sums.
+__device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs& a, const TileDesc& T, double& x,
+                                              double& y) {
+  x = 0.0;
+  y = 0.0;
+  for (int lr = threadIdx.x; lr < T.nrows; lr += NTHREADS) {
     const int row = T.row0 + lr;
     double s, c;
     const double th = a.theta[row - dp.row_begin];
@@ -294,38 +318,30 @@ __global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const S
     x += c;
     y += s;
   }
-  tile_partial_and_finish(dp, a, lt, x, y, red);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const StageArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* zs = reinterpret_cast<double2*>(smem_raw);       // [WZ + 8]: window + 8 zero sentinels
-  double2* Ws = zs + (WZ + 8);                              // [rows_per_tile]: W_j of the tile
-  __shared__ double2 red[NWARPS];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ int s_nonfinite;
+// a3-a5 for one tile (all threads of the CTA call it; contains barriers).
+// zs: [WZ + 8] window + zero sentinels, Ws: [rows_per_tile] row sums (both
+// unused when the plan has no parts).  Returns the thread's partial sums of
+// the next stage's z in (px, py) and whether a phase became non-finite.
+template <int MODE, bool SMALL>
+__device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a, const TileDesc& T, double2* zs,
+                                           double2* Ws, uint64_t* bar, uint32_t& phase, double& px, double& py) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lt = dp.order[blockIdx.x];
-  const TileDesc T = dp.tiles[lt];
-  const uint64_t pol = evict_first_policy();
-  for (int r = tid; r < T.nrows; r += NTHREADS) Ws[r] = make_double2(0.0, 0.0);
-  if (tid < 8) zs[WZ + tid] = make_double2(0.0, 0.0);
-  if (tid == 0) {
-    s_nonfinite = 0;
-    mbar_init(&bar, 1);
+  const bool parts = dp.has_parts;
+  if (parts) {
+    for (int r = tid; r < T.nrows; r += NTHREADS) Ws[r] = make_double2(0.0, 0.0);
+    __syncthreads();
   }
-  __syncthreads();
-
   // ---- parts: hot ones gather from the staged window, remote ones from global memory
-  uint32_t phase = 0;
+  const uint64_t pol = evict_first_policy();
   int loaded = -1;
   for (int p = T.part0; p < T.part0 + T.nparts; ++p) {
     const PartDesc P = dp.parts[p];
     const bool hot = P.window >= 0;
     if (hot && P.window != loaded) {  // all reads of the previous window ended at the last barrier
-      if (tid == 0) tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), &bar);
-      mbar_wait(&bar, phase);
+      if (tid == 0) tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), bar);
+      mbar_wait(bar, phase);
       phase ^= 1u;
       loaded = P.window;
     }
@@ -338,7 +354,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
       const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
       double sx, sy;
       if (hot) run_hot(q + HDR_UNITS + lane, cd.y, zs, pol, sx, sy);
-      else run_remote(q + HDR_UNITS + lane, cd.y, a.zin, pol, sx, sy);
+      else run_remote<SMALL>(q + HDR_UNITS + lane, cd.y, a.zin, pol, sx, sy);
       if (row != EMPTY_LANE) {
         double2 w = Ws[row];
         if (P.neg) {
@@ -355,15 +371,16 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   }
 
   // ---- finalize: k_j = omega_j + (K/N) Im(conj z_j W_j), fused RK4 stage
-  const double2 Tc = a.Tin[T.comm];
-  double px = 0.0, py = 0.0;
+  const double2 Tc = __ldcg(a.Tin + T.comm);
+  px = 0.0;
+  py = 0.0;
   bool bad = false;
   for (int lr = tid; lr < T.nrows; lr += NTHREADS) {
     const int row = T.row0 + lr;
     const int li = row - dp.row_begin;
-    const double2 w = Ws[lr];
+    const double2 w = parts ? Ws[lr] : make_double2(0.0, 0.0);
     const double wx = Tc.x + w.x, wy = Tc.y + w.y;
-    const double2 zj = a.zin[row];
+    const double2 zj = SMALL ? __ldcg(a.zin + row) : a.zin[row];
     const double k = a.omega[li] + a.KN * (zj.x * wy - zj.y * wx);
     if (MODE == MODE_RHS) {
       a.out[li] = k;
@@ -392,11 +409,112 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
       py += s;
     }
   }
+  return bad;
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const StageArgs a) {
+  __shared__ double2 red[NWARPS];
+  const int lt = dp.order[blockIdx.x];
+  const TileDesc T = dp.tiles[lt];
+  double x, y;
+  prologue_rows(dp, a, T, x, y);
+  tile_partial_and_finish(dp, a, lt, x, y, red);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const StageArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* zs = reinterpret_cast<double2*>(smem_raw);  // [WZ + 8]: window + 8 zero sentinels
+  double2* Ws = zs + (WZ + 8);                         // [rows_per_tile]: W_j of the tile
+  __shared__ double2 red[NWARPS];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int s_nonfinite;
+  const int tid = threadIdx.x;
+  const int lt = dp.order[blockIdx.x];
+  const TileDesc T = dp.tiles[lt];
+  if (dp.has_parts && tid < 8) zs[WZ + tid] = make_double2(0.0, 0.0);
+  if (tid == 0) {
+    s_nonfinite = 0;
+    mbar_init(&bar, 1);
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  double px, py;
+  const bool bad = stage_rows<MODE, false>(dp, a, T, zs, Ws, &bar, phase, px, py);
   if (MODE == MODE_RHS) return;
   if (MODE == MODE_S4 && bad) s_nonfinite = 1;
   __syncthreads();
   if (MODE == MODE_S4 && tid == 0 && s_nonfinite) dp.ctrl->nonfinite = 1;
   tile_partial_and_finish(dp, a, lt, px, py, red);
+}
+
+// ---- single-CTA trajectory kernel for tiny graphs (world == 1): the whole
+// kur_step (prologue + nsteps x 4 stages, each followed by the block-sum
+// reduction) in one launch, barriers instead of kernel boundaries.
+template <int MODE>
+__device__ __forceinline__ void small_stage(const DevPlan& dp, StageArgs a, const double2* zin, double2* zout,
+                                            const double2* Tin, double2* Tout, int record, double2* zs,
+                                            double2* Ws, uint64_t* bar, uint32_t& phase, double2* red,
+                                            int* s_bad) {
+  a.zin = zin;
+  a.zout = zout;
+  a.Tin = Tin;
+  a.Tout = Tout;
+  a.record = record;
+  for (int lt = 0; lt < dp.ntiles; ++lt) {
+    const TileDesc T = dp.tiles[lt];
+    double px, py;
+    const bool bad = stage_rows<MODE, true>(dp, a, T, zs, Ws, bar, phase, px, py);
+    if (MODE == MODE_S4 && bad) *s_bad = 1;
+    block_sum2(px, py, red);
+    if (threadIdx.x == 0) dp.partial[lt] = make_double2(px, py);
+    __syncthreads();
+  }
+  __threadfence_block();
+  __syncthreads();
+  finish_reduce(dp, a);
+  __threadfence_block();
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1) k_small(const DevPlan dp, StageArgs a, double2* zA, double2* zB,
+                                                       double2* TA, double2* TB, long long nsteps) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* zs = reinterpret_cast<double2*>(smem_raw);
+  double2* Ws = zs + (WZ + 8);
+  __shared__ double2 red[NWARPS];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int s_bad;
+  if (dp.has_parts && threadIdx.x < 8) zs[WZ + threadIdx.x] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    s_bad = 0;
+    mbar_init(&bar, 1);
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  // prologue: z(theta_n) and the block sums of theta_n, record n = 0
+  a.zout = zA;
+  a.Tout = TA;
+  a.record = REC_START;
+  for (int lt = 0; lt < dp.ntiles; ++lt) {
+    double x, y;
+    prologue_rows(dp, a, dp.tiles[lt], x, y);
+    block_sum2(x, y, red);
+    if (threadIdx.x == 0) dp.partial[lt] = make_double2(x, y);
+    __syncthreads();
+  }
+  __threadfence_block();
+  __syncthreads();
+  finish_reduce(dp, a);
+  __threadfence_block();
+  __syncthreads();
+  for (long long n = 0; n < nsteps; ++n) {
+    small_stage<MODE_S1>(dp, a, zA, zB, TA, TB, REC_NONE, zs, Ws, &bar, phase, red, &s_bad);
+    small_stage<MODE_S2>(dp, a, zB, zA, TB, TA, REC_NONE, zs, Ws, &bar, phase, red, &s_bad);
+    small_stage<MODE_S3>(dp, a, zA, zB, TA, TB, REC_NONE, zs, Ws, &bar, phase, red, &s_bad);
+    small_stage<MODE_S4>(dp, a, zB, zA, TB, TA, REC_STEP, zs, Ws, &bar, phase, red, &s_bad);
+  }
+  if (threadIdx.x == 0 && s_bad) dp.ctrl->nonfinite = 1;
 }
 
 // world > 1: z of the non-local rows from the exchanged stage phases (the same
@@ -448,7 +566,7 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_stage<MODE><<<dp.ntiles, NTHREADS, stage_smem_bytes(dp.rows_per_tile), s>>>(dp, a);
+  k_stage<MODE><<<dp.ntiles, NTHREADS, dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) : 0, s>>>(dp, a);
   return cudaGetLastError();
 }
 
@@ -472,6 +590,19 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
     case MODE_S4: return launch_stage_m<MODE_S4>(dp, a, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, double2* zB, double2* TA, double2* TB,
+                         long long nsteps, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)stage_smem_bytes(MAX_TILE_ROWS));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k_small<<<1, NTHREADS, dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) : 0, s>>>(dp, a, zA, zB, TA, TB, nsteps);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, cudaStream_t s) {

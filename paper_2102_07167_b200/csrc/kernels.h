@@ -25,6 +25,7 @@ struct DevPlan {
   int32_t tile_base;      // global id of local tile 0
   int32_t row_begin;      // internal id of local row 0
   int32_t world;
+  int32_t has_parts;          // any tile has stored entries (else no shared memory is needed)
   const TileDesc* tiles;      // [ntiles]
   const int32_t* order;       // [ntiles] launch order
   const PartDesc* parts;      // [n_parts]
@@ -70,6 +71,9 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
 // world > 1: after the all-gather of the packed buffers (xrecv = world x xstride doubles),
 // z of every non-local row from its exchanged phase, all tile partials; then the
 // fixed-order block-sum reduction by one CTA.
+// world == 1, tiny graphs: the whole kur_step in one single-CTA launch.
+cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, double2* zB, double2* TA, double2* TB,
+                         long long nsteps, cudaStream_t s);
 cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, cudaStream_t s);
 cudaError_t launch_finish(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
 cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, cudaStream_t s);
