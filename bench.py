@@ -168,6 +168,8 @@ def main():
     ap.add_argument("--impl", default="kur", choices=["kur", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tile-rows", type=int, default=0, help="tuning: force the tile size (rows)")
+    ap.add_argument("--hot-min", type=int, default=0, help="tuning: window staging threshold")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -191,9 +193,10 @@ def main():
     if world > 1:
         obj = [kur.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        g = kur.graph_build(inst, device=local, dist=(rank, world, obj[0]))
+        g = kur.graph_build(inst, device=local, dist=(rank, world, obj[0]), tile_rows=args.tile_rows,
+                            hot_min=args.hot_min)
     else:
-        g = kur.graph_build(inst, device=local)
+        g = kur.graph_build(inst, device=local, tile_rows=args.tile_rows, hot_min=args.hot_min)
     build_s = time.perf_counter() - t0
     info = g.info
     th = g.local(g.to_internal(torch.from_numpy(inst.theta0).to(dev))).clone()

@@ -645,13 +645,16 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
       const bool hot = pd.window >= 0;
       if (hot != (pi < T.part0 + T.nhot)) return fail(KUR_ERR_INVALID_ARG, "plan: part order");
       std::vector<uint8_t> seen((size_t)T.nrows, 0);
+      const int pcs = 1 << (pd.neg >> 8);  // row pieces per row (aligned lane groups)
       for (uint32_t c = 0; c < pd.nchunks; ++c) {
         const ChunkDesc cd = P.chunks[(size_t)pd.chunk0 + c];
         const uint16_t* hdr = reinterpret_cast<const uint16_t*>(&P.pool[(size_t)cd.ofs]);
         for (int l = 0; l < 32; ++l) {
           const uint16_t lr = hdr[l];
           if (lr != EMPTY_LANE) {
-            if (lr >= T.nrows || seen[lr]) return fail(KUR_ERR_INVALID_ARG, "plan: bad chunk header");
+            const bool lead = (l % pcs) == 0;
+            if (lr >= T.nrows || (lead && seen[lr]) || (!lead && hdr[l - l % pcs] != lr))
+              return fail(KUR_ERR_INVALID_ARG, "plan: bad chunk header");
             seen[lr] = 1;
           }
           for (uint32_t g = 0; g < cd.ng; ++g) {
@@ -670,7 +673,7 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
               }
               if (lr == EMPTY_LANE) return fail(KUR_ERR_INVALID_ARG, "plan: entry in an empty lane");
               if (col < 0 || col >= P.n) return fail(KUR_ERR_INVALID_ARG, "plan: column out of range");
-              ents.push_back(E{(int32_t)(T.row0 + lr - P.row_begin), (int32_t)col, (int8_t)pd.neg});
+              ents.push_back(E{(int32_t)(T.row0 + lr - P.row_begin), (int32_t)col, (int8_t)(pd.neg & 1)});
             }
           }
         }

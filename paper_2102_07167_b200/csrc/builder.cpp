@@ -435,24 +435,27 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   for (int64_t i = 0; i < n; ++i) inv[(size_t)P.perm[(size_t)i]] = (int32_t)i;
 
   // ------------------------------------------------------------ 4. tiles
-  // the largest tile (<= 2048 rows) that still gives >= 2 waves of 2 CTAs/SM
-  // tiny graphs run whole trajectories in one CTA (kur_step), with the largest tiles
+  // The largest power-of-two tile (256..2048 rows) that still gives >= 4
+  // tiles per SM (measured on B200: smaller tiles leave warps idle per part,
+  // larger ones unbalance heterogeneous graphs).  Tiny graphs run whole
+  // trajectories in one CTA (kur_step) with one tile.
   int64_t total_len = 0;
 #pragma omp parallel for reduction(+ : total_len)
   for (int64_t u = 0; u < n; ++u) total_len += rlen[(size_t)u];
   P.small = world == 1 && n <= 8192 && total_len <= (1 << 18);
   int rows_per_tile = force_rows ? force_rows : (P.small ? MAX_TILE_ROWS : 0);
-  for (int r = MAX_TILE_ROWS; r >= 32 && !rows_per_tile; r >>= 1) {
+  for (int r = MAX_TILE_ROWS; r >= 256 && !rows_per_tile; r >>= 1) {
     int64_t nt = 0;
     for (int32_t c = 0; c < C; ++c) nt += (S.csize[(size_t)c] + r - 1) / r;
-    if (nt >= 4LL * sm_count || r == 32) { rows_per_tile = r; break; }
+    if (nt >= 4LL * sm_count || r == 256) rows_per_tile = r;
   }
   P.rows_per_tile = rows_per_tile;
-  const int RT = P.rows_per_tile;
+  std::vector<int32_t> crt((size_t)C, rows_per_tile);
   std::vector<TileDesc> all;
   P.comm_tile0.assign((size_t)C + 1, 0);
   for (int32_t c = 0; c < C; ++c) {
     P.comm_tile0[(size_t)c] = (int32_t)all.size();
+    const int RT = crt[(size_t)c];
     for (int64_t r0 = S.moff[(size_t)c]; r0 < S.moff[(size_t)c + 1]; r0 += RT) {
       TileDesc t{};
       t.row0 = (int32_t)r0;
@@ -516,7 +519,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
 #pragma omp parallel
   {
     std::vector<uint64_t> keys, remk;
-    std::vector<int32_t> rows, rb, cnt;
+    std::vector<int32_t> rows, rb, cnt, rl;
     std::vector<uint32_t> pos;  // arranged positions of one quarter: 8 slots each
     std::vector<uint16_t> lst[8][8];
 #pragma omp for schedule(dynamic, 1)
@@ -552,12 +555,39 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
         std::vector<int32_t> ord(rows.size());
         std::iota(ord.begin(), ord.end(), 0);
         std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return cnt[(size_t)x] > cnt[(size_t)y]; });
+        rl.resize(rows.size());
+        for (size_t i = 0; i < rows.size(); ++i) rl[i] = (int32_t)((src[k0 + (size_t)rb[i]] >> 32) & 0x7FF);
+        // ROW PIECES: few long rows -> split each row over an aligned group of lp lanes (combined by
+        // a warp butterfly in the kernel) so the part still has ~16 chunks for the 16 warps
+        int lp = 0;
+        {
+          const size_t nr = rows.size(), ne = k1 - k0;
+          while (lp < 5 && nr * ((size_t)2 << lp) <= (size_t)NTHREADS && ne / (nr * ((size_t)2 << lp)) >= 16) ++lp;
+        }
+        if (lp > 0) {
+          const int pcs = 1 << lp;
+          std::vector<int32_t> vrb, vcnt, vrl;
+          for (int32_t ri : ord)
+            for (int i = 0; i < pcs; ++i) {
+              const int32_t b0 = (int32_t)((int64_t)cnt[(size_t)ri] * i / pcs);
+              const int32_t b1 = (int32_t)((int64_t)cnt[(size_t)ri] * (i + 1) / pcs);
+              vrb.push_back(rb[(size_t)ri] + b0);
+              vcnt.push_back(b1 - b0);
+              vrl.push_back(rl[(size_t)ri]);
+            }
+          rb.swap(vrb);
+          cnt.swap(vcnt);
+          rl.swap(vrl);
+          ord.resize(rb.size());
+          std::iota(ord.begin(), ord.end(), 0);  // units stay contiguous and lp-aligned
+          pd.neg |= lp << 8;
+        }
         auto slot_of = [&](int32_t ri, int e) -> uint32_t {
           return (uint32_t)((src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) - (uint64_t)window * WZ);
         };
         // chunks (lane -> row); hot parts: residue-balanced quarter-warps from 128-row pools
         std::vector<std::array<int32_t, 32>> lanes;
-        if (hot) {
+        if (hot && lp == 0) {
           plan_pools(ord, cnt, lanes, [&](int32_t ri, int* cv) {
             for (int e = 0; e < cnt[(size_t)ri]; ++e) cv[slot_of(ri, e) & 7]++;
           });
@@ -573,8 +603,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
           Unit hdr[HDR_UNITS];
           uint16_t* h16 = reinterpret_cast<uint16_t*>(hdr);
           for (int l = 0; l < 32; ++l)
-            h16[l] = lane_row[(size_t)l] >= 0 ? (uint16_t)((src[k0 + (size_t)rb[(size_t)lane_row[(size_t)l]]] >> 32) & 0x7FF)
-                                             : EMPTY_LANE;
+            h16[l] = lane_row[(size_t)l] >= 0 ? (uint16_t)rl[(size_t)lane_row[(size_t)l]] : EMPTY_LANE;
           O.units.insert(O.units.end(), hdr, hdr + HDR_UNITS);
           const size_t gbase = O.units.size();
           if (hot) {

@@ -355,9 +355,14 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       double sx, sy;
       if (hot) run_hot(q + HDR_UNITS + lane, cd.y, zs, pol, sx, sy);
       else run_remote<SMALL>(q + HDR_UNITS + lane, cd.y, a.zin, pol, sx, sy);
-      if (row != EMPTY_LANE) {
+      const int lp = P.neg >> 8;  // row pieces: 2^lp consecutive lanes hold one row
+      for (int o = 1; o < (1 << lp); o <<= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      }
+      if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) {
         double2 w = Ws[row];
-        if (P.neg) {
+        if (P.neg & 1) {
           w.x -= sx;
           w.y -= sy;
         } else {
