@@ -95,7 +95,15 @@ typedef struct {
                                window to be staged in shared memory; <= 0 selects the default */
   int32_t flags;            /* 0 (size-based choice), or a forced tile size in rows: a multiple of 32
                                in [32, 2048] (tuning / tests) */
+  int32_t scaling;          /* KUR_SCALING_UNIFORM: M_m = N (the north_star model), or
+                               KUR_SCALING_DEGREE: M_m = sum_l A_ml (a zero row gives
+                               theta_m' = omega_m).  The degree counts the off-diagonal
+                               ones plus A_mm, and A_mm = 1 only when m is listed in a KUR_ONES
+                               segment of its own community (reading R22). */
+  int32_t reserved;         /* must be 0 */
 } kur_graph_desc;
+
+enum { KUR_SCALING_UNIFORM = 0, KUR_SCALING_DEGREE = 1 };
 
 /* Multi-GPU placement: contiguous ranges of whole communities per rank,
  * balanced by stored-entry count (every rank computes the same split).
@@ -181,6 +189,16 @@ kur_status kur_group_rhs(kur_graph *const *g, int32_t world, const double *const
 kur_status kur_group_step(kur_graph *const *g, int32_t world, double *const *theta, const double *const *omega,
                           double K, double h, int64_t nsteps, int32_t record_every, double *const *r_trace,
                           void *stream);
+
+/* V_out[0] (device) = the potential of the model on the graph (eq.
+ * ExtendedPotentialConservation; P:221-233 for the complete graph):
+ *   V = -sum_m omega_m theta_m + (K/2) sum_{m,l} (A_ml / M_m) (1 - cos(theta_l - theta_m)),
+ * evaluated with the same localised sums as the RHS, through the auxiliary
+ * identity of P:457-466: sum_l A_ml cos(theta_l - theta_m) = Re(conj z_m W_m).
+ * V is a Lyapunov function of the flow for symmetric A with uniform scaling
+ * (P:212-218).  Collective for world > 1 (replicated result). */
+kur_status kur_potential(kur_graph *g, const double *theta, const double *omega, double K, double *V_out,
+                         void *stream);
 
 /* Synchronises `stream`; returns KUR_ERR_NONFINITE (and clears the flag) if a
  * previous kur_step produced a non-finite phase. */

@@ -120,6 +120,7 @@ class Instance:
     nsteps: int = 10
     record_every: int = 1
     seed: int = 0
+    scaling: int = 0  # 0: uniform M_m = N; 1: degree M_m = sum_l A_ml
     meta: dict = field(default_factory=dict)
 
     @property
@@ -282,12 +283,14 @@ def config(k):
 
 
 def from_dense(A, labels, *, kind="auto", seed=0, omega=None, theta0=None, K=1.0, h=0.01,
-               nsteps=10, record_every=1, name="dense"):
-    """Encode a dense 0/1 matrix (diagonal ignored) with community labels.
+               nsteps=10, record_every=1, name="dense", scaling=0, self_loops=False):
+    """Encode a dense 0/1 matrix with community labels.
 
     kind: 'ones' (plain CSR), 'zeros' (every block as KUR_ZEROS), 'auto'
     (per row/block whichever list is shorter), 'random' (coin per segment).
-    Small sizes only (tests).
+    The diagonal is ignored unless self_loops: then A[u,u] = 1 is stored by
+    listing u in a KUR_ONES segment of its own community (reading R22; it only
+    matters for the degree scaling).  Small sizes only (tests).
     """
     A = np.asarray(A).astype(np.uint8)
     n = A.shape[0]
@@ -304,7 +307,11 @@ def from_dense(A, labels, *, kind="auto", seed=0, omega=None, theta0=None, K=1.0
             row = A[u, m_off]
             ones = m_off[row == 1]
             zeros = m_off[row == 0]
-            if kind == "ones":
+            loop = bool(self_loops and b == labels[u] and A[u, u])
+            if loop:
+                kd = KUR_ONES
+                ones = np.sort(np.concatenate([ones, [u]])).astype(np.int32)
+            elif kind == "ones":
                 kd = KUR_ONES
             elif kind == "zeros":
                 kd = KUR_ZEROS
@@ -330,7 +337,7 @@ def from_dense(A, labels, *, kind="auto", seed=0, omega=None, theta0=None, K=1.0
                     seg_kind=np.asarray(seg_kind, np.uint8),
                     idx_ptr=np.asarray(idx_ptr, np.int64), idx=np.asarray(idx, np.int32),
                     omega=om.copy(), theta0=th.copy(), K=K, h=h, nsteps=nsteps,
-                    record_every=record_every, seed=seed)
+                    record_every=record_every, seed=seed, scaling=scaling)
 
 
 def random_dense(n, C, seed, p_in=0.8, p_out=0.1, symmetric=True):

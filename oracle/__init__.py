@@ -40,6 +40,9 @@ def _load():
     lib.orc_order_parameter.argtypes = [i64, p, p]
     lib.orc_row_degree.argtypes = [p, p]
     lib.orc_num_threads.restype = ctypes.c_int
+    lib.orc_graph_set_scaling.argtypes = [p, ctypes.c_int]
+    lib.orc_potential.argtypes = [p, d, p, p]
+    lib.orc_potential.restype = d
     lib.orc_set_num_threads.argtypes = [ctypes.c_int]
     return lib
 
@@ -76,6 +79,8 @@ class Graph:
             inst.idx_ptr.astype(np.int64, copy=False), inst.idx.astype(np.int32, copy=False))]
         self.n = int(inst.n)
         self._h = lib().orc_graph_new(self.n, int(inst.n_comm), *[_p(a) for a in self._keep])
+        self.scaling = int(getattr(inst, "scaling", 0))
+        lib().orc_graph_set_scaling(self._h, self.scaling)
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -117,6 +122,13 @@ def rk4(g: Graph, theta0, omega, K, h, nsteps, record_every=1, mode="matvec"):
     if rc:
         raise ValueError("orc_rk4 failed")
     return th, th10, rt[:nrec]
+
+
+def potential(g: Graph, theta, omega, K):
+    """V(theta) of P:474-487 from its definition (uses the graph's scaling)."""
+    theta = np.ascontiguousarray(theta, np.float64)
+    omega = np.ascontiguousarray(omega, np.float64)
+    return float(lib().orc_potential(g._h, float(K), _p(theta), _p(omega)))
 
 
 def order_parameter(theta):

@@ -16,6 +16,9 @@
  * evaluated by direct O(nnz) summation — no block sums, no localised order
  * parameters, no permutation.  The community labels are
  * used ONLY to decode KUR_ZEROS segments into the explicit list of ones.
+ * orc_graph_set_scaling selects the non-uniform scaling M_m = sum_l A_ml of
+ * P:409-415 instead (zero rows: theta_m' = omega_m),
+ * and orc_potential evaluates the potential V of P:474-487 (NEXT-1).
  *
  * Three evaluation modes:
  *   ORC_NAIVE  (0)  per-edge sin(theta_l - theta_m), P:388 (and P:130 for the
@@ -46,7 +49,7 @@
 #include <string.h>
 #include <omp.h>
 
-enum { ORC_NAIVE = 0, ORC_MATVEC = 1, ORC_OP = 2 };
+enum { ORC_NAIVE = 0, ORC_MATVEC = 1, ORC_OP = 2, ORC_COSINE = 3 /* internal: potential */ };
 enum { SEG_ONES = 0, SEG_ZEROS = 1 }; /* row-segment kinds (see kurgen/) */
 
 /* Graph as given by the caller (user numbering):
@@ -68,7 +71,25 @@ typedef struct {
   const int32_t *idx;
   int64_t *member_off; /* [n_comm+1] */
   int32_t *members;    /* ascending user ids per community */
+  int scaling;         /* ORC_UNIFORM: M_m = M; ORC_DEGREE: M_m = sum_l A_ml */
 } orc_graph;
+
+enum { ORC_UNIFORM = 0, ORC_DEGREE = 1 };
+
+/* Select the scaling M_m of P:388 (reading R22 of DESIGN.md for the degree:
+ * the off-diagonal ones plus A_mm, which is 1 only when m is listed in a
+ * KUR_ONES segment of its own community). */
+void orc_graph_set_scaling(orc_graph *g, int scaling) { g->scaling = scaling; }
+
+/* 1 iff row u lists itself in a ONES segment (a stored self-loop). */
+static int self_loop(const orc_graph *g, int64_t u) {
+  for (int64_t sg = g->seg_ptr[u]; sg < g->seg_ptr[u + 1]; ++sg) {
+    if (g->seg_kind[sg] != SEG_ONES || g->seg_comm[sg] != g->community[u]) continue;
+    for (int64_t e = g->idx_ptr[sg]; e < g->idx_ptr[sg + 1]; ++e)
+      if (g->idx[e] == u) return 1;
+  }
+  return 0;
+}
 
 orc_graph *orc_graph_new(int64_t n, int32_t n_comm, const int32_t *community,
                          const int64_t *seg_ptr, const int32_t *seg_comm,
@@ -117,6 +138,8 @@ static int64_t row_sums(const orc_graph *g, int64_t u, int mode, const double *t
     if ((l) != u) {                                   \
       if (mode == ORC_NAIVE) {                        \
         acc0 += sin(theta[(l)] - tu);                 \
+      } else if (mode == ORC_COSINE) {                \
+        acc0 += cos(theta[(l)] - tu);                 \
       } else {                                        \
         acc0 += s[(l)];                               \
         acc1 += c[(l)];                               \
@@ -176,6 +199,7 @@ int orc_rhs(const orc_graph *g, int mode, double K, const double *theta,
   const int64_t n = g->n;
   if (mode != ORC_NAIVE && mode != ORC_MATVEC && mode != ORC_OP) return -1;
   const int64_t cnt = rows ? nrows : n;
+  if (mode == ORC_OP && g->scaling != ORC_UNIFORM) return -1; /* classical model only */
   if (mode == ORC_OP) { /* P:249-255 */
     double C, S;
     order_sums(n, theta, &C, &S);
@@ -198,16 +222,21 @@ int orc_rhs(const orc_graph *g, int mode, double K, const double *theta,
       c[l] = cos(theta[l]);
     }
   }
-  const double M = (double)n; /* uniform scaling M_m = M */
 #pragma omp parallel for schedule(dynamic, 64)
   for (int64_t i = 0; i < cnt; ++i) {
     const int64_t m = rows ? rows[i] : i;
     double a0, a1;
-    row_sums(g, m, mode, theta, s, c, &a0, &a1);
+    const int64_t ones = row_sums(g, m, mode, theta, s, c, &a0, &a1);
+    /* scaling M_m: uniform M or the row degree */
+    const double M = g->scaling == ORC_UNIFORM ? (double)n : (double)(ones + self_loop(g, m));
+    if (M == 0.0) { /* zero row: theta_m' = omega_m, "the scaling is dispensible" */
+      out[i] = omega[m];
+      continue;
+    }
     if (mode == ORC_NAIVE) {
       out[i] = omega[m] + (K / M) * a0;
     } else {
-      const double As = a0 / M, Ac = a1 / M; /* (A sin)_m, (A cos)_m with A = A/M */
+      const double As = a0 / M, Ac = a1 / M; /* (A sin)_m, (A cos)_m with A = A/M_m */
       out[i] = omega[m] + K * (As * c[m] - Ac * s[m]);
     }
   }
@@ -280,6 +309,30 @@ int orc_rk4(const orc_graph *g, int mode, double K, double h, int64_t nsteps,
   free(k4);
   free(ts);
   return rc;
+}
+
+/* Potential of the model on a graph (eq. ExtendedPotentialConservation;
+ * P:221-233 for the complete graph), evaluated from its definition
+ *     V = -sum_m omega_m theta_m + (K/2) sum_{m,l} (A_ml / M_m) (1 - cos(theta_l - theta_m)),
+ * with M_m the graph's scaling (rows with M_m = 0 contribute nothing).  Per-row
+ * terms are computed in parallel, then summed sequentially in row order. */
+double orc_potential(const orc_graph *g, double K, const double *theta, const double *omega) {
+  const int64_t n = g->n;
+  double *term = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t m = 0; m < n; ++m) {
+    double a0, a1;
+    const int64_t ones = row_sums(g, m, ORC_COSINE, theta, NULL, NULL, &a0, &a1);
+    const double M = g->scaling == ORC_UNIFORM ? (double)n : (double)(ones + self_loop(g, m));
+    term[m] = M == 0.0 ? 0.0 : ((double)ones - a0) / M; /* sum_l A_ml (1 - cos), diagonal term 0 */
+  }
+  double wt = 0.0, s = 0.0;
+  for (int64_t m = 0; m < n; ++m) {
+    wt += omega[m] * theta[m];
+    s += term[m];
+  }
+  free(term);
+  return -wt + (K / 2.0) * s;
 }
 
 int orc_num_threads(void) { return omp_get_max_threads(); }

@@ -63,6 +63,7 @@ struct kur_graph {
   ncclComm_t comm = nullptr;
   int world = 1;
   int32_t *d_shard_row0 = nullptr, *d_shard_tile0 = nullptr;
+  double *d_rowscale = nullptr, *d_potc = nullptr;
   double *xsend = nullptr, *xrecv = nullptr;  // world > 1: packed exchange buffers
   // optional per-launch CUDA-event timing (kur_timing)
   bool timing = false;
@@ -85,7 +86,7 @@ struct kur_graph {
     cudaSetDevice(device);
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
-                    xsend, xrecv};
+                    xsend, xrecv, d_rowscale, d_potc};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -189,6 +190,8 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   if ((e = upload(&g->d_D_idx, P.D_idx)) != cudaSuccess) return bail(e, "D_idx");
   if ((e = upload(&g->d_csize, csize)) != cudaSuccess) return bail(e, "comm sizes");
   if ((e = upload(&g->d_perm, P.perm)) != cudaSuccess) return bail(e, "perm");
+  if (!P.rowscale.empty() && (e = upload(&g->d_rowscale, P.rowscale)) != cudaSuccess) return bail(e, "rowscale");
+  if ((e = upload(&g->d_potc, P.potc)) != cudaSuccess) return bail(e, "potc");
   const size_t zbytes = sizeof(double2) * (size_t)g->n_pad;
   if ((e = cudaMalloc((void**)&g->zA, zbytes)) != cudaSuccess) return bail(e, "zA");
   if ((e = cudaMalloc((void**)&g->zB, zbytes)) != cudaSuccess) return bail(e, "zB");
@@ -243,6 +246,8 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   dp.row_begin = (int32_t)P.row_begin;
   dp.world = world;
   dp.rank = rank;
+  dp.rowscale = g->d_rowscale;
+  dp.potc = g->d_potc;
   dp.has_parts = 0;
   for (const TileDesc& T : P.tiles)
     if (T.nparts > 0) dp.has_parts = 1;
@@ -341,6 +346,7 @@ struct RankIO {
   double* out;      // dtheta (RHS)
   double* op_rpsi;  // order parameter outputs
   double* op_local;
+  double* v_out;    // kur_potential output
 };
 
 kur_status exchange(const std::vector<kur_graph*>& gs, cudaStream_t s) {
@@ -381,6 +387,8 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
     a.record = record;
     a.op_rpsi = io[r].op_rpsi;
     a.op_local = io[r].op_local;
+    a.K = K;
+    a.v_out = mode == MODE_POT ? io[r].v_out : nullptr;
     a.xsend = world > 1 ? g->xsend : nullptr;
     if (mode == PH_PROLOGUE) {
       a.zout = g->zA;
@@ -451,6 +459,7 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
     a.omega = io[0].omega;
     a.acc = g->acc;
     a.KN = K / (double)g->n;
+    a.K = K;
     a.h = h;
     KUR_CUDA(g->mark(s));
     KUR_CUDA(launch_small(g->dp, a, g->zA, g->zB, g->TA, g->TB, (long long)nsteps, s));
@@ -499,6 +508,21 @@ kur_status kur_order_parameter(kur_graph* g, const double* theta, double* r_psi,
   KUR_CUDA(cudaSetDevice(g->device));
   return run_phase(gs, PH_PROLOGUE, {RankIO{const_cast<double*>(theta), nullptr, nullptr, r_psi, local}}, 0.0, 0.0,
                    REC_NONE, true, (cudaStream_t)stream);
+}
+
+kur_status kur_potential(kur_graph* g, const double* theta, const double* omega, double K, double* V_out,
+                         void* stream) {
+  if (!g || !V_out) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  if (g->n_local > 0 && (!theta || !omega)) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
+  std::vector<kur_graph*> gs{g};
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
+  KUR_CUDA(cudaSetDevice(g->device));
+  std::vector<RankIO> io{RankIO{const_cast<double*>(theta), omega, nullptr, nullptr, nullptr, V_out}};
+  st = run_phase(gs, PH_PROLOGUE, io, K, 0.0, REC_NONE, true, (cudaStream_t)stream);
+  if (st != KUR_OK) return st;
+  return run_phase(gs, MODE_POT, io, K, 0.0, REC_NONE, true, (cudaStream_t)stream);
 }
 
 kur_status kur_group_rhs(kur_graph* const* g, int32_t world, const double* const* theta,

@@ -264,6 +264,11 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     return KUR_ERR_INVALID_ARG;
   }
   if (d->n >= INT32_MAX - 2 * WZ) { err = "n too large for int32 internal ids"; return KUR_ERR_UNSUPPORTED; }
+  if (d->scaling != KUR_SCALING_UNIFORM && d->scaling != KUR_SCALING_DEGREE) {
+    err = "scaling must be KUR_SCALING_UNIFORM or KUR_SCALING_DEGREE";
+    return KUR_ERR_INVALID_ARG;
+  }
+  if (d->reserved != 0) { err = "reserved must be 0"; return KUR_ERR_INVALID_ARG; }
   const int force_rows = d->flags;
   if (force_rows != 0 && (force_rows < 32 || force_rows > MAX_TILE_ROWS || force_rows % 32 != 0)) {
     err = "flags: 0 or a tile size in rows (multiple of 32 in [32, 2048])";
@@ -383,7 +388,8 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   for (int32_t a = 0; a < C; ++a) P.D_idx.insert(P.D_idx.end(), Dl[(size_t)a].begin(), Dl[(size_t)a].end());
 
   // ------------------------------------------------------------ 3. lengths + order
-  std::vector<int64_t> rlen((size_t)n, 0);
+  std::vector<int64_t> rlen((size_t)n, 0), ones_off((size_t)n, 0);
+  std::vector<uint8_t> selfl((size_t)n, 0);
 #pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t u = 0; u < n; ++u) {
     const int32_t a = d->community[u];
@@ -391,7 +397,21 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     const int64_t s1 = d->seg_ptr[u + 1];
     int32_t di = P.D_ptr[(size_t)a];
     const int32_t d1 = P.D_ptr[(size_t)a + 1];
-    int64_t L = 0;
+    int64_t L = 0, ones = 0;
+    for (int64_t t = s; t < s1; ++t) {  // degree: off-diagonal ones, and a listed self-loop (R22)
+      const int32_t b = d->seg_comm[t];
+      const int32_t* lst = d->idx + d->idx_ptr[t];
+      const int64_t len = d->idx_ptr[t + 1] - d->idx_ptr[t];
+      const bool diag = b == a && has_diag(lst, len, (int32_t)u);
+      const int64_t lnd = len - (diag ? 1 : 0);
+      if (d->seg_kind[t] == KUR_ONES) {
+        ones += lnd;
+        if (diag) selfl[(size_t)u] = 1;
+      } else {
+        ones += S.csize[(size_t)b] - (b == a ? 1 : 0) - lnd;
+      }
+    }
+    ones_off[(size_t)u] = ones;
     while (s < s1 || di < d1) {
       const int32_t bs = s < s1 ? d->seg_comm[s] : INT32_MAX;
       const int32_t bd = di < d1 ? P.D_idx[(size_t)di] : INT32_MAX;
@@ -742,6 +762,27 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
       P.chunks[(size_t)cofs[(size_t)lt] + c] = cd;
     }
     std::vector<Unit>().swap(O.units);
+  }
+  // per local row: scale 1/M_m for the degree scaling (0 for a zero
+  // row) and the potential constant ones_off + [z_m inside W_m]
+  // (own block dense: its block sum includes z_m), see kur_potential.
+  {
+    const int64_t nl = P.row_end - P.row_begin;
+    P.potc.assign((size_t)std::max<int64_t>(nl, 1), 0.0);
+    if (d->scaling == KUR_SCALING_DEGREE) P.rowscale.assign((size_t)std::max<int64_t>(nl, 1), 0.0);
+    std::vector<uint8_t> self_dense((size_t)C, 0);
+    for (int32_t a = 0; a < C; ++a)
+      for (int32_t i = P.D_ptr[(size_t)a]; i < P.D_ptr[(size_t)a + 1]; ++i)
+        if (P.D_idx[(size_t)i] == a) self_dense[(size_t)a] = 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t li = 0; li < nl; ++li) {
+      const int32_t u = P.perm[(size_t)(P.row_begin + li)];
+      P.potc[(size_t)li] = (double)ones_off[(size_t)u] + (double)self_dense[(size_t)d->community[u]];
+      if (d->scaling == KUR_SCALING_DEGREE) {
+        const int64_t deg = ones_off[(size_t)u] + selfl[(size_t)u];
+        P.rowscale[(size_t)li] = deg > 0 ? 1.0 / (double)deg : 0.0;
+      }
+    }
   }
   // launch order: decreasing work (longest-processing-time first)
   P.tile_order.resize((size_t)nt);

@@ -199,6 +199,14 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
   __shared__ double2 fred[NWARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int BIG = 64;  // communities with more tiles are reduced by the whole CTA
+  if (a.v_out) {  // kur_potential: V = sum of the tile partials in tile order (fixed shape)
+    double x = 0.0, y = 0.0;
+    const int nt = dp.comm_tile0[dp.C];
+    for (int t = tid; t < nt; t += NTHREADS) x += __ldcg(dp.partial + t).x;
+    block_sum2(x, y, fred);
+    if (tid == 0) a.v_out[0] = x;
+    return;
+  }
   for (int c = warp; c < dp.C; c += NWARPS) {  // S_b = sum of its tiles' partials
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
     if (t1 - t0 > BIG) continue;
@@ -386,7 +394,14 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     const double2 w = parts ? Ws[lr] : make_double2(0.0, 0.0);
     const double wx = Tc.x + w.x, wy = Tc.y + w.y;
     const double2 zj = SMALL ? __ldcg(a.zin + row) : a.zin[row];
-    const double k = a.omega[li] + a.KN * (zj.x * wy - zj.y * wx);
+    // K/M_m: uniform K/N, or K/deg_m for the degree scaling
+    const double kn = dp.rowscale ? a.K * dp.rowscale[li] : a.KN;
+    if (MODE == MODE_POT) {  // -omega_m theta_m + (K/2)(1/M_m)(sum_l A_ml - Re(conj z_m W_m))
+      const double sm = dp.rowscale ? dp.rowscale[li] : a.KN / a.K;
+      px += -a.omega[li] * a.theta[li] + 0.5 * a.K * sm * (dp.potc[li] - (zj.x * wx + zj.y * wy));
+      continue;
+    }
+    const double k = a.omega[li] + kn * (zj.x * wy - zj.y * wx);
     if (MODE == MODE_RHS) {
       a.out[li] = k;
     } else {
@@ -593,6 +608,7 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
     case MODE_S2: return launch_stage_m<MODE_S2>(dp, a, s);
     case MODE_S3: return launch_stage_m<MODE_S3>(dp, a, s);
     case MODE_S4: return launch_stage_m<MODE_S4>(dp, a, s);
+    case MODE_POT: return launch_stage_m<MODE_POT>(dp, a, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -41,12 +41,14 @@ struct DevPlan {
   int32_t xrows;              // max rows of a shard (theta region of the exchange buffer)
   const int32_t* shard_row0;  // [world+1] internal row range of every rank
   const int32_t* shard_tile0; // [world+1] tile range of every rank
+  const double* rowscale;     // [local rows] 1/M_m (degree scaling) or NULL (uniform: K/N)
+  const double* potc;         // [local rows] potential constants (kur_potential)
   double2* partial;           // [ntiles_all] per-tile sums of z (global tile ids)
   double2* S;                 // [C] block sums S_b of the last reduction
   Ctrl* ctrl;
 };
 
-enum StageMode { MODE_RHS = 0, MODE_S1 = 1, MODE_S2 = 2, MODE_S3 = 3, MODE_S4 = 4 };
+enum StageMode { MODE_RHS = 0, MODE_S1 = 1, MODE_S2 = 2, MODE_S3 = 3, MODE_S4 = 4, MODE_POT = 5 };
 enum RecordMode { REC_NONE = 0, REC_START = 1, REC_STEP = 2 };
 
 struct StageArgs {
@@ -59,7 +61,9 @@ struct StageArgs {
   const double2* Tin;     // [C] T_a = sum_{b in D(a)} S_b of the stage state
   double2* Tout;          // [C] T of the next stage state
   double KN;              // K / N
+  double K;               // coupling (degree scaling and potential)
   double h;               // step
+  double* v_out;          // MODE_POT: device scalar receiving V
   double* op_rpsi;        // kur_order_parameter outputs (device) or NULL
   double* op_local;
   int record;             // RecordMode

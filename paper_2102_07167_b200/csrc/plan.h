@@ -92,6 +92,8 @@ struct HostPlan {
   std::vector<ChunkDesc> chunks;    // this rank's chunks
   std::vector<Unit> pool;           // index data
   std::vector<int32_t> tile_order;  // launch order (local tile ids, decreasing work)
+  std::vector<double> rowscale;     // [local rows] 1/M_m (degree scaling only; empty = uniform K/N)
+  std::vector<double> potc;         // [local rows] off-diagonal ones + [z_m inside W_m] (kur_potential)
   std::vector<int32_t> shard_row0;  // [world+1] internal row ranges of all ranks
   std::vector<int32_t> shard_tile0; // [world+1]
   // statistics (this rank)

@@ -37,7 +37,7 @@ _d = ctypes.c_double
 class GraphDesc(ctypes.Structure):
     _fields_ = [("n", _i64), ("n_comm", _i32), ("community", _p), ("seg_ptr", _p), ("seg_comm", _p),
                 ("seg_kind", _p), ("idx_ptr", _p), ("idx", _p), ("dense_threshold", _d),
-                ("hot_min", _i32), ("flags", _i32)]
+                ("hot_min", _i32), ("flags", _i32), ("scaling", _i32), ("reserved", _i32)]
 
 
 class DistDesc(ctypes.Structure):
@@ -62,6 +62,7 @@ _lib.kur_rhs.argtypes = [_p, _p, _p, _d, _p, _p]
 _lib.kur_step.argtypes = [_p, _p, _p, _d, _d, _i64, _i32, _p, _p]
 _lib.kur_order_parameter.argtypes = [_p, _p, _p, _p, _p]
 _lib.kur_check.argtypes = [_p, _p]
+_lib.kur_potential.argtypes = [_p, _p, _p, _d, _p, _p]
 _lib.kur_timing.argtypes = [_p, _i32]
 _lib.kur_timing_read.argtypes = [_p, _p]
 _lib.kur_nccl_unique_id.argtypes = [_p]
@@ -72,13 +73,13 @@ _lib.kur_status_string.argtypes = [ctypes.c_int]
 _lib.kur_last_error.restype = ctypes.c_char_p
 for _f in ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
            "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id", "kur_timing",
-           "kur_timing_read", "kur_group_rhs", "kur_group_step"):
+           "kur_timing_read", "kur_group_rhs", "kur_group_step", "kur_potential"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
             "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id",
             "kur_status_string", "kur_last_error", "kur_timing", "kur_timing_read", "kur_group_rhs",
-            "kur_group_step")
+            "kur_group_step", "kur_potential")
 
 
 class KurError(RuntimeError):
@@ -168,11 +169,16 @@ class Graph:
         return x_internal_full[self.row_begin:self.row_end]
 
 
-def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, device=None, dist=None, **arrays):
-    """kur_graph_build from a kurgen.Instance (or the same arrays as keywords)."""
+def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, scaling=None, device=None, dist=None,
+                **arrays):
+    """kur_graph_build from a kurgen.Instance (or the same arrays as keywords).
+
+    scaling: 0 = uniform K/N (default, or inst.scaling), 1 = degree K/deg_m."""
     src = arrays if inst is None else dict(
         n=inst.n, n_comm=inst.n_comm, community=inst.community, seg_ptr=inst.seg_ptr,
         seg_comm=inst.seg_comm, seg_kind=inst.seg_kind, idx_ptr=inst.idx_ptr, idx=inst.idx)
+    if scaling is None:
+        scaling = int(getattr(inst, "scaling", 0)) if inst is not None else int(arrays.get("scaling", 0))
     keep = dict(
         community=np.ascontiguousarray(src["community"], np.int32),
         seg_ptr=np.ascontiguousarray(src["seg_ptr"], np.int64),
@@ -184,7 +190,8 @@ def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, devi
                      community=_np_ptr(keep["community"]), seg_ptr=_np_ptr(keep["seg_ptr"]),
                      seg_comm=_np_ptr(keep["seg_comm"]), seg_kind=_np_ptr(keep["seg_kind"]),
                      idx_ptr=_np_ptr(keep["idx_ptr"]), idx=_np_ptr(keep["idx"]),
-                     dense_threshold=float(dense_threshold), hot_min=int(hot_min), flags=int(tile_rows))
+                     dense_threshold=float(dense_threshold), hot_min=int(hot_min), flags=int(tile_rows),
+                     scaling=int(scaling), reserved=0)
     if device is None:
         device = torch.cuda.current_device()
     dd = None
@@ -283,6 +290,15 @@ def group_step(graphs, thetas, omegas, K, h, nsteps, record_every=0, stream=None
     return rts
 
 
+def potential(g: Graph, theta, omega, K, stream=None):
+    """V(theta) as a device tensor [1]."""
+    out = torch.empty(1, dtype=torch.float64, device=f"cuda:{g.device}")
+    _check(_lib.kur_potential(g._h, _dev_vec(theta, g.n_local, g.device, "theta"),
+                              _dev_vec(omega, g.n_local, g.device, "omega"), float(K),
+                              ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+    return out
+
+
 def check(g: Graph, stream=None):
     _check(_lib.kur_check(g._h, _stream(stream)))
 
@@ -320,7 +336,8 @@ def _desc_from(inst, dense_threshold=-1.0, hot_min=0, tile_rows=0):
                      seg_ptr=_np_ptr(keep["seg_ptr"]), seg_comm=_np_ptr(keep["seg_comm"]),
                      seg_kind=_np_ptr(keep["seg_kind"]), idx_ptr=_np_ptr(keep["idx_ptr"]),
                      idx=_np_ptr(keep["idx"]), dense_threshold=float(dense_threshold),
-                     hot_min=int(hot_min), flags=int(tile_rows))
+                     hot_min=int(hot_min), flags=int(tile_rows), scaling=int(getattr(inst, "scaling", 0)),
+                     reserved=0)
     return desc, keep
 
 

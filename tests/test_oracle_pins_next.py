@@ -1,0 +1,134 @@
+"""Pins for the oracle's NEXT-row functions:
+NEXT-2 non-uniform scaling M_m = sum_l A_ml and NEXT-1 the
+potential V (P:474-487 on graphs, P:221-233 for the complete graph)."""
+import math
+
+import numpy as np
+import pytest
+
+import kurgen
+import oracle
+
+
+def _inst(A, labels, theta, omega, scaling, **kw):
+    return kurgen.from_dense(A, labels, theta0=np.asarray(theta, float), omega=np.asarray(omega, float),
+                             scaling=scaling, **kw)
+
+
+# ---------------------------------------------------------------- NEXT-2 degree scaling
+def test_spec_directed_edge_degree_scaling():
+    """M=2, only edge 0->1, theta=(0, pi/2), omega=0, K=1, non-uniform -> (1, 0);
+    row 1 has degree 0, so theta_1' = omega_1."""
+    A = np.array([[0, 1], [0, 0]], np.uint8)
+    inst = _inst(A, [0, 0], [0.0, math.pi / 2], [0.0, 0.0], 1, kind="ones")
+    g = oracle.Graph(inst)
+    for mode in ("naive", "matvec"):
+        f = oracle.rhs(g, inst.theta0, inst.omega, 1.0, mode=mode)
+        assert f[0] == 1.0 and f[1] == 0.0, (mode, f)
+
+
+def test_block_example_P502():
+    """A = [[ones(M0 x M0), 0], [0, 0]] (diagonal included) with
+    M_m = M0: the first M0 oscillators form a classical Kuramoto model of M0
+    oscillators, f_m = omega_m + K r0 sin(psi0 - theta_m) with r0 e^{i psi0} the block's
+    order parameter, the rest are free, f_m = omega_m."""
+    M, M0, K = 40, 25, 2.5
+    A = np.zeros((M, M), np.uint8)
+    A[:M0, :M0] = 1
+    th = kurgen.uniform(3, 2, M, 0, 2 * math.pi)
+    om = kurgen.normal(3, 1, M)
+    inst = _inst(A, np.zeros(M, np.int32), th, om, 1, kind="random", self_loops=True)
+    g = oracle.Graph(inst)
+    z0 = np.exp(1j * th[:M0]).mean()
+    ref = om.copy()
+    ref[:M0] = om[:M0] + K * abs(z0) * np.sin(np.angle(z0) - th[:M0])
+    for mode in ("naive", "matvec"):
+        f = oracle.rhs(g, th, om, K, mode=mode)
+        assert np.max(np.abs(f[:M0] - ref[:M0])) <= 1e-13
+        assert np.array_equal(f[M0:], om[M0:])
+
+
+def test_degree_vs_uniform_on_regular_graph():
+    """Complete graph without self-loops: deg = N - 1, so f_deg - omega = N/(N-1) (f_uni - omega)."""
+    N = 300
+    A = np.ones((N, N), np.uint8) - np.eye(N, dtype=np.uint8)
+    th = kurgen.uniform(4, 2, N, 0, 2 * math.pi)
+    om = kurgen.normal(4, 1, N)
+    fu = oracle.rhs(oracle.Graph(_inst(A, np.zeros(N, np.int32), th, om, 0)), th, om, 3.0)
+    fd = oracle.rhs(oracle.Graph(_inst(A, np.zeros(N, np.int32), th, om, 1)), th, om, 3.0)
+    assert np.max(np.abs((fd - om) - N / (N - 1) * (fu - om))) <= 1e-13
+
+
+def test_degree_matches_bruteforce():
+    A, labels = kurgen.random_dense(50, 3, seed=8, p_in=0.6, p_out=0.1, symmetric=False)
+    A[7] = 0  # a zero row
+    inst = kurgen.from_dense(A, labels, kind="random", seed=1, scaling=1)
+    f = oracle.rhs(oracle.Graph(inst), inst.theta0, inst.omega, 1.7, mode="naive")
+    for m in range(50):
+        nb = [l for l in range(50) if l != m and A[m, l]]
+        ref = inst.omega[m] + (1.7 / len(nb) * math.fsum(math.sin(inst.theta0[l] - inst.theta0[m]) for l in nb)
+                               if nb else 0.0)
+        assert abs(f[m] - ref) <= 1e-14, m
+    assert f[7] == inst.omega[7]
+
+
+def test_degree_scaling_breaks_conservation():
+    """with non-uniform scaling the scaled matrix is not symmetric and the sum
+    over all phases is not conserved (non-vacuity of O3)."""
+    inst = kurgen.sbm([60, 20], [[0.9, 0.05], [0.05, 0.3]], 12)
+    inst.scaling = 1
+    g = oracle.Graph(inst)
+    d = oracle.rhs(g, inst.theta0, inst.omega, 2.0) - inst.omega
+    assert abs(math.fsum(d)) > 1e-6
+
+
+# ---------------------------------------------------------------- NEXT-1 potential
+def test_potential_classical_closed_form():
+    """V = -omega^T theta + (KM/2)(1 - C_M^2 - S_M^2) for the complete graph."""
+    N, K = 500, 1.7
+    A = np.ones((N, N), np.uint8) - np.eye(N, dtype=np.uint8)
+    th = kurgen.uniform(6, 2, N, 0, 2 * math.pi)
+    om = kurgen.normal(6, 1, N)
+    g = oracle.Graph(_inst(A, np.zeros(N, np.int32), th, om, 0))
+    C, S = np.cos(th).mean(), np.sin(th).mean()
+    ref = -math.fsum(om * th) + K * N / 2 * (1 - C * C - S * S)
+    assert abs(oracle.potential(g, th, om, K) - ref) <= 1e-10 * (1 + abs(ref))
+
+
+def test_potential_examples():
+    """all phases equal, omega = 0 -> V = 0; theta=(0, pi), omega=0, K=1, M=2 -> V = 1."""
+    A = np.array([[0, 1], [1, 0]], np.uint8)
+    g = oracle.Graph(_inst(A, [0, 0], [0.3, 0.3], [0, 0], 0))
+    assert abs(oracle.potential(g, [0.3, 0.3], [0.0, 0.0], 1.0)) <= 1e-16
+    assert abs(oracle.potential(g, [0.0, math.pi], [0.0, 0.0], 1.0) - 1.0) <= 1e-15
+
+
+@pytest.mark.parametrize("scaling", [0])
+def test_potential_gradient_is_minus_rhs(scaling):
+    """Gradient structure: for symmetric A and uniform scaling
+    -dV/dtheta_m = f_m (central differences)."""
+    A, labels = kurgen.random_dense(30, 2, seed=5, p_in=0.7, p_out=0.2, symmetric=True)
+    inst = kurgen.from_dense(A, labels, seed=2, scaling=scaling)
+    g = oracle.Graph(inst)
+    K, eps = 2.0, 1e-6
+    f = oracle.rhs(g, inst.theta0, inst.omega, K)
+    for m in range(30):
+        tp = inst.theta0.copy()
+        tm = inst.theta0.copy()
+        tp[m] += eps
+        tm[m] -= eps
+        dV = (oracle.potential(g, tp, inst.omega, K) - oracle.potential(g, tm, inst.omega, K)) / (2 * eps)
+        assert abs(-dV - f[m]) <= 1e-6, m
+
+
+def test_potential_decreases_along_rk4():
+    """dV/dt = -|grad V|^2 <= 0 along the flow (symmetric, uniform)."""
+    inst = kurgen.sbm([80, 40], [[0.9, 0.1], [0.1, 0.7]], 21, K=3.0)
+    g = oracle.Graph(inst)
+    th = inst.theta0.copy()
+    v = oracle.potential(g, th, inst.omega, inst.K)
+    for _ in range(30):
+        th, _, _ = oracle.rk4(g, th, inst.omega, inst.K, 0.01, 1, 0, mode="naive")
+        v2 = oracle.potential(g, th, inst.omega, inst.K)
+        assert v2 <= v + 1e-12
+        v = v2
