@@ -44,6 +44,8 @@ def _load():
     lib.orc_potential.argtypes = [p, d, p, p]
     lib.orc_potential.restype = d
     lib.orc_set_num_threads.argtypes = [ctypes.c_int]
+    lib.orc_step_method.argtypes = [p, ctypes.c_int, ctypes.c_int, d, d, i64, i32, p, p, p, d, i32]
+    lib.orc_step_method.restype = ctypes.c_int
     return lib
 
 
@@ -122,6 +124,24 @@ def rk4(g: Graph, theta0, omega, K, h, nsteps, record_every=1, mode="matvec"):
     if rc:
         raise ValueError("orc_rk4 failed")
     return th, th10, rt[:nrec]
+
+
+METHODS = {"euler": 1, "heun": 2, "implicit_midpoint": 3}
+
+
+def step_method(g: Graph, method, theta0, omega, K, h, nsteps, record_every=1, mode="matvec", fp_tol=1e-13,
+                fp_max_iter=50):
+    """Euler / Heun / implicit midpoint (NEXT-4); returns (theta_final, r_trace[nrec, 2])."""
+    th = np.array(theta0, np.float64, copy=True)
+    omega = np.ascontiguousarray(omega, np.float64)
+    nrec = (nsteps // record_every + 1) if record_every > 0 else 0
+    rt = np.zeros((max(nrec, 1), 2), np.float64)
+    rc = lib().orc_step_method(g._h, METHODS[method], _MODES[mode], float(K), float(h), int(nsteps),
+                               int(record_every), _p(th), _p(omega), _p(rt) if nrec else None, float(fp_tol),
+                               int(fp_max_iter))
+    if rc:
+        raise ValueError("orc_step_method failed")
+    return th, rt[:nrec]
 
 
 def potential(g: Graph, theta, omega, K):

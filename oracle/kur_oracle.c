@@ -311,6 +311,58 @@ int orc_rk4(const orc_graph *g, int mode, double K, double h, int64_t nsteps,
   return rc;
 }
 
+/* Other one-step integrators of the paper, fixed step h:
+ *   ORC_EULER (1): theta_{n+1} = theta_n + h F(theta_n)
+ *   ORC_HEUN  (2): k1 = F(theta_n), k2 = F(theta_n + h k1),
+ *                  theta_{n+1} = theta_n + (h/2)(k1 + k2)           (2nd-order explicit RK)
+ *   ORC_IMPMID(3): theta_{n+1} = theta_n + h F((theta_n + theta_{n+1})/2), solved by fixed-point
+ *                  iteration from the Euler predictor until max|update| <= fp_tol or fp_max_iter
+ *                  iterations (2nd-order implicit, geometric; reading R23)
+ * (method 0 = classical RK4 is orc_rk4).  r_trace as in orc_rk4.  Returns 0, -1 on a bad method. */
+int orc_step_method(const orc_graph *g, int method, int mode, double K, double h, int64_t nsteps,
+                    int32_t record_every, double *theta, const double *omega, double *r_trace,
+                    double fp_tol, int32_t fp_max_iter) {
+  if (method < 1 || method > 3) return -1;
+  const int64_t n = g->n;
+  double *k1 = (double *)malloc(sizeof(double) * (size_t)n);
+  double *k2 = (double *)malloc(sizeof(double) * (size_t)n);
+  double *ts = (double *)malloc(sizeof(double) * (size_t)n);
+  double *tp = (double *)malloc(sizeof(double) * (size_t)n);
+  for (int64_t step = 0; step <= nsteps; ++step) {
+    if (r_trace && record_every > 0 && step % record_every == 0)
+      orc_order_parameter(n, theta, r_trace + 2 * (step / record_every));
+    if (step == nsteps) break;
+    orc_rhs(g, mode, K, theta, omega, 0, NULL, k1);
+    if (method == 1) {
+      for (int64_t m = 0; m < n; ++m) theta[m] = theta[m] + h * k1[m];
+    } else if (method == 2) {
+      for (int64_t m = 0; m < n; ++m) ts[m] = theta[m] + h * k1[m];
+      orc_rhs(g, mode, K, ts, omega, 0, NULL, k2);
+      for (int64_t m = 0; m < n; ++m) theta[m] = theta[m] + (h / 2.0) * (k1[m] + k2[m]);
+    } else {
+      for (int64_t m = 0; m < n; ++m) tp[m] = theta[m] + h * k1[m]; /* Euler predictor */
+      for (int32_t it = 0; it < fp_max_iter; ++it) {
+        for (int64_t m = 0; m < n; ++m) ts[m] = (theta[m] + tp[m]) / 2.0;
+        orc_rhs(g, mode, K, ts, omega, 0, NULL, k2);
+        double diff = 0.0;
+        for (int64_t m = 0; m < n; ++m) {
+          const double nv = theta[m] + h * k2[m];
+          const double d = fabs(nv - tp[m]);
+          if (d > diff) diff = d;
+          tp[m] = nv;
+        }
+        if (diff <= fp_tol) break;
+      }
+      memcpy(theta, tp, sizeof(double) * (size_t)n);
+    }
+  }
+  free(k1);
+  free(k2);
+  free(ts);
+  free(tp);
+  return 0;
+}
+
 /* Potential of the model on a graph (eq. ExtendedPotentialConservation;
  * P:221-233 for the complete graph), evaluated from its definition
  *     V = -sum_m omega_m theta_m + (K/2) sum_{m,l} (A_ml / M_m) (1 - cos(theta_l - theta_m)),

@@ -132,3 +132,61 @@ def test_potential_decreases_along_rk4():
         v2 = oracle.potential(g, th, inst.omega, inst.K)
         assert v2 <= v + 1e-12
         v = v2
+
+
+# ---------------------------------------------------------------- NEXT-4 integrators
+def _adler(t, K, w, th1_0, th2_0):
+    phi0 = th2_0 - th1_0
+    phi = 2.0 * math.atan(math.tan(phi0 / 2.0) * math.exp(-K * t))
+    s = th1_0 + th2_0 + 2.0 * w * t
+    return np.array([(s - phi) / 2.0, (s + phi) / 2.0])
+
+
+@pytest.mark.parametrize("method,order", [("euler", 1), ("heun", 2), ("implicit_midpoint", 2)])
+def test_integrator_orders_against_adler(method, order):
+    """Observed order vs the closed-form two-oscillator solution (see O5)."""
+    K, w, T = 1.0, 0.3, 2.0
+    th0 = np.array([0.1, 2.1])
+    A = np.ones((2, 2), np.uint8) - np.eye(2, dtype=np.uint8)
+    inst = _inst(A, [0, 0], th0, [w, w], 0, kind="zeros")
+    g = oracle.Graph(inst)
+    ex = _adler(T, K, w, *th0)
+    errs = []
+    for h in (0.1, 0.05, 0.025, 0.0125):
+        th, _ = oracle.step_method(g, method, th0, inst.omega, K, h, int(round(T / h)), 0, mode="naive")
+        errs.append(np.max(np.abs(th - ex)))
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(3)]
+    assert all(order - 0.2 <= o <= order + 0.25 for o in orders), orders
+
+
+def test_euler_step_is_definition():
+    """P:303-306 on the SPEC example: M=2, theta=(0, pi/2), omega=0, K=1, h=0.1 ->
+    theta + 0.1*(0.5, -0.5)."""
+    A = np.array([[0, 1], [1, 0]], np.uint8)
+    th0 = np.array([0.0, math.pi / 2])
+    inst = _inst(A, [0, 0], th0, [0.0, 0.0], 0, kind="ones")
+    th, _ = oracle.step_method(oracle.Graph(inst), "euler", th0, inst.omega, 1.0, 0.1, 1, 0, mode="naive")
+    assert np.array_equal(th, th0 + 0.1 * np.array([0.5, -0.5]))
+
+
+@pytest.mark.parametrize("method", ["euler", "heun", "implicit_midpoint"])
+def test_integrators_preserve_linear_invariant(method):
+    """Symmetric A, uniform scaling: sum_m (theta_m(t) - omega_m t - theta_m(0)) = 0
+    is linear, so every Runge-Kutta method keeps it up to rounding (S:329 for Euler)."""
+    inst = kurgen.sbm([70, 50], [[0.9, 0.05], [0.05, 0.6]], 33)
+    g = oracle.Graph(inst)
+    th, _ = oracle.step_method(g, method, inst.theta0, inst.omega, 3.0, 0.01, 25, 0, mode="naive")
+    res = math.fsum(th) - math.fsum(inst.theta0) - 25 * 0.01 * math.fsum(inst.omega)
+    assert abs(res) <= 1e-11 * inst.n
+
+
+def test_implicit_midpoint_solves_its_equation():
+    """The returned step satisfies theta+ = theta + h F((theta + theta+)/2) to the fixed-point tolerance."""
+    inst = kurgen.sbm([60, 40], [[0.9, 0.1], [0.1, 0.7]], 5, K=3.0)
+    g = oracle.Graph(inst)
+    h = 0.05
+    tp, _ = oracle.step_method(g, "implicit_midpoint", inst.theta0, inst.omega, inst.K, h, 1, 0, mode="naive",
+                               fp_tol=1e-15, fp_max_iter=200)
+    mid = (inst.theta0 + tp) / 2
+    res = tp - inst.theta0 - h * oracle.rhs(g, mid, inst.omega, inst.K, mode="naive")
+    assert np.max(np.abs(res)) <= 1e-14
