@@ -172,6 +172,27 @@ kur_status kur_rhs(kur_graph *g, const double *theta, const double *omega, doubl
 kur_status kur_step(kur_graph *g, double *theta, const double *omega, double K, double h,
                     int64_t nsteps, int32_t record_every, double *r_trace, void *stream);
 
+/* The paper's other one-step integrators on the same RHS,
+ * fixed step h, theta updated in place, r_trace / record_every / kur_check as
+ * for kur_step (which equals method KUR_RK4):
+ *   KUR_RK4:    classical 4-stage Runge-Kutta;
+ *   KUR_EULER:  theta_{n+1} = theta_n + h G(theta_n);
+ *   KUR_HEUN:   k1 = G(theta_n), k2 = G(theta_n + h k1),
+ *               theta_{n+1} = theta_n + (h/2)(k1 + k2) (explicit 2nd order);
+ *   KUR_IMPLICIT_MIDPOINT: theta_{n+1} = theta_n + h G((theta_n + theta_{n+1})/2)
+ *               (implicit 2nd order, geometric), solved by fixed-point
+ *               iteration from the Euler predictor theta_n + h G(theta_n): iterate
+ *               t <- theta_n + h G((theta_n + t)/2) until max_m |t_new - t_old| <=
+ *               fp_tol or fp_max_iter iterations (reading R23); the
+ *               convergence test runs on the device (iterations after it are no-ops).
+ * fp_tol (>= 0, finite) and fp_max_iter (>= 1) are only read for the implicit
+ * midpoint rule.  Collective for world > 1.  KUR_ERR_INVALID_ARG for an
+ * unknown method or bad fixed-point parameters. */
+enum { KUR_RK4 = 0, KUR_EULER = 1, KUR_HEUN = 2, KUR_IMPLICIT_MIDPOINT = 3 };
+kur_status kur_step_method(kur_graph *g, int32_t method, double *theta, const double *omega, double K, double h,
+                           int64_t nsteps, int32_t record_every, double *r_trace, double fp_tol,
+                           int32_t fp_max_iter, void *stream);
+
 /* r_psi[2] = (r, psi) of the complex order parameter r e^{i psi} =
  * (1/N) sum_k e^{i theta_k} (psi = 0 when r = 0).  local (may be
  * NULL): [n_comm][2] = (r_b, psi_b) of the localised order parameters
@@ -189,6 +210,10 @@ kur_status kur_group_rhs(kur_graph *const *g, int32_t world, const double *const
 kur_status kur_group_step(kur_graph *const *g, int32_t world, double *const *theta, const double *const *omega,
                           double K, double h, int64_t nsteps, int32_t record_every, double *const *r_trace,
                           void *stream);
+kur_status kur_group_step_method(kur_graph *const *g, int32_t world, int32_t method, double *const *theta,
+                                 const double *const *omega, double K, double h, int64_t nsteps,
+                                 int32_t record_every, double *const *r_trace, double fp_tol, int32_t fp_max_iter,
+                                 void *stream);
 
 /* V_out[0] (device) = the potential of the model on the graph (eq.
  * ExtendedPotentialConservation; P:221-233 for the complete graph):

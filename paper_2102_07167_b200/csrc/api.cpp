@@ -59,6 +59,7 @@ struct kur_graph {
   int32_t *d_comm_tile0 = nullptr, *d_D_ptr = nullptr, *d_D_idx = nullptr, *d_csize = nullptr, *d_perm = nullptr;
   double2 *zA = nullptr, *zB = nullptr, *TA = nullptr, *TB = nullptr, *S = nullptr, *partial = nullptr;
   double* acc = nullptr;
+  double* pmax = nullptr;
   Ctrl* ctrl = nullptr;
   ncclComm_t comm = nullptr;
   int world = 1;
@@ -86,7 +87,7 @@ struct kur_graph {
     cudaSetDevice(device);
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
-                    xsend, xrecv, d_rowscale, d_potc};
+                    xsend, xrecv, d_rowscale, d_potc, pmax};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -204,6 +205,8 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   const int32_t ntiles_all = P.comm_tile0[(size_t)P.C];
   if ((e = cudaMalloc((void**)&g->partial, sizeof(double2) * (size_t)std::max<int32_t>(ntiles_all, 1))) != cudaSuccess)
     return bail(e, "partial");
+  if ((e = cudaMalloc((void**)&g->pmax, sizeof(double) * (size_t)std::max<int32_t>(ntiles_all, 1))) != cudaSuccess)
+    return bail(e, "pmax");
   if ((e = cudaMalloc((void**)&g->acc, sizeof(double) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess)
     return bail(e, "acc");
   if ((e = cudaMalloc((void**)&g->ctrl, sizeof(Ctrl))) != cudaSuccess) return bail(e, "ctrl");
@@ -217,7 +220,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
     xrows = std::max(xrows, P.shard_row0[(size_t)r + 1] - P.shard_row0[(size_t)r]);
     xtiles = std::max(xtiles, P.shard_tile0[(size_t)r + 1] - P.shard_tile0[(size_t)r]);
   }
-  const int32_t xstride = std::max(xrows + 2 * xtiles, 1);
+  const int32_t xstride = std::max(xrows + 3 * xtiles, 1);  // [phases | per tile (sum z, max |update|)]
   if ((e = upload(&g->d_shard_row0, P.shard_row0)) != cudaSuccess) return bail(e, "shard_row0");
   if ((e = upload(&g->d_shard_tile0, P.shard_tile0)) != cudaSuccess) return bail(e, "shard_tile0");
   if (world > 1) {
@@ -268,6 +271,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   dp.comm_size = g->d_csize;
   dp.perm = g->d_perm;
   dp.partial = g->partial;
+  dp.pmax = g->pmax;
   dp.S = g->S;
   dp.ctrl = g->ctrl;
 
@@ -370,8 +374,9 @@ kur_status exchange(const std::vector<kur_graph*>& gs, cudaStream_t s) {
 enum { PH_PROLOGUE = -1 };
 
 // mode: PH_PROLOGUE or a StageMode.  zin/zout/Tin/Tout select the ping-pong buffers.
+// commit (prologue only): theta = acc first (implicit midpoint step completion).
 kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vector<RankIO>& io, double K,
-                     double h, int record, bool z_from_A, cudaStream_t s) {
+                     double h, int record, bool z_from_A, cudaStream_t s, bool commit = false) {
   const int world = gs[0]->world;
   std::vector<StageArgs> args(gs.size());
   for (size_t r = 0; r < gs.size(); ++r) {
@@ -390,6 +395,9 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
     a.K = K;
     a.v_out = mode == MODE_POT ? io[r].v_out : nullptr;
     a.xsend = world > 1 ? g->xsend : nullptr;
+    a.commit = commit ? g->acc : nullptr;
+    a.fp_reset = mode == MODE_M0;
+    a.fp_check = mode == MODE_MI;
     if (mode == PH_PROLOGUE) {
       a.zout = g->zA;
       a.Tout = g->TA;
@@ -439,7 +447,11 @@ kur_status rhs_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO>
 }
 
 kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO>& io, double K, double h,
-                     int64_t nsteps, int32_t record_every, const std::vector<double*>& r_trace, cudaStream_t s) {
+                     int64_t nsteps, int32_t record_every, const std::vector<double*>& r_trace, cudaStream_t s,
+                     int method = KUR_RK4, double fp_tol = 0.0, int32_t fp_max_iter = 0) {
+  if (method < KUR_RK4 || method > KUR_IMPLICIT_MIDPOINT) return fail(KUR_ERR_INVALID_ARG, "unknown method");
+  if (method == KUR_IMPLICIT_MIDPOINT && (!(fp_tol >= 0.0) || !std::isfinite(fp_tol) || fp_max_iter < 1))
+    return fail(KUR_ERR_INVALID_ARG, "implicit midpoint needs fp_tol >= 0 (finite) and fp_max_iter >= 1");
   if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
   if (!(h > 0.0) || !std::isfinite(h)) return fail(KUR_ERR_INVALID_ARG, "h must be finite and > 0");
   if (nsteps < 0) return fail(KUR_ERR_INVALID_ARG, "nsteps must be >= 0");
@@ -450,9 +462,9 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
   for (size_t r = 0; r < gs.size(); ++r) {
     const bool rec = record_every > 0 && r_trace[r];
     const int64_t cap = rec ? nsteps / record_every + 1 : 0;
-    KUR_CUDA(launch_set_ctrl(gs[r]->ctrl, rec ? record_every : 0, (int)cap, rec ? r_trace[r] : nullptr, s));
+    KUR_CUDA(launch_set_ctrl(gs[r]->ctrl, rec ? record_every : 0, (int)cap, rec ? r_trace[r] : nullptr, fp_tol, s));
   }
-  if (gs.size() == 1 && gs[0]->small) {  // tiny graph: one single-CTA launch for the whole trajectory
+  if (gs.size() == 1 && gs[0]->small && method == KUR_RK4) {  // tiny graph: one single-CTA launch for the whole trajectory
     kur_graph* g = gs[0];
     StageArgs a{};
     a.theta = io[0].theta;
@@ -469,12 +481,34 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
   }
   kur_status st = run_phase(gs, PH_PROLOGUE, io, K, h, REC_START, true, s);
   if (st != KUR_OK) return st;
-  for (int64_t n = 0; n < nsteps; ++n)
-    for (int m = MODE_S1; m <= MODE_S4; ++m) {
-      st = run_phase(gs, m, io, K, h, m == MODE_S4 ? REC_STEP : REC_NONE, m == MODE_S1 || m == MODE_S3, s);
-      if (st != KUR_OK) return st;
+  // z / T ping-pong: the prologue fills A; every stage reads one buffer and writes the other
+  bool from_A = true;
+  auto stage = [&](int mode, int record) {
+    kur_status r = run_phase(gs, mode, io, K, h, record, from_A, s);
+    from_A = !from_A;
+    return r;
+  };
+  for (int64_t n = 0; n < nsteps && st == KUR_OK; ++n) {
+    switch (method) {
+      case KUR_RK4:
+        for (int m = MODE_S1; m <= MODE_S4 && st == KUR_OK; ++m) st = stage(m, m == MODE_S4 ? REC_STEP : REC_NONE);
+        break;
+      case KUR_EULER:
+        st = stage(MODE_E1, REC_STEP);
+        break;
+      case KUR_HEUN:
+        st = stage(MODE_H1, REC_NONE);
+        if (st == KUR_OK) st = stage(MODE_H2, REC_STEP);
+        break;
+      default:  // implicit midpoint: predictor, fp_max_iter iterations (no-ops once converged), commit
+        st = stage(MODE_M0, REC_NONE);
+        for (int32_t it = 0; it < fp_max_iter && st == KUR_OK; ++it) st = stage(MODE_MI, REC_NONE);
+        if (st == KUR_OK) st = run_phase(gs, PH_PROLOGUE, io, K, h, REC_STEP, true, s, /*commit=*/true);
+        from_A = true;
+        break;
     }
-  return KUR_OK;
+  }
+  return st;
 }
 
 }  // namespace
@@ -498,6 +532,17 @@ kur_status kur_step(kur_graph* g, double* theta, const double* omega, double K, 
   if (st != KUR_OK) return st;
   return step_impl(gs, {RankIO{theta, omega, nullptr, nullptr, nullptr}}, K, h, nsteps, record_every, {r_trace},
                    (cudaStream_t)stream);
+}
+
+kur_status kur_step_method(kur_graph* g, int32_t method, double* theta, const double* omega, double K, double h,
+                           int64_t nsteps, int32_t record_every, double* r_trace, double fp_tol, int32_t fp_max_iter,
+                           void* stream) {
+  if (!g) return fail(KUR_ERR_INVALID_ARG, "graph is NULL");
+  std::vector<kur_graph*> gs{g};
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
+  return step_impl(gs, {RankIO{theta, omega, nullptr, nullptr, nullptr}}, K, h, nsteps, record_every, {r_trace},
+                   (cudaStream_t)stream, method, fp_tol, fp_max_iter);
 }
 
 kur_status kur_order_parameter(kur_graph* g, const double* theta, double* r_psi, double* local, void* stream) {
@@ -550,6 +595,22 @@ kur_status kur_group_step(kur_graph* const* g, int32_t world, double* const* the
     rt.push_back(r_trace ? r_trace[r] : nullptr);
   }
   return step_impl(gs, io, K, h, nsteps, record_every, rt, (cudaStream_t)stream);
+}
+
+kur_status kur_group_step_method(kur_graph* const* g, int32_t world, int32_t method, double* const* theta,
+                                 const double* const* omega, double K, double h, int64_t nsteps, int32_t record_every,
+                                 double* const* r_trace, double fp_tol, int32_t fp_max_iter, void* stream) {
+  if (!g || !theta || !omega || world < 1) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  std::vector<kur_graph*> gs(g, g + world);
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
+  std::vector<RankIO> io;
+  std::vector<double*> rt;
+  for (int r = 0; r < world; ++r) {
+    io.push_back(RankIO{theta[r], omega[r], nullptr, nullptr, nullptr});
+    rt.push_back(r_trace ? r_trace[r] : nullptr);
+  }
+  return step_impl(gs, io, K, h, nsteps, record_every, rt, (cudaStream_t)stream, method, fp_tol, fp_max_iter);
 }
 
 kur_status kur_timing(kur_graph* g, int32_t enable) {

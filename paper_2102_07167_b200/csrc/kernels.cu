@@ -104,6 +104,21 @@ __device__ __forceinline__ void block_sum2(double& x, double& y, double2* red) {
   }
 }
 
+// Fixed-shape block maximum over NTHREADS threads; result valid in warp 0.
+__device__ __forceinline__ double block_max(double d, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+  if (lane == 0) red[warp] = d;
+  __syncthreads();
+  if (warp == 0) {
+    d = lane < NWARPS ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = NWARPS / 2; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+  }
+  return d;
+}
+
 // Sum of the 8 window-local z entries named by one 16-byte unit (P:557-570:
 // complement or non-zero entries; the part's sign is applied by the caller).
 __device__ __forceinline__ void hot8(const uint4 v, const double2* zs, double& x0, double& y0,
@@ -207,6 +222,16 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
     if (tid == 0) a.v_out[0] = x;
     return;
   }
+  if (a.fp_reset || a.fp_check) {  // implicit midpoint: convergence of the fixed-point iteration
+    double d = 0.0;
+    if (a.fp_check) {
+      const int nt = dp.comm_tile0[dp.C];
+      for (int t = tid; t < nt; t += NTHREADS) d = fmax(d, __ldcg(dp.pmax + t));
+    }
+    d = block_max(d, reinterpret_cast<double*>(fred));
+    if (tid == 0) dp.ctrl->fp_done = a.fp_check ? (d <= dp.ctrl->fp_tol) : 0;
+    __syncthreads();
+  }
   for (int c = warp; c < dp.C; c += NWARPS) {  // S_b = sum of its tiles' partials
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
     if (t1 - t0 > BIG) continue;
@@ -287,15 +312,22 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
 }
 
 // Writes the tile partial, then lets the last CTA of the grid finish.
+// dmax: this thread's max |fixed-point update| (implicit midpoint iterations, else 0).
 __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const StageArgs& a, int lt,
-                                                        double x, double y, double2* red) {
+                                                        double x, double y, double2* red, double dmax = 0.0) {
   __shared__ bool s_last;
+  if (a.fp_check) {
+    dmax = block_max(dmax, reinterpret_cast<double*>(red));
+    __syncthreads();
+  }
   block_sum2(x, y, red);
   if (threadIdx.x == 0) {
     dp.partial[dp.tile_base + lt] = make_double2(x, y);
+    if (a.fp_check) dp.pmax[dp.tile_base + lt] = dmax;
     if (a.xsend) {
-      a.xsend[dp.xrows + 2 * lt] = x;
-      a.xsend[dp.xrows + 2 * lt + 1] = y;
+      a.xsend[dp.xrows + 3 * lt] = x;
+      a.xsend[dp.xrows + 3 * lt + 1] = y;
+      a.xsend[dp.xrows + 3 * lt + 2] = dmax;
     }
     s_last = false;
     if (dp.world == 1) {  // world > 1: the reduction runs after the exchange
@@ -319,7 +351,14 @@ __device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs
   for (int lr = threadIdx.x; lr < T.nrows; lr += NTHREADS) {
     const int row = T.row0 + lr;
     double s, c;
-    const double th = a.theta[row - dp.row_begin];
+    double th;
+    if (a.commit) {  // implicit midpoint: theta_{n+1} = the converged fixed point
+      th = a.commit[row - dp.row_begin];
+      a.theta[row - dp.row_begin] = th;
+      if (!isfinite(th)) dp.ctrl->nonfinite = 1;
+    } else {
+      th = a.theta[row - dp.row_begin];
+    }
     sincos(th, &s, &c);  // z = e^{i theta}
     a.zout[row] = make_double2(c, s);
     if (a.xsend) a.xsend[row - dp.row_begin] = th;
@@ -334,7 +373,8 @@ __device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs
 // the next stage's z in (px, py) and whether a phase became non-finite.
 template <int MODE, bool SMALL>
 __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a, const TileDesc& T, double2* zs,
-                                           double2* Ws, uint64_t* bar, uint32_t& phase, double& px, double& py) {
+                                           double2* Ws, uint64_t* bar, uint32_t& phase, double& px, double& py,
+                                           double& dmax) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool parts = dp.has_parts;
   if (parts) {
@@ -387,6 +427,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   const double2 Tc = __ldcg(a.Tin + T.comm);
   px = 0.0;
   py = 0.0;
+  dmax = 0.0;
   bool bad = false;
   for (int lr = tid; lr < T.nrows; lr += NTHREADS) {
     const int row = T.row0 + lr;
@@ -416,10 +457,27 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       } else if (MODE == MODE_S3) {
         a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
         ts = __dadd_rn(thn, __dmul_rn(a.h, k));
-      } else {  // MODE_S4: theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
+      } else if (MODE == MODE_S4) {  // theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
         ts = __dadd_rn(thn, __dmul_rn(a.h / 6.0, __dadd_rn(a.acc[li], k)));
         a.theta[li] = ts;
         bad |= !isfinite(ts);
+      } else if (MODE == MODE_E1) {  // explicit Euler: theta_{n+1} = theta_n + h k
+        ts = __dadd_rn(thn, __dmul_rn(a.h, k));
+        a.theta[li] = ts;
+        bad |= !isfinite(ts);
+      } else if (MODE == MODE_H1) {  // Heun: k1, stage state theta_n + h k1
+        a.acc[li] = k;
+        ts = __dadd_rn(thn, __dmul_rn(a.h, k));
+      } else if (MODE == MODE_H2) {  // theta_{n+1} = theta_n + (h/2)(k1 + k2)
+        ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, __dadd_rn(a.acc[li], k)));
+        a.theta[li] = ts;
+        bad |= !isfinite(ts);
+      } else {  // MODE_M0 / MODE_MI: implicit midpoint fixed point on tp (kept in acc)
+        const double nv = __dadd_rn(thn, __dmul_rn(a.h, k));
+        if (MODE == MODE_MI) dmax = fmax(dmax, fabs(__dadd_rn(nv, -a.acc[li])));
+        a.acc[li] = nv;
+        ts = __dadd_rn(thn, nv) / 2.0;
+        if (MODE == MODE_MI && !(fabs(nv) <= 1.79e308)) dmax = __longlong_as_double(0x7ff0000000000000ll);
       }
       double s, c;
       sincos(ts, &s, &c);
@@ -450,6 +508,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __shared__ __align__(8) uint64_t bar;
   __shared__ int s_nonfinite;
   const int tid = threadIdx.x;
+  // implicit midpoint: iterations after convergence are no-ops (uniform: every CTA reads the same flag)
+  if (MODE == MODE_MI && *(volatile const int*)&dp.ctrl->fp_done) return;
   const int lt = dp.order[blockIdx.x];
   const TileDesc T = dp.tiles[lt];
   if (dp.has_parts && tid < 8) zs[WZ + tid] = make_double2(0.0, 0.0);
@@ -459,13 +519,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   }
   __syncthreads();
   uint32_t phase = 0;
-  double px, py;
-  const bool bad = stage_rows<MODE, false>(dp, a, T, zs, Ws, &bar, phase, px, py);
+  double px, py, dmax;
+  const bool bad = stage_rows<MODE, false>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax);
   if (MODE == MODE_RHS) return;
-  if (MODE == MODE_S4 && bad) s_nonfinite = 1;
+  constexpr bool FINAL = MODE == MODE_S4 || MODE == MODE_E1 || MODE == MODE_H2;
+  if (FINAL && bad) s_nonfinite = 1;
   __syncthreads();
-  if (MODE == MODE_S4 && tid == 0 && s_nonfinite) dp.ctrl->nonfinite = 1;
-  tile_partial_and_finish(dp, a, lt, px, py, red);
+  if (FINAL && tid == 0 && s_nonfinite) dp.ctrl->nonfinite = 1;
+  tile_partial_and_finish(dp, a, lt, px, py, red, dmax);
 }
 
 // ---- single-CTA trajectory kernel for tiny graphs (world == 1): the whole
@@ -483,8 +544,8 @@ __device__ __forceinline__ void small_stage(const DevPlan& dp, StageArgs a, cons
   a.record = record;
   for (int lt = 0; lt < dp.ntiles; ++lt) {
     const TileDesc T = dp.tiles[lt];
-    double px, py;
-    const bool bad = stage_rows<MODE, true>(dp, a, T, zs, Ws, bar, phase, px, py);
+    double px, py, dmax;
+    const bool bad = stage_rows<MODE, true>(dp, a, T, zs, Ws, bar, phase, px, py, dmax);
     if (MODE == MODE_S4 && bad) *s_bad = 1;
     block_sum2(px, py, red);
     if (threadIdx.x == 0) dp.partial[lt] = make_double2(px, py);
@@ -554,8 +615,9 @@ __global__ void k_unpack(const DevPlan dp, const double* __restrict__ xrecv, dou
   if (i < nt) {
     int r = 0;
     while (dp.shard_tile0[r + 1] <= i) ++r;
-    const double* src = xrecv + (size_t)r * dp.xstride + dp.xrows + 2 * (i - dp.shard_tile0[r]);
+    const double* src = xrecv + (size_t)r * dp.xstride + dp.xrows + 3 * (i - dp.shard_tile0[r]);
     dp.partial[i] = make_double2(src[0], src[1]);
+    dp.pmax[i] = src[2];
   }
 }
 
@@ -563,7 +625,8 @@ __global__ void __launch_bounds__(NTHREADS) k_finish(const DevPlan dp, const Sta
   finish_reduce(dp, a);
 }
 
-__global__ void k_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace) {
+__global__ void k_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, double fp_tol) {
+  c->fp_tol = fp_tol;
   c->record_every = record_every;
   c->nrec_cap = nrec_cap;
   c->r_trace = r_trace;
@@ -609,6 +672,11 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
     case MODE_S3: return launch_stage_m<MODE_S3>(dp, a, s);
     case MODE_S4: return launch_stage_m<MODE_S4>(dp, a, s);
     case MODE_POT: return launch_stage_m<MODE_POT>(dp, a, s);
+    case MODE_E1: return launch_stage_m<MODE_E1>(dp, a, s);
+    case MODE_H1: return launch_stage_m<MODE_H1>(dp, a, s);
+    case MODE_H2: return launch_stage_m<MODE_H2>(dp, a, s);
+    case MODE_M0: return launch_stage_m<MODE_M0>(dp, a, s);
+    case MODE_MI: return launch_stage_m<MODE_MI>(dp, a, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -638,8 +706,9 @@ cudaError_t launch_finish(const DevPlan& dp, const StageArgs& a, cudaStream_t s)
   return cudaGetLastError();
 }
 
-cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, cudaStream_t s) {
-  k_set_ctrl<<<1, 1, 0, s>>>(c, record_every, nrec_cap, r_trace);
+cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, double fp_tol,
+                            cudaStream_t s) {
+  k_set_ctrl<<<1, 1, 0, s>>>(c, record_every, nrec_cap, r_trace, fp_tol);
   return cudaGetLastError();
 }
 

@@ -13,6 +13,9 @@ struct Ctrl {             // device-resident control block
   int record_every;       // > 0: record (r, psi) of theta_n when n % record_every == 0
   int nrec_cap;           // capacity of r_trace in pairs
   long long step;         // n of the current theta_n inside kur_step
+  int fp_done;            // implicit midpoint: the fixed-point iteration of this step converged
+  int fp_pad;
+  double fp_tol;          // implicit midpoint: stop when max_m |theta^{(i+1)}_m - theta^{(i)}_m| <= fp_tol
   double* r_trace;        // [nrec_cap][2]
   double rpsi[2];         // last computed (r, psi)
 };
@@ -44,11 +47,25 @@ struct DevPlan {
   const double* rowscale;     // [local rows] 1/M_m (degree scaling) or NULL (uniform: K/N)
   const double* potc;         // [local rows] potential constants (kur_potential)
   double2* partial;           // [ntiles_all] per-tile sums of z (global tile ids)
+  double* pmax;               // [ntiles_all] per-tile max |fixed-point update| (implicit midpoint)
   double2* S;                 // [C] block sums S_b of the last reduction
   Ctrl* ctrl;
 };
 
-enum StageMode { MODE_RHS = 0, MODE_S1 = 1, MODE_S2 = 2, MODE_S3 = 3, MODE_S4 = 4, MODE_POT = 5 };
+// Stage epilogues (k = RHS of the stage state, theta_n = a.theta, acc = a.acc):
+//   RK4:  S1 acc = k, ts = theta_n + h/2 k;  S2 acc += 2k, ts = theta_n + h/2 k;
+//                     S3 acc += 2k, ts = theta_n + h k;  S4 theta = theta_n + h/6 (acc + k)
+//   Euler: E1 theta = theta_n + h k
+//   Heun:      H1 acc = k, ts = theta_n + h k;    H2 theta = theta_n + h/2 (acc + k)
+//   implicit midpoint (reading R23), fixed point on tp = theta_{n+1}:
+//                     M0 tp = theta_n + h k (Euler predictor), ts = (theta_n + tp)/2
+//                     MI nv = theta_n + h k, d = |nv - tp|, tp = nv, ts = (theta_n + tp)/2;
+//                        skipped entirely once ctrl->fp_done; the finish sets fp_done = (max d <= tol)
+//                     then the prologue with a.commit = tp sets theta = tp (step done)
+enum StageMode {
+  MODE_RHS = 0, MODE_S1 = 1, MODE_S2 = 2, MODE_S3 = 3, MODE_S4 = 4, MODE_POT = 5,
+  MODE_E1 = 6, MODE_H1 = 7, MODE_H2 = 8, MODE_M0 = 9, MODE_MI = 10
+};
 enum RecordMode { REC_NONE = 0, REC_START = 1, REC_STEP = 2 };
 
 struct StageArgs {
@@ -67,7 +84,10 @@ struct StageArgs {
   double* op_rpsi;        // kur_order_parameter outputs (device) or NULL
   double* op_local;
   int record;             // RecordMode
-  double* xsend;          // world > 1: packed [stage theta of local rows | local tile partials]
+  double* xsend;          // world > 1: packed [stage theta of local rows | tile partials | tile max]
+  const double* commit;   // prologue only: theta = commit (implicit midpoint step completion) or NULL
+  int fp_reset;           // the finish clears ctrl->fp_done (implicit midpoint predictor M0)
+  int fp_check;           // MODE_MI: tiles publish max |update|, the finish sets ctrl->fp_done
 };
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
@@ -80,7 +100,8 @@ cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, dou
                          long long nsteps, cudaStream_t s);
 cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, cudaStream_t s);
 cudaError_t launch_finish(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
-cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, cudaStream_t s);
+cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, double fp_tol,
+                            cudaStream_t s);
 cudaError_t launch_permute(const int32_t* perm, int64_t n, const double* in, double* out, int dir,
                            cudaStream_t s);
 size_t stage_smem_bytes(int rows_per_tile);

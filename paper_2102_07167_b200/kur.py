@@ -68,18 +68,22 @@ _lib.kur_timing_read.argtypes = [_p, _p]
 _lib.kur_nccl_unique_id.argtypes = [_p]
 _lib.kur_group_rhs.argtypes = [_p, _i32, _p, _p, _d, _p, _p]
 _lib.kur_group_step.argtypes = [_p, _i32, _p, _p, _d, _d, _i64, _i32, _p, _p]
+_lib.kur_step_method.argtypes = [_p, _i32, _p, _p, _d, _d, _i64, _i32, _p, _d, _i32, _p]
+_lib.kur_group_step_method.argtypes = [_p, _i32, _i32, _p, _p, _d, _d, _i64, _i32, _p, _d, _i32, _p]
 _lib.kur_status_string.restype = ctypes.c_char_p
 _lib.kur_status_string.argtypes = [ctypes.c_int]
 _lib.kur_last_error.restype = ctypes.c_char_p
 for _f in ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
            "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id", "kur_timing",
-           "kur_timing_read", "kur_group_rhs", "kur_group_step", "kur_potential"):
+           "kur_timing_read", "kur_group_rhs", "kur_group_step", "kur_potential", "kur_step_method",
+           "kur_group_step_method"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
             "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id",
             "kur_status_string", "kur_last_error", "kur_timing", "kur_timing_read", "kur_group_rhs",
-            "kur_group_step", "kur_potential")
+            "kur_group_step", "kur_potential", "kur_step_method", "kur_group_step_method")
+METHODS = {"rk4": 0, "euler": 1, "heun": 2, "implicit_midpoint": 3}
 
 
 class KurError(RuntimeError):
@@ -243,6 +247,21 @@ def step(g: Graph, theta, omega, K, h, nsteps, record_every=0, r_trace=None, str
     return r_trace
 
 
+def step_method(g: Graph, method, theta, omega, K, h, nsteps, record_every=0, r_trace=None, fp_tol=1e-13,
+                fp_max_iter=50, stream=None, check=False):
+    """kur_step_method: nsteps of 'rk4' | 'euler' | 'heun' | 'implicit_midpoint' in place on theta."""
+    if record_every and r_trace is None:
+        r_trace = torch.zeros((int(nsteps) // int(record_every) + 1, 2), dtype=torch.float64,
+                              device=f"cuda:{g.device}")
+    rt = ctypes.c_void_p(r_trace.data_ptr()) if r_trace is not None else None
+    _check(_lib.kur_step_method(g._h, METHODS[method], _dev_vec(theta, g.n_local, g.device, "theta"),
+                                _dev_vec(omega, g.n_local, g.device, "omega"), float(K), float(h), int(nsteps),
+                                int(record_every), rt, float(fp_tol), int(fp_max_iter), _stream(stream)))
+    if check:
+        _check(_lib.kur_check(g._h, _stream(stream)))
+    return r_trace
+
+
 def timing(g: Graph, enable: bool):
     """Enable/disable per-launch CUDA-event timing inside kur_step (clears the record)."""
     _check(_lib.kur_timing(g._h, 1 if enable else 0))
@@ -287,6 +306,21 @@ def group_step(graphs, thetas, omegas, K, h, nsteps, record_every=0, stream=None
     rt = _ptr_array([r.data_ptr() if r is not None else None for r in rts]) if record_every else None
     _check(_lib.kur_group_step(hs, len(graphs), th, om, float(K), float(h), int(nsteps), int(record_every), rt,
                                _stream(stream)))
+    return rts
+
+
+def group_step_method(graphs, method, thetas, omegas, K, h, nsteps, record_every=0, fp_tol=1e-13, fp_max_iter=50,
+                      stream=None):
+    """kur_group_step_method on per-rank local-row device tensors; returns per-rank r_traces."""
+    dev = f"cuda:{graphs[0].device}"
+    rts = [torch.zeros((int(nsteps) // int(record_every) + 1, 2), dtype=torch.float64, device=dev)
+           if record_every else None for _ in graphs]
+    hs = _ptr_array([g._h for g in graphs])
+    th = _ptr_array([_dev_vec(t, g.n_local, g.device, "theta").value for g, t in zip(graphs, thetas)])
+    om = _ptr_array([_dev_vec(o, g.n_local, g.device, "omega").value for g, o in zip(graphs, omegas)])
+    rt = _ptr_array([r.data_ptr() if r is not None else None for r in rts]) if record_every else None
+    _check(_lib.kur_group_step_method(hs, len(graphs), METHODS[method], th, om, float(K), float(h), int(nsteps),
+                                      int(record_every), rt, float(fp_tol), int(fp_max_iter), _stream(stream)))
     return rts
 
 
