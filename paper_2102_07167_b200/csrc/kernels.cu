@@ -160,50 +160,57 @@ __device__ __forceinline__ void rem4(const uint4 v, const double2* __restrict__ 
 }
 
 // Hot part of one chunk: ng groups of 32 units starting at q (lane-offset applied).
-// Software-pipelined: the next 4 groups are in flight while 4 are gathered.
+// Rotating software pipeline: the unit of group g+4 is requested before group g
+// is gathered, so four 16-byte index loads per lane are always in flight and
+// there is no serial tail (loads past ng are predicated off).
 __device__ __forceinline__ void run_hot(const uint4* __restrict__ q, uint32_t ng, const double2* zs,
                                         uint64_t pol, double& sx, double& sy) {
   double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
-  uint32_t g = 0;
-  if (ng >= 4) {
-    uint4 a0 = ldg_stream(q + 0 * 32, pol), a1 = ldg_stream(q + 1 * 32, pol);
-    uint4 a2 = ldg_stream(q + 2 * 32, pol), a3 = ldg_stream(q + 3 * 32, pol);
-    for (g = 4; g + 4 <= ng; g += 4) {
-      const uint4 b0 = ldg_stream(q + (size_t)(g + 0) * 32, pol);
-      const uint4 b1 = ldg_stream(q + (size_t)(g + 1) * 32, pol);
-      const uint4 b2 = ldg_stream(q + (size_t)(g + 2) * 32, pol);
-      const uint4 b3 = ldg_stream(q + (size_t)(g + 3) * 32, pol);
-      hot8(a0, zs, x0, y0, x1, y1);
-      hot8(a1, zs, x0, y0, x1, y1);
-      hot8(a2, zs, x0, y0, x1, y1);
-      hot8(a3, zs, x0, y0, x1, y1);
-      a0 = b0;
-      a1 = b1;
-      a2 = b2;
-      a3 = b3;
-    }
-    hot8(a0, zs, x0, y0, x1, y1);
-    hot8(a1, zs, x0, y0, x1, y1);
-    hot8(a2, zs, x0, y0, x1, y1);
-    hot8(a3, zs, x0, y0, x1, y1);
+  const uint4 z4 = make_uint4(0, 0, 0, 0);
+  uint4 b0 = ng > 0 ? ldg_stream(q, pol) : z4;
+  uint4 b1 = ng > 1 ? ldg_stream(q + 32, pol) : z4;
+  uint4 b2 = ng > 2 ? ldg_stream(q + 64, pol) : z4;
+  uint4 b3 = ng > 3 ? ldg_stream(q + 96, pol) : z4;
+  for (uint32_t g = 0; g < ng; g += 4) {
+    const uint4* qn = q + (size_t)(g + 4) * 32;
+    uint4 c = b0;
+    if (g + 4 < ng) b0 = ldg_stream(qn, pol);
+    hot8(c, zs, x0, y0, x1, y1);
+    if (g + 1 >= ng) break;
+    c = b1;
+    if (g + 5 < ng) b1 = ldg_stream(qn + 32, pol);
+    hot8(c, zs, x0, y0, x1, y1);
+    if (g + 2 >= ng) break;
+    c = b2;
+    if (g + 6 < ng) b2 = ldg_stream(qn + 64, pol);
+    hot8(c, zs, x0, y0, x1, y1);
+    if (g + 3 >= ng) break;
+    c = b3;
+    if (g + 7 < ng) b3 = ldg_stream(qn + 96, pol);
+    hot8(c, zs, x0, y0, x1, y1);
   }
-  for (; g < ng; ++g) hot8(ldg_stream(q + (size_t)g * 32, pol), zs, x0, y0, x1, y1);
   sx = x0 + x1;
   sy = y0 + y1;
 }
 
+// Remote part of one chunk: the index units run two groups ahead of the z gathers.
 template <bool COHERENT>
 __device__ __forceinline__ void run_remote(const uint4* __restrict__ q, uint32_t ng,
                                            const double2* __restrict__ z, uint64_t pol, double& sx, double& sy) {
   double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
-  uint32_t g = 0;
-  for (; g + 2 <= ng; g += 2) {
-    const uint4 v0 = ldg_stream(q + (size_t)(g + 0) * 32, pol);
-    const uint4 v1 = ldg_stream(q + (size_t)(g + 1) * 32, pol);
-    rem4<COHERENT>(v0, z, x0, y0, x1, y1);
-    rem4<COHERENT>(v1, z, x0, y0, x1, y1);
+  const uint4 z4 = make_uint4(0, 0, 0, 0);
+  uint4 b0 = ng > 0 ? ldg_stream(q, pol) : z4;
+  uint4 b1 = ng > 1 ? ldg_stream(q + 32, pol) : z4;
+  for (uint32_t g = 0; g < ng; g += 2) {
+    const uint4* qn = q + (size_t)(g + 2) * 32;
+    uint4 c = b0;
+    if (g + 2 < ng) b0 = ldg_stream(qn, pol);
+    rem4<COHERENT>(c, z, x0, y0, x1, y1);
+    if (g + 1 >= ng) break;
+    c = b1;
+    if (g + 3 < ng) b1 = ldg_stream(qn + 32, pol);
+    rem4<COHERENT>(c, z, x0, y0, x1, y1);
   }
-  for (; g < ng; ++g) rem4<COHERENT>(ldg_stream(q + (size_t)g * 32, pol), z, x0, y0, x1, y1);
   sx = x0 + x1;
   sy = y0 + y1;
 }
@@ -393,11 +400,14 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       phase ^= 1u;
       loaded = P.window;
     }
-    // chunks of the part, snake order over the 16 warps (chunks are sorted longest first)
-    for (uint32_t r = 0;; ++r) {
-      const uint32_t c = r * NWARPS + ((r & 1) ? (NWARPS - 1 - warp) : warp);
-      if (c >= P.nchunks) break;
-      const uint2 cd = dp.chunks[P.chunk0 + c];
+    // chunks of the part, snake order over the 16 warps (chunks are sorted longest first);
+    // the next chunk's descriptor is requested before the current chunk is gathered
+    uint32_t c = warp;
+    uint2 cdn = c < P.nchunks ? __ldg(dp.chunks + P.chunk0 + c) : make_uint2(0, 0);
+    for (uint32_t r = 0; c < P.nchunks; ++r) {
+      const uint2 cd = cdn;
+      const uint32_t cnext = (r + 1) * NWARPS + (((r + 1) & 1) ? (NWARPS - 1 - warp) : warp);
+      if (cnext < P.nchunks) cdn = __ldg(dp.chunks + P.chunk0 + cnext);
       const uint4* q = dp.pool + cd.x;
       const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
       double sx, sy;
@@ -419,6 +429,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
         }
         Ws[row] = w;
       }
+      c = cnext;
     }
     __syncthreads();
   }
