@@ -32,7 +32,13 @@ $(PKG)/libkur.so: $(KUR_SRCS) $(KUR_HDRS)
 	  -L$(NCCL_LIB) -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_LIB) -lgomp 2> $(PKG)/ptxas.log || \
 	  (cat $(PKG)/ptxas.log; exit 1)
 
+# tooling: the same library with per-tile clock64 phase stamps (tools/tile_profile.py); not the product build
+prof: $(KUR_SRCS) $(KUR_HDRS)
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -DKUR_PROFILE -Iinclude -I$(NCCL_INC) \
+	  -Xcompiler -fPIC,-fopenmp,-O3 -shared -o $(PKG)/libkur_prof.so $(KUR_SRCS) \
+	  -L$(NCCL_LIB) -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_LIB) -lgomp
+
 clean:
 	rm -f kurgen/libkurgen.so oracle/liboracle.so $(PKG)/libkur.so $(PKG)/ptxas.log
 
-.PHONY: all clean
+.PHONY: all clean prof

@@ -27,6 +27,19 @@
 #include "kernels.h"
 
 namespace kur {
+#ifdef KUR_PROFILE
+// Tooling build only (make prof): per-tile clock64 stamps of k_stage phases.
+__device__ unsigned long long* g_prof = nullptr;
+constexpr int PROF_STRIDE = 192;  // [0] start, [1+3p..] window wait begin/end + part end, [25] finalize, [26] end,
+                                  // [32 + 16p + w] warp w done with part p (p < 8)
+#define PROF_T(i) \
+  do { if (g_prof && threadIdx.x == 0) g_prof[(size_t)blockIdx.x * PROF_STRIDE + (i)] = clock64(); } while (0)
+#define PROF_W(p, w) \
+  do { if (g_prof && (threadIdx.x & 31) == 0 && (p) < 8) g_prof[(size_t)blockIdx.x * PROF_STRIDE + 32 + 16 * (p) + (w)] = clock64(); } while (0)
+#else
+#define PROF_T(i) do {} while (0)
+#define PROF_W(p, w) do {} while (0)
+#endif
 namespace {
 
 // Index stream: read once per RHS, never reused within it -> do not allocate
@@ -391,15 +404,25 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   // ---- parts: hot ones gather from the staged window, remote ones from global memory
   const uint64_t pol = evict_first_policy();
   int loaded = -1;
+  if (!SMALL) PROF_T(0);
+#ifdef KUR_PROFILE
+  if (!SMALL && g_prof && tid == 0) {
+    g_prof[(size_t)blockIdx.x * PROF_STRIDE + 27] = (unsigned long long)T.nhot;
+    g_prof[(size_t)blockIdx.x * PROF_STRIDE + 28] = (unsigned long long)T.nparts;
+  }
+#endif
   for (int p = T.part0; p < T.part0 + T.nparts; ++p) {
     const PartDesc P = dp.parts[p];
     const bool hot = P.window >= 0;
+    const int pi = p - T.part0;
+    if (!SMALL && pi < 8) PROF_T(1 + 3 * pi);
     if (hot && P.window != loaded) {  // all reads of the previous window ended at the last barrier
       if (tid == 0) tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), bar);
       mbar_wait(bar, phase);
       phase ^= 1u;
       loaded = P.window;
     }
+    if (!SMALL && pi < 8) PROF_T(2 + 3 * pi);
     // chunks of the part, snake order over the 16 warps (chunks are sorted longest first);
     // the next chunk's descriptor is requested before the current chunk is gathered
     uint32_t c = warp;
@@ -431,8 +454,11 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       }
       c = cnext;
     }
+    if (!SMALL) PROF_W(pi, warp);
     __syncthreads();
+    if (!SMALL && pi < 8) PROF_T(3 + 3 * pi);
   }
+  if (!SMALL) PROF_T(25);
 
   // ---- finalize: k_j = omega_j + (K/N) Im(conj z_j W_j), fused RK4 stage
   const double2 Tc = __ldcg(a.Tin + T.comm);
@@ -537,6 +563,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   if (FINAL && bad) s_nonfinite = 1;
   __syncthreads();
   if (FINAL && tid == 0 && s_nonfinite) dp.ctrl->nonfinite = 1;
+  PROF_T(26);
   tile_partial_and_finish(dp, a, lt, px, py, red, dmax);
 }
 
@@ -665,6 +692,14 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
 }
 
 }  // namespace
+
+#ifdef KUR_PROFILE
+}  // namespace kur
+extern "C" int kur_prof_attach(unsigned long long* p) {
+  return (int)cudaMemcpyToSymbol(kur::g_prof, &p, sizeof(p));
+}
+namespace kur {
+#endif
 
 size_t stage_smem_bytes(int rows_per_tile) { return sizeof(double2) * (size_t)(WZ + 8 + rows_per_tile); }
 

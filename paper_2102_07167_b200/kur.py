@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkur.so")
+LIB_PATH = os.environ.get("KUR_LIB") or os.path.join(_HERE, "libkur.so")  # KUR_LIB: tooling builds only
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build() "
                       "(there is no CPU fallback)")

@@ -1,0 +1,94 @@
+// mb_lds.cu — microbenchmark (tooling, not product): the achievable rate of
+// conflict-free 16-byte shared-memory gathers + fp64 accumulation on one SM,
+// i.e. the ceiling of k_stage's hot loop.  Variants:
+//   0: slot ids computed in registers (pure LDS.128 + DADD)
+//   1: slot ids streamed from global memory as 16-bit pairs (k_stage's layout), L2-resident
+//   2: as 1 with 4 independent accumulator pairs per lane
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb_lds tools/mb_lds.cu
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+constexpr int NT = 512, WZ = 4096;
+
+template <int VAR>
+__global__ void __launch_bounds__(NT, 2) k_gather(const uint4* __restrict__ units, int ngroups, int reps, double* out) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  double2* zs = reinterpret_cast<double2*>(sm);
+  for (int i = threadIdx.x; i < WZ; i += NT) zs[i] = make_double2(i * 1e-3, 1.0 - i * 1e-3);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double x0 = 0, y0 = 0, x1 = 0, y1 = 0, x2 = 0, y2 = 0, x3 = 0, y3 = 0;
+  uint32_t h = 2654435761u * (blockIdx.x * NT + threadIdx.x + 1);
+  for (int r = 0; r < reps; ++r) {
+    for (int g = wid; g < ngroups; g += NT / 32) {
+      uint32_t w[4];
+      if (VAR == 0) {
+        h = h * 1664525u + 1013904223u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t base = (h >> (q * 3)) & (WZ - 8);
+          const uint32_t s0 = (base & ~7u) | ((lane + 2 * q) & 7), s1 = ((base ^ 0x5a8) & ~7u) | ((lane + 2 * q + 1) & 7);
+          w[q] = s0 | (s1 << 16);
+        }
+      } else {
+        const uint4 v = __ldg(units + (size_t)g * 32 + lane);
+        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 a = zs[w[q] & 0xFFFF], b = zs[w[q] >> 16];
+        if (VAR == 2 && (q & 1)) { x2 += a.x; y2 += a.y; x3 += b.x; y3 += b.y; }
+        else { x0 += a.x; y0 += a.y; x1 += b.x; y1 += b.y; }
+      }
+    }
+  }
+  out[blockIdx.x * NT + threadIdx.x] = x0 + x1 + x2 + x3 + 3 * (y0 + y1 + y2 + y3);
+}
+
+int main() {
+  const int ngroups = 4096;  // 4096 groups x 512 B = 2 MB of index units: L2-resident
+  std::vector<uint32_t> hu((size_t)ngroups * 32 * 4);
+  uint32_t s = 12345;
+  for (size_t i = 0; i < hu.size(); ++i) {
+    const int lane = (int)((i / 4) % 32), q = (int)(i % 4);
+    s = s * 1664525u + 1013904223u;
+    const uint32_t b0 = (s >> 8) & (WZ - 8), b1 = (s >> 20) & (WZ - 8);
+    hu[i] = (b0 | ((lane + 2 * q) & 7)) | ((b1 | ((lane + 2 * q + 1) & 7)) << 16);
+  }
+  uint4* du; double* dout;
+  const int grid = 148 * 2, reps = 200;
+  cudaMalloc(&du, hu.size() * 4);
+  cudaMalloc(&dout, sizeof(double) * grid * NT);
+  cudaMemcpy(du, hu.data(), hu.size() * 4, cudaMemcpyHostToDevice);
+  const int smem = WZ * 16;
+  cudaFuncSetAttribute(k_gather<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_gather<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_gather<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  for (int var = 0; var < 3; ++var) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+      cudaEventRecord(a);
+      if (var == 0) k_gather<0><<<grid, NT, smem>>>(du, ngroups, reps, dout);
+      if (var == 1) k_gather<1><<<grid, NT, smem>>>(du, ngroups, reps, dout);
+      if (var == 2) k_gather<2><<<grid, NT, smem>>>(du, ngroups, reps, dout);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      if (rep) best = ms < best ? ms : best;
+    }
+    const double slots = (double)grid * reps * ngroups * 256;  // per CTA: all groups, 256 slots each
+    const double per_clk = slots / (best * 1e-3) / 148 / (1965e6);
+    printf("var %d: %.3f ms, %.1f G slots/s, %.2f slots/clk/SM at 1965 MHz (peak 8), err=%s\n", var, best,
+           slots / (best * 1e6), per_clk, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
