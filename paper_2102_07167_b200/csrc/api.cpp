@@ -724,6 +724,14 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
   const int64_t nl = P.row_end - P.row_begin;
   struct E { int32_t row, col; int8_t neg; };
   std::vector<E> ents;
+  // hot chunk layout (plan.h): cd.ng half-groups of 4 slots per lane; full groups of 8
+  // 16-bit slots (16 bytes per lane), then one trailing half-group (8 bytes per lane) if odd
+  auto hot_slot = [&](const ChunkDesc& cd, int l, uint32_t pos) -> uint32_t {
+    const uint16_t* s16 = reinterpret_cast<const uint16_t*>(&P.pool[(size_t)cd.ofs + HDR_UNITS]);
+    const uint32_t g = pos / 8, full = cd.ng / 2;
+    const int ne = g < full ? 8 : 4;
+    return s16[(size_t)g * 256 + (size_t)l * ne + pos % 8];
+  };
   for (const TileDesc& T : P.tiles) {
     for (int pi = T.part0; pi < T.part0 + T.nparts; ++pi) {
       const PartDesc& pd = P.parts[(size_t)pi];
@@ -742,17 +750,17 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
               return fail(KUR_ERR_INVALID_ARG, "plan: bad chunk header");
             seen[lr] = 1;
           }
-          for (uint32_t g = 0; g < cd.ng; ++g) {
-            const Unit& U = P.pool[(size_t)cd.ofs + HDR_UNITS + (size_t)g * 32 + (size_t)l];
-            for (int q = 0; q < (hot ? 8 : 4); ++q) {
+          // hot: cd.ng half-groups of 4 slots; remote: cd.ng groups of 4 32-bit columns
+          for (uint32_t pos = 0; pos < 4 * cd.ng; ++pos) {
+            {
               int64_t col;
               if (hot) {
-                const uint32_t e = (q & 1) ? (U.w[q >> 1] >> 16) : (U.w[q >> 1] & 0xFFFFu);
+                const uint32_t e = hot_slot(cd, l, pos);
                 if (e >= HOT_SENT && e < HOT_SENT + 8) continue;
                 if (e > HOT_SENT) return fail(KUR_ERR_INVALID_ARG, "plan: hot index out of window");
                 col = (int64_t)pd.window * WZ + e;
               } else {
-                const uint32_t e = U.w[q];
+                const uint32_t e = P.pool[(size_t)cd.ofs + HDR_UNITS + (size_t)(pos / 4) * 32 + (size_t)l].w[pos % 4];
                 if (e == (uint32_t)P.n) continue;
                 col = e;
               }
@@ -763,17 +771,15 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
           }
         }
         if (hot) {  // bank-conflict freedom: distinct slot residues per quarter-warp position
-          for (uint32_t g = 0; g < cd.ng; ++g)
-            for (int q = 0; q < 8; ++q)
-              for (int qw = 0; qw < 4; ++qw) {
-                int mask = 0;
-                for (int l = qw * 8; l < qw * 8 + 8; ++l) {
-                  const Unit& U = P.pool[(size_t)cd.ofs + HDR_UNITS + (size_t)g * 32 + (size_t)l];
-                  const uint32_t e = (q & 1) ? (U.w[q >> 1] >> 16) : (U.w[q >> 1] & 0xFFFFu);
-                  if (mask >> (e & 7) & 1) p->conflicts++;  // NOLINT
-                  mask |= 1 << (e & 7);
-                }
+          for (uint32_t pos = 0; pos < 4 * cd.ng; ++pos)
+            for (int qw = 0; qw < 4; ++qw) {
+              int mask = 0;
+              for (int l = qw * 8; l < qw * 8 + 8; ++l) {
+                const uint32_t e = hot_slot(cd, l, pos);
+                if (mask >> (e & 7) & 1) p->conflicts++;  // NOLINT
+                mask |= 1 << (e & 7);
               }
+            }
         }
       }
     }

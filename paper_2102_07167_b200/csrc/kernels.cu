@@ -58,6 +58,14 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p, uint64_t pol) {
   return r;
 }
 
+__device__ __forceinline__ uint2 ldg_stream2(const uint2* p, uint64_t pol) {
+  uint2 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+      : "=r"(r.x), "=r"(r.y)
+      : "l"(p), "l"(pol));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -148,6 +156,23 @@ __device__ __forceinline__ void hot8(const uint4 v, const double2* zs, double& x
   }
 }
 
+// The 4 window-local z entries of a trailing half-group unit (8 bytes).
+__device__ __forceinline__ void hot4(const uint2 v, const double2* zs, double& x0, double& y0, double& x1,
+                                     double& y1) {
+  const double2 a = zs[v.x & 0xFFFFu];
+  const double2 b = zs[v.x >> 16];
+  const double2 c = zs[v.y & 0xFFFFu];
+  const double2 d = zs[v.y >> 16];
+  x0 += a.x;
+  y0 += a.y;
+  x1 += b.x;
+  y1 += b.y;
+  x0 += c.x;
+  y0 += c.y;
+  x1 += d.x;
+  y1 += d.y;
+}
+
 // COHERENT: z was written earlier by the same kernel (single-CTA trajectory
 // kernel) -> read through L2 (ld.global.cg) instead of the non-coherent path.
 template <bool COHERENT>
@@ -172,12 +197,18 @@ __device__ __forceinline__ void rem4(const uint4 v, const double2* __restrict__ 
   y1 += d.y;
 }
 
-// Hot part of one chunk: ng groups of 32 units starting at q (lane-offset applied).
-// Rotating software pipeline: the unit of group g+4 is requested before group g
-// is gathered, so four 16-byte index loads per lane are always in flight and
-// there is no serial tail (loads past ng are predicated off).
-__device__ __forceinline__ void run_hot(const uint4* __restrict__ q, uint32_t ng, const double2* zs,
+// Hot part of one chunk: H half-groups of 4 slots per lane starting at base (the
+// chunk's first group, no lane offset): H/2 full groups of 32 16-byte units, then
+// one trailing group of 32 8-byte units when H is odd.  Rotating software
+// pipeline: the unit of group g+4 is requested before group g is gathered, so
+// four 16-byte index loads per lane are always in flight and there is no serial
+// tail (loads past the last group are predicated off).
+__device__ __forceinline__ void run_hot(const uint4* __restrict__ base, uint32_t H, int lane, const double2* zs,
                                         uint64_t pol, double& sx, double& sy) {
+  const uint32_t ng = H >> 1;
+  const uint4* q = base + lane;
+  const uint2 tail = (H & 1u) ? ldg_stream2(reinterpret_cast<const uint2*>(base + (size_t)ng * 32) + lane, pol)
+                              : make_uint2(0, 0);
   double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
   const uint4 z4 = make_uint4(0, 0, 0, 0);
   uint4 b0 = ng > 0 ? ldg_stream(q, pol) : z4;
@@ -202,6 +233,7 @@ __device__ __forceinline__ void run_hot(const uint4* __restrict__ q, uint32_t ng
     if (g + 7 < ng) b3 = ldg_stream(qn + 96, pol);
     hot8(c, zs, x0, y0, x1, y1);
   }
+  if (H & 1u) hot4(tail, zs, x0, y0, x1, y1);
   sx = x0 + x1;
   sy = y0 + y1;
 }
@@ -434,7 +466,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       const uint4* q = dp.pool + cd.x;
       const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
       double sx, sy;
-      if (hot) run_hot(q + HDR_UNITS + lane, cd.y, zs, pol, sx, sy);
+      if (hot) run_hot(q + HDR_UNITS, cd.y, lane, zs, pol, sx, sy);
       else run_remote<SMALL>(q + HDR_UNITS + lane, cd.y, a.zin, pol, sx, sy);
       const int lp = P.neg >> 8;  // row pieces: 2^lp consecutive lanes hold one row
       for (int o = 1; o < (1 << lp); o <<= 1) {

@@ -21,8 +21,12 @@
 // (longest first) and cut into CHUNKS of 32 rows, one row per lane, so the
 // rows of a chunk have nearly equal lengths (little padding).  A chunk is a
 // 64-byte header (32 x uint16 local row ids, 0xFFFF = empty lane) followed by
-// ng groups of 32 16-byte units; unit (g, lane) holds the lane's entries at
-// positions 8g..8g+7 (hot) or 4g..4g+3 (remote).  In hot parts the entries of
+// the lane-interleaved entries.  Remote chunks: ng groups of 32 16-byte units,
+// unit (g, lane) = the lane's 32-bit columns at positions 4g..4g+3.  Hot chunks:
+// ng counts HALF-groups of 4 positions; ng/2 full groups of 32 16-byte units
+// (unit (g, lane) = 16-bit slots at positions 8g..8g+7), then, if ng is odd, one
+// trailing group of 32 8-byte units (positions 8(ng/2)..+3), so a chunk's length
+// is rounded up to 4 positions, not 8.  In hot parts the entries of
 // every quarter-warp (lanes 8q..8q+7) at one position have pairwise distinct
 // slot residues mod 8, i.e. they hit distinct 16-byte shared-memory bank
 // groups: every LDS.128 of the gather loop is bank-conflict free.  Padding
@@ -67,7 +71,7 @@ struct PartDesc {   // 16 bytes; device array
 
 struct ChunkDesc {  // 8 bytes; device array
   uint32_t ofs;     // pool offset (16-byte units) of the chunk header
-  uint32_t ng;      // groups after the header (each group = 32 units)
+  uint32_t ng;      // remote: groups of 4 positions; hot: half-groups of 4 positions (see above)
 };
 
 struct Unit {       // 16 bytes of the pool

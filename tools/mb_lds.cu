@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(NT, 2) k_gather(const uint4* __restrict__ unit
   double x0 = 0, y0 = 0, x1 = 0, y1 = 0, x2 = 0, y2 = 0, x3 = 0, y3 = 0;
   uint32_t h = 2654435761u * (blockIdx.x * NT + threadIdx.x + 1);
   for (int r = 0; r < reps; ++r) {
-    for (int g = wid; g < ngroups; g += NT / 32) {
+    for (int g = blockIdx.x * (NT / 32) + wid; g < ngroups; g += gridDim.x * (NT / 32)) {
       uint32_t w[4];
       if (VAR == 0) {
         h = h * 1664525u + 1013904223u;
@@ -50,9 +50,10 @@ __global__ void __launch_bounds__(NT, 2) k_gather(const uint4* __restrict__ unit
   out[blockIdx.x * NT + threadIdx.x] = x0 + x1 + x2 + x3 + 3 * (y0 + y1 + y2 + y3);
 }
 
-int main() {
-  const int ngroups = 4096;  // 4096 groups x 512 B = 2 MB of index units: L2-resident
-  std::vector<uint32_t> hu((size_t)ngroups * 32 * 4);
+int main(int argc, char** argv) {
+  // default: 4096 groups x 512 B = 2 MB of index units (L2-resident); argv[1] groups (e.g. 4194304 = 2 GB: HBM)
+  const int ngroups = argc > 1 ? atoi(argv[1]) : 4096;
+  std::vector<uint32_t> hu((size_t)ngroups * 32 * 4);  // up to 2 GB
   uint32_t s = 12345;
   for (size_t i = 0; i < hu.size(); ++i) {
     const int lane = (int)((i / 4) % 32), q = (int)(i % 4);
@@ -61,7 +62,7 @@ int main() {
     hu[i] = (b0 | ((lane + 2 * q) & 7)) | ((b1 | ((lane + 2 * q + 1) & 7)) << 16);
   }
   uint4* du; double* dout;
-  const int grid = 148 * 2, reps = 200;
+  const int grid = 148 * 2, reps = argc > 2 ? atoi(argv[2]) : 20000;
   cudaMalloc(&du, hu.size() * 4);
   cudaMalloc(&dout, sizeof(double) * grid * NT);
   cudaMemcpy(du, hu.data(), hu.size() * 4, cudaMemcpyHostToDevice);
@@ -85,7 +86,7 @@ int main() {
       float ms; cudaEventElapsedTime(&ms, a, b);
       if (rep) best = ms < best ? ms : best;
     }
-    const double slots = (double)grid * reps * ngroups * 256;  // per CTA: all groups, 256 slots each
+    const double slots = (double)reps * ngroups * 256;  // every group once per rep, 256 slots each
     const double per_clk = slots / (best * 1e-3) / 148 / (1965e6);
     printf("var %d: %.3f ms, %.1f G slots/s, %.2f slots/clk/SM at 1965 MHz (peak 8), err=%s\n", var, best,
            slots / (best * 1e6), per_clk, cudaGetErrorString(cudaGetLastError()));
