@@ -93,8 +93,10 @@ typedef struct {
                                (direct CSR); must be <= 1. */
   int32_t hot_min;          /* tuning: minimum entries of a tile in one column window for the
                                window to be staged in shared memory; <= 0 selects the default */
-  int32_t flags;            /* 0 (size-based choice), or a forced tile size in rows: a multiple of 32
-                               in [32, 2048] (tuning / tests) */
+  int32_t flags;            /* tuning / tests, 0 = automatic: low 16 bits a forced tile size in rows
+                               (a multiple of 32 in [32, 2048]); | KUR_FLAG_REMOTE_PASS or
+                               | KUR_FLAG_REMOTE_INLINE forces where the remote (global-gather)
+                               entries are summed: a separate pass before each stage, or inline */
   int32_t scaling;          /* KUR_SCALING_UNIFORM: M_m = N (the north_star model), or
                                KUR_SCALING_DEGREE: M_m = sum_l A_ml (a zero row gives
                                theta_m' = omega_m).  The degree counts the off-diagonal
@@ -104,6 +106,7 @@ typedef struct {
 } kur_graph_desc;
 
 enum { KUR_SCALING_UNIFORM = 0, KUR_SCALING_DEGREE = 1 };
+enum { KUR_FLAG_REMOTE_PASS = 1 << 16, KUR_FLAG_REMOTE_INLINE = 2 << 16 };
 
 /* Multi-GPU placement: contiguous ranges of whole communities per rank,
  * balanced by stored-entry count (every rank computes the same split).

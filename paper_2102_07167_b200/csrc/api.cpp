@@ -60,6 +60,7 @@ struct kur_graph {
   double2 *zA = nullptr, *zB = nullptr, *TA = nullptr, *TB = nullptr, *S = nullptr, *partial = nullptr;
   double* acc = nullptr;
   double* pmax = nullptr;
+  double2* Wr = nullptr;
   Ctrl* ctrl = nullptr;
   ncclComm_t comm = nullptr;
   int world = 1;
@@ -87,7 +88,7 @@ struct kur_graph {
     cudaSetDevice(device);
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
-                    xsend, xrecv, d_rowscale, d_potc, pmax};
+                    xsend, xrecv, d_rowscale, d_potc, pmax, Wr};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -252,8 +253,16 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   dp.rowscale = g->d_rowscale;
   dp.potc = g->d_potc;
   dp.has_parts = 0;
-  for (const TileDesc& T : P.tiles)
+  dp.has_remote = 0;
+  for (const TileDesc& T : P.tiles) {
     if (T.nparts > 0) dp.has_parts = 1;
+    if (T.nparts > T.nhot && P.split_remote) dp.has_remote = 1;
+  }
+  if (dp.has_remote) {
+    if ((e = cudaMalloc((void**)&g->Wr, sizeof(double2) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess)
+      return bail(e, "Wr");
+  }
+  dp.Wr = g->Wr;
   // tiny graphs run a whole trajectory in one CTA (launch latency dominates otherwise)
   g->small = P.small;
   dp.shard_row0 = g->d_shard_row0;

@@ -331,9 +331,12 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     return KUR_ERR_INVALID_ARG;
   }
   if (d->reserved != 0) { err = "reserved must be 0"; return KUR_ERR_INVALID_ARG; }
-  const int force_rows = d->flags;
-  if (force_rows != 0 && (force_rows < 32 || force_rows > MAX_TILE_ROWS || force_rows % 32 != 0)) {
-    err = "flags: 0 or a tile size in rows (multiple of 32 in [32, 2048])";
+  const int force_rows = d->flags & 0xFFFF;
+  const int force_split = (d->flags >> 16) & 3;  // KUR_FLAG_REMOTE_PASS (1) / KUR_FLAG_REMOTE_INLINE (2)
+  if ((force_rows != 0 && (force_rows < 32 || force_rows > MAX_TILE_ROWS || force_rows % 32 != 0)) ||
+      (d->flags >> 18) != 0 || force_split == 3) {
+    err = "flags: 0 or a tile size in rows (multiple of 32 in [32, 2048]), optionally | KUR_FLAG_REMOTE_PASS "
+          "or | KUR_FLAG_REMOTE_INLINE";
     return KUR_ERR_INVALID_ARG;
   }
   const double thr = d->dense_threshold;
@@ -813,6 +816,15 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     P.n_hot_parts += O.nhot;
     P.n_window_loads += O.loads;
   }
+  // Remote parts (global z gathers, ~1 L1 wavefront each) are summed by a separate
+  // k_remote pass before k_stage when they are numerous and concentrated: then the
+  // latency-bound gathers get 3 CTAs per SM of their own instead of stalling a
+  // tile between its shared-memory gathers.  Measured on B200 (RK stage time):
+  // config 5 (42 M remote slots, 20 K per tile) 1.226 -> 1.181 ms with the pass;
+  // config 4 (7.7 M, 7 K per tile) 0.312 -> 0.350 ms and config 3 (4.3 M, 17 K per
+  // tile, 44 us stage) 0.044 -> 0.049 ms, so those stay inline.
+  P.split_remote = !P.small && P.n_slots_remote >= (16LL << 20) && nt > 0 && P.n_slots_remote / nt >= 8192;
+  if (force_split) P.split_remote = !P.small && force_split == 1;
 #pragma omp parallel for schedule(dynamic, 4)
   for (int32_t lt = 0; lt < nt; ++lt) {
     TileOut& O = outs[(size_t)lt];

@@ -260,6 +260,46 @@ __device__ __forceinline__ void run_remote(const uint4* __restrict__ q, uint32_t
   sy = y0 + y1;
 }
 
+// The chunks of one part (P:562-570 complement entries subtracted, P:538-542
+// non-zero entries added into the tile's row sums Ws), snake order over the
+// NWARPS warps (chunks are sorted longest first); the next chunk's descriptor
+// is requested before the current chunk is gathered.  Hot parts gather from the
+// staged window zs, remote parts from global z.
+template <bool COHERENT>
+__device__ __forceinline__ void run_part(const DevPlan& dp, const PartDesc& P, bool hot, const double2* zs,
+                                         const double2* __restrict__ z, double2* Ws, uint64_t pol, int warp,
+                                         int lane) {
+    uint32_t c = warp;
+    uint2 cdn = c < P.nchunks ? __ldg(dp.chunks + P.chunk0 + c) : make_uint2(0, 0);
+    for (uint32_t r = 0; c < P.nchunks; ++r) {
+      const uint2 cd = cdn;
+      const uint32_t cnext = (r + 1) * NWARPS + (((r + 1) & 1) ? (NWARPS - 1 - warp) : warp);
+      if (cnext < P.nchunks) cdn = __ldg(dp.chunks + P.chunk0 + cnext);
+      const uint4* q = dp.pool + cd.x;
+      const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
+      double sx, sy;
+      if (hot) run_hot(q + HDR_UNITS, cd.y, lane, zs, pol, sx, sy);
+      else run_remote<COHERENT>(q + HDR_UNITS + lane, cd.y, z, pol, sx, sy);
+      const int lp = P.neg >> 8;  // row pieces: 2^lp consecutive lanes hold one row
+      for (int o = 1; o < (1 << lp); o <<= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      }
+      if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) {
+        double2 w = Ws[row];
+        if (P.neg & 1) {
+          w.x -= sx;
+          w.y -= sy;
+        } else {
+          w.x += sx;
+          w.y += sy;
+        }
+        Ws[row] = w;
+      }
+      c = cnext;
+    }
+}
+
 // Executed by every thread of the LAST CTA of a grid: S_b from the per-tile
 // partials, T_a, the order parameter and its recording.
 __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
@@ -429,8 +469,12 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
                                            double& dmax) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool parts = dp.has_parts;
+  // remote parts of the tile were summed by k_remote into Wr (SMALL: inline, below)
+  const bool split = !SMALL && dp.has_remote;  // small plans (k_small, or kur_rhs on them) stay inline
+  const bool pre = split && T.nparts > T.nhot;
   if (parts) {
-    for (int r = tid; r < T.nrows; r += NTHREADS) Ws[r] = make_double2(0.0, 0.0);
+    for (int r = tid; r < T.nrows; r += NTHREADS)
+      Ws[r] = pre ? __ldcg(dp.Wr + (T.row0 - dp.row_begin) + r) : make_double2(0.0, 0.0);
     __syncthreads();
   }
   // ---- parts: hot ones gather from the staged window, remote ones from global memory
@@ -443,49 +487,34 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     g_prof[(size_t)blockIdx.x * PROF_STRIDE + 28] = (unsigned long long)T.nparts;
   }
 #endif
-  for (int p = T.part0; p < T.part0 + T.nparts; ++p) {
+  // Order: remote parts first (when inline), then the hot parts in window order,
+  // so W_j accumulates in the same sequence whether the remote parts run here or
+  // in k_remote (Ws then starts from Wr): bitwise identical results either way.
+  // The first hot window's TMA copy is issued up front and overlaps the remote parts.
+  const int nrem = split ? 0 : T.nparts - T.nhot;
+  bool pending = false;
+#ifdef KUR_PROFILE
+  if (!SMALL && g_prof && tid == 0) g_prof[(size_t)blockIdx.x * PROF_STRIDE + 29] = (unsigned long long)nrem;
+#endif
+  if (T.nhot > 0) {
+    loaded = dp.parts[T.part0].window;
+    pending = true;
+    if (tid == 0) tma_load_1d(zs, a.zin + (size_t)loaded * WZ, WZ * sizeof(double2), bar);
+  }
+  for (int pi = 0; pi < nrem + T.nhot; ++pi) {
+    const int p = pi < nrem ? T.part0 + T.nhot + pi : T.part0 + (pi - nrem);
     const PartDesc P = dp.parts[p];
     const bool hot = P.window >= 0;
-    const int pi = p - T.part0;
     if (!SMALL && pi < 8) PROF_T(1 + 3 * pi);
-    if (hot && P.window != loaded) {  // all reads of the previous window ended at the last barrier
-      if (tid == 0) tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), bar);
+    if (hot && (P.window != loaded || pending)) {  // all reads of the previous window ended at the last barrier
+      if (P.window != loaded && tid == 0) tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), bar);
       mbar_wait(bar, phase);
       phase ^= 1u;
       loaded = P.window;
+      pending = false;
     }
     if (!SMALL && pi < 8) PROF_T(2 + 3 * pi);
-    // chunks of the part, snake order over the 16 warps (chunks are sorted longest first);
-    // the next chunk's descriptor is requested before the current chunk is gathered
-    uint32_t c = warp;
-    uint2 cdn = c < P.nchunks ? __ldg(dp.chunks + P.chunk0 + c) : make_uint2(0, 0);
-    for (uint32_t r = 0; c < P.nchunks; ++r) {
-      const uint2 cd = cdn;
-      const uint32_t cnext = (r + 1) * NWARPS + (((r + 1) & 1) ? (NWARPS - 1 - warp) : warp);
-      if (cnext < P.nchunks) cdn = __ldg(dp.chunks + P.chunk0 + cnext);
-      const uint4* q = dp.pool + cd.x;
-      const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
-      double sx, sy;
-      if (hot) run_hot(q + HDR_UNITS, cd.y, lane, zs, pol, sx, sy);
-      else run_remote<SMALL>(q + HDR_UNITS + lane, cd.y, a.zin, pol, sx, sy);
-      const int lp = P.neg >> 8;  // row pieces: 2^lp consecutive lanes hold one row
-      for (int o = 1; o < (1 << lp); o <<= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        sy += __shfl_xor_sync(0xffffffffu, sy, o);
-      }
-      if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) {
-        double2 w = Ws[row];
-        if (P.neg & 1) {
-          w.x -= sx;
-          w.y -= sy;
-        } else {
-          w.x += sx;
-          w.y += sy;
-        }
-        Ws[row] = w;
-      }
-      c = cnext;
-    }
+    run_part<SMALL>(dp, P, hot, zs, a.zin, Ws, pol, warp, lane);
     if (!SMALL) PROF_W(pi, warp);
     __syncthreads();
     if (!SMALL && pi < 8) PROF_T(3 + 3 * pi);
@@ -566,6 +595,27 @@ __global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const S
   double x, y;
   prologue_rows(dp, a, T, x, y);
   tile_partial_and_finish(dp, a, lt, x, y, red);
+}
+
+// a3, remote half: the remote parts of every tile (global z gathers, latency
+// bound), W_r = -sum_{Z_j remote} z_k + sum_{NZ_j remote} z_k, into Wr.  A
+// separate launch before k_stage: with up to 4 CTAs per SM (no window in
+// shared memory) the random gathers get four times the memory-level
+// parallelism they have between k_stage's shared-memory gathers.
+__global__ void __launch_bounds__(NTHREADS, 3) k_remote(const DevPlan dp, const double2* __restrict__ zin) {
+  extern __shared__ __align__(16) double2 Wrs[];
+  const TileDesc T = dp.tiles[dp.order[blockIdx.x]];
+  if (T.nparts == T.nhot) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int r = tid; r < T.nrows; r += NTHREADS) Wrs[r] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const uint64_t pol = evict_first_policy();
+  for (int p = T.part0 + T.nhot; p < T.part0 + T.nparts; ++p) {
+    const PartDesc P = dp.parts[p];
+    run_part<false>(dp, P, false, nullptr, zin, Wrs, pol, warp, lane);
+    __syncthreads();
+  }
+  for (int r = tid; r < T.nrows; r += NTHREADS) dp.Wr[(T.row0 - dp.row_begin) + r] = Wrs[r];
 }
 
 template <int MODE>
@@ -718,6 +768,11 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
     cudaError_t e = cudaFuncSetAttribute(k_stage<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
+  }
+  if (dp.has_remote) {
+    k_remote<<<dp.ntiles, NTHREADS, sizeof(double2) * (size_t)dp.rows_per_tile, s>>>(dp, a.zin);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
   }
   k_stage<MODE><<<dp.ntiles, NTHREADS, dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) : 0, s>>>(dp, a);
   return cudaGetLastError();

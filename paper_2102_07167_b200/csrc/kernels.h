@@ -29,6 +29,7 @@ struct DevPlan {
   int32_t row_begin;      // internal id of local row 0
   int32_t world;
   int32_t has_parts;          // any tile has stored entries (else no shared memory is needed)
+  int32_t has_remote;         // any tile has remote parts (k_remote runs before each k_stage)
   const TileDesc* tiles;      // [ntiles]
   const int32_t* order;       // [ntiles] launch order
   const PartDesc* parts;      // [n_parts]
@@ -48,6 +49,7 @@ struct DevPlan {
   const double* potc;         // [local rows] potential constants (kur_potential)
   double2* partial;           // [ntiles_all] per-tile sums of z (global tile ids)
   double* pmax;               // [ntiles_all] per-tile max |fixed-point update| (implicit midpoint)
+  double2* Wr;                // [local rows] remote-part row sums of the current stage (k_remote -> k_stage)
   double2* S;                 // [C] block sums S_b of the last reduction
   Ctrl* ctrl;
 };

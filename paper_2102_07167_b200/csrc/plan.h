@@ -83,6 +83,7 @@ struct HostPlan {
   int32_t C = 0;
   int rows_per_tile = NTHREADS;
   bool small = false;                     // world 1, n <= 8192, few entries: single-CTA kur_step
+  bool split_remote = false;              // remote parts summed by a separate k_remote pass (see builder)
   int32_t rank = 0, world = 1;
   int64_t row_begin = 0, row_end = 0;     // this rank's internal rows
   int32_t tile_begin = 0, tile_end = 0;   // this rank's tiles (global ids)

@@ -173,11 +173,19 @@ class Graph:
         return x_internal_full[self.row_begin:self.row_end]
 
 
-def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, scaling=None, device=None, dist=None,
-                **arrays):
+FLAG_REMOTE_PASS, FLAG_REMOTE_INLINE = 1 << 16, 2 << 16
+
+
+def _flags(tile_rows, remote_pass):
+    return int(tile_rows) | (0 if remote_pass is None else (FLAG_REMOTE_PASS if remote_pass else FLAG_REMOTE_INLINE))
+
+
+def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, remote_pass=None, scaling=None,
+                device=None, dist=None, **arrays):
     """kur_graph_build from a kurgen.Instance (or the same arrays as keywords).
 
-    scaling: 0 = uniform K/N (default, or inst.scaling), 1 = degree K/deg_m."""
+    scaling: 0 = uniform K/N (default, or inst.scaling), 1 = degree K/deg_m.
+    remote_pass: None = automatic, True/False = force the separate remote-gather pass / inline."""
     src = arrays if inst is None else dict(
         n=inst.n, n_comm=inst.n_comm, community=inst.community, seg_ptr=inst.seg_ptr,
         seg_comm=inst.seg_comm, seg_kind=inst.seg_kind, idx_ptr=inst.idx_ptr, idx=inst.idx)
@@ -194,8 +202,8 @@ def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, scal
                      community=_np_ptr(keep["community"]), seg_ptr=_np_ptr(keep["seg_ptr"]),
                      seg_comm=_np_ptr(keep["seg_comm"]), seg_kind=_np_ptr(keep["seg_kind"]),
                      idx_ptr=_np_ptr(keep["idx_ptr"]), idx=_np_ptr(keep["idx"]),
-                     dense_threshold=float(dense_threshold), hot_min=int(hot_min), flags=int(tile_rows),
-                     scaling=int(scaling), reserved=0)
+                     dense_threshold=float(dense_threshold), hot_min=int(hot_min),
+                     flags=_flags(tile_rows, remote_pass), scaling=int(scaling), reserved=0)
     if device is None:
         device = torch.cuda.current_device()
     dd = None

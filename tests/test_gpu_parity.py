@@ -72,18 +72,36 @@ def test_rhs_small_random(cfg, kind, thr):
     assert ok, err
 
 
+@pytest.mark.parametrize("remote_pass", [None, True, False])
 @pytest.mark.parametrize("hot_min", [1, 1 << 30])
 @pytest.mark.parametrize("tile_rows", [32, 512, 2048])
-def test_rhs_layout_variants(hot_min, tile_rows):
-    """All-hot / all-remote layouts and several tile sizes give the same RHS."""
+def test_rhs_layout_variants(hot_min, tile_rows, remote_pass):
+    """All-hot / all-remote layouts, several tile sizes, remote entries summed by the
+    separate k_remote pass or inline: the same RHS."""
     inst = kurgen.sbm([2100, 700, 5000, 1, 33, 0, 900], np.array(
         [[0.97, 0.3, 0.001, 0.0, 0.9, 0, 0.0], [0.3, 0.6, 0.0, 0.5, 0.0, 0, 0.01],
          [0.001, 0.0, 0.02, 0.0, 0.3, 0, 0.0], [0.0, 0.5, 0.0, 0.0, 0.0, 0, 0.0],
          [0.9, 0.0, 0.3, 0.0, 1.0, 0, 0.0], [0] * 7, [0.0, 0.01, 0.0, 0.0, 0.0, 0, 0.99]]), 13, K=3.0)
     ref = oracle.rhs(oracle.Graph(inst), inst.theta0, inst.omega, inst.K, mode="naive")
-    got = Run(inst, hot_min=hot_min, tile_rows=tile_rows).rhs()
+    got = Run(inst, hot_min=hot_min, tile_rows=tile_rows, remote_pass=remote_pass).rhs()
     ok, err = close(got, ref, abs_tol=1e-13, rel_tol=1e-12)
     assert ok, err
+
+
+@pytest.mark.parametrize("remote_pass", [True, False])
+def test_trajectory_remote_pass_modes(remote_pass):
+    """RK4 with the remote entries summed by k_remote (or inline), 10 steps + r(t), bitwise repeatable."""
+    inst = kurgen.sbm([3000, 2500, 1200], np.array([[0.97, 0.002, 0.01], [0.002, 0.95, 0.003],
+                                                     [0.01, 0.003, 0.2]]), 29, K=3.0, h=0.01)
+    th_ref, th10_ref, rt_ref = oracle.rk4(oracle.Graph(inst), inst.theta0, inst.omega, inst.K, inst.h, 10, 1,
+                                          mode="naive")
+    run = Run(inst, tile_rows=512, remote_pass=remote_pass)
+    th, rt = run.step(10, 1)
+    th_b, rt_b = run.step(10, 1)
+    ok, err = close(th, th10_ref)
+    assert ok, err
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(rt_ref))) <= R_TOL
+    assert np.array_equal(th, th_b) and np.array_equal(rt, rt_b)
 
 
 def test_trajectory_small_sbm_and_determinism():

@@ -21,10 +21,11 @@ def _instances():
     yield "cfg3", kurgen.config(3)
 
 
+@pytest.mark.parametrize("remote_pass", [None, True])
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_group_bitwise_equals_single(world):
+def test_group_bitwise_equals_single(world, remote_pass):
     for name, inst in _instances():
-        g1 = kur.graph_build(inst)
+        g1 = kur.graph_build(inst, remote_pass=remote_pass)
         dev = "cuda:0"
         th_full = g1.to_internal(torch.from_numpy(inst.theta0).to(dev))
         om_full = g1.to_internal(torch.from_numpy(inst.omega).to(dev))
@@ -32,7 +33,7 @@ def test_group_bitwise_equals_single(world):
         th1 = th_full.clone()
         rt1 = kur.step(g1, th1, om_full, inst.K, inst.h, 6, 1)
 
-        gs = kur.group_build(inst, world)
+        gs = kur.group_build(inst, world, remote_pass=remote_pass)
         assert all(np.array_equal(g.perm, g1.perm) for g in gs)
         bounds = [(g.row_begin, g.row_end) for g in gs]
         assert bounds[0][0] == 0 and bounds[-1][1] == inst.n

@@ -23,6 +23,20 @@
 
 constexpr int NT = 512, NW = NT / 32;
 
+template <int KIND>
+__device__ __forceinline__ double2 ldz(const double2* p) {
+  double2 r;
+  if (KIND == 0) return __ldg(p);
+  if (KIND == 1) return __ldcg(p);
+  if (KIND == 2) {
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+  }
+  asm("ld.global.nc.L1::evict_first.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+
+template <int KIND>
 __global__ void __launch_bounds__(NT, 2) k_ldg(const uint4* __restrict__ units, long long ngroups,
                                                const double2* __restrict__ z, double* out) {
   double x = 0, y = 0;
@@ -30,7 +44,7 @@ __global__ void __launch_bounds__(NT, 2) k_ldg(const uint4* __restrict__ units, 
   const long long w = (long long)blockIdx.x * NW + (threadIdx.x >> 5), nw = (long long)gridDim.x * NW;
   for (long long g = w; g < ngroups; g += nw) {
     const uint4 u = __ldg(units + g * 32 + lane);
-    const double2 a = __ldg(z + u.x), b = __ldg(z + u.y), c = __ldg(z + u.z), d = __ldg(z + u.w);
+    const double2 a = ldz<KIND>(z + u.x), b = ldz<KIND>(z + u.y), c = ldz<KIND>(z + u.z), d = ldz<KIND>(z + u.w);
     x += a.x + b.x + c.x + d.x;
     y += a.y + b.y + c.y + d.y;
   }
@@ -128,12 +142,15 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
   double sums[2];
-  for (int which = 0; which < 2; ++which) {
+  for (int which = 0; which < 5; ++which) {
     float best = 1e30f;
     for (int rep = 0; rep < 6; ++rep) {
       cudaEventRecord(a);
-      if (which == 0) k_ldg<<<grid, NT>>>(du, ngroups, dz, dout);
-      else k_tma<<<grid / 2, NT, smem>>>(tm, du, ngroups, dout);
+      if (which == 0) k_ldg<0><<<grid, NT>>>(du, ngroups, dz, dout);
+      if (which == 1) k_tma<<<grid / 2, NT, smem>>>(tm, du, ngroups, dout);
+      if (which == 2) k_ldg<1><<<grid, NT>>>(du, ngroups, dz, dout);
+      if (which == 3) k_ldg<2><<<grid, NT>>>(du, ngroups, dz, dout);
+      if (which == 4) k_ldg<3><<<grid, NT>>>(du, ngroups, dz, dout);
       cudaEventRecord(b);
       CK(cudaEventSynchronize(b));
       float ms; cudaEventElapsedTime(&ms, a, b);
@@ -143,9 +160,9 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(ho.data(), dout, sizeof(double) * grid * NT, cudaMemcpyDeviceToHost));
     if (which == 1) for (int i = grid / 2 * NT; i < grid * NT; ++i) ho[i] = 0;
     double t = 0; for (double v : ho) t += v;
-    sums[which] = t;
-    printf("%s: %.3f ms for %lld entries = %.2f G entries/s, sum %.10e\n", which ? "tma_gather4" : "ldg", best, E,
-           E / (best * 1e6), t);
+    if (which < 2) sums[which] = t;
+    const char* nm[5] = {"ldg.nc", "tma_gather4", "ldg.cg", "ldg.nc.L1::no_allocate", "ldg.nc.L1::evict_first"};
+    printf("%s: %.3f ms for %lld entries = %.2f G entries/s, sum %.10e\n", nm[which], best, E, E / (best * 1e6), t);
   }
   double ref = 0;
   for (long long i = 0; i < E; ++i) ref += hz[idx[i]].x + 3.0 * hz[idx[i]].y;

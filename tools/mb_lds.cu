@@ -4,6 +4,8 @@
 //   0: slot ids computed in registers (pure LDS.128 + DADD)
 //   1: slot ids streamed from global memory as 16-bit pairs (k_stage's layout), L2-resident
 //   2: as 1 with 4 independent accumulator pairs per lane
+//   3: slot ids staged by per-warp TMA bulk copies (cp.async.bulk, 4-deep ring of 512-byte
+//      groups, mbarrier per slot) and read back with LDS.128 (no LSU global loads)
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb_lds tools/mb_lds.cu
 #include <cuda_runtime.h>
@@ -14,6 +16,8 @@
 #include <vector>
 
 constexpr int NT = 512, WZ = 4096;
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <int VAR>
 __global__ void __launch_bounds__(NT, 2) k_gather(const uint4* __restrict__ units, int ngroups, int reps, double* out) {
@@ -27,6 +31,7 @@ __global__ void __launch_bounds__(NT, 2) k_gather(const uint4* __restrict__ unit
   for (int r = 0; r < reps; ++r) {
     for (int g = blockIdx.x * (NT / 32) + wid; g < ngroups; g += gridDim.x * (NT / 32)) {
       uint32_t w[4];
+      if (VAR == 3) break;
       if (VAR == 0) {
         h = h * 1664525u + 1013904223u;
 #pragma unroll
@@ -44,6 +49,46 @@ __global__ void __launch_bounds__(NT, 2) k_gather(const uint4* __restrict__ unit
         const double2 a = zs[w[q] & 0xFFFF], b = zs[w[q] >> 16];
         if (VAR == 2 && (q & 1)) { x2 += a.x; y2 += a.y; x3 += b.x; y3 += b.y; }
         else { x0 += a.x; y0 += a.y; x1 += b.x; y1 += b.y; }
+      }
+    }
+  }
+  if (VAR == 3) {
+    constexpr int D = 4;
+    uint4* ring = reinterpret_cast<uint4*>(sm + WZ * 16) + wid * D * 32;
+    __shared__ __align__(8) uint64_t bar[NT / 32][D];
+    if (lane < D) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar[wid][lane])));
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncwarp();
+    const int g0 = blockIdx.x * (NT / 32) + wid, gs = gridDim.x * (NT / 32);
+    const long long per = ((long long)ngroups - g0 + gs - 1) / gs;  // groups of this warp per rep
+    const long long total = per * reps;
+    auto issue = [&](long long k) {
+      const int g = (int)(g0 + (k % per) * gs);
+      const int d = (int)(k % D);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar[wid][d])), "r"(512) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       sa(ring + d * 32)), "l"(units + (size_t)g * 32), "r"(512), "r"(sa(&bar[wid][d]))
+                   : "memory");
+    };
+    if (lane == 0)
+      for (long long k = 0; k < D && k < total; ++k) issue(k);
+    uint32_t ph = 0;  // bit d = parity of slot d
+    for (long long k = 0; k < total; ++k) {
+      const int d = (int)(k % D);
+      asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+                       sa(&bar[wid][d])), "r"((ph >> d) & 1u) : "memory");
+      ph ^= 1u << d;
+      const uint4 v = ring[d * 32 + lane];
+      __syncwarp();
+      if (lane == 0 && k + D < total) issue(k + D);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 a = zs[w[q] & 0xFFFF], b = zs[w[q] >> 16];
+        x0 += a.x; y0 += a.y; x1 += b.x; y1 += b.y;
       }
     }
   }
@@ -66,21 +111,23 @@ int main(int argc, char** argv) {
   cudaMalloc(&du, hu.size() * 4);
   cudaMalloc(&dout, sizeof(double) * grid * NT);
   cudaMemcpy(du, hu.data(), hu.size() * 4, cudaMemcpyHostToDevice);
-  const int smem = WZ * 16;
+  const int smem = WZ * 16 + (NT / 32) * 4 * 512;
   cudaFuncSetAttribute(k_gather<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_gather<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_gather<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_gather<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
   int clk = 0;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  for (int var = 0; var < 3; ++var) {
+  for (int var = 0; var < 4; ++var) {
     float best = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(a);
       if (var == 0) k_gather<0><<<grid, NT, smem>>>(du, ngroups, reps, dout);
       if (var == 1) k_gather<1><<<grid, NT, smem>>>(du, ngroups, reps, dout);
       if (var == 2) k_gather<2><<<grid, NT, smem>>>(du, ngroups, reps, dout);
+      if (var == 3) k_gather<3><<<grid, NT, smem>>>(du, ngroups, reps, dout);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms; cudaEventElapsedTime(&ms, a, b);

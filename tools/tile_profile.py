@@ -42,15 +42,15 @@ def main():
     attach(None)
     P = buf.view(nt, STRIDE).cpu().numpy().astype(np.float64)
     t0, t25, t26 = P[:, 0], P[:, 25], P[:, 26]
-    nhot, nparts = P[:, 27].astype(int), P[:, 28].astype(int)
+    nhot, nparts, nrem = P[:, 27].astype(int), P[:, 28].astype(int), P[:, 29].astype(int)
     tot = t26 - t0
     wait = np.zeros(nt); hot = np.zeros(nt); rem = np.zeros(nt); imb = np.zeros(nt)
     for t in range(nt):
-        for p in range(min(nparts[t], 8)):
+        for p in range(min(nrem[t] + nhot[t], 8)):
             wb, we, pe = P[t, 1 + 3 * p], P[t, 2 + 3 * p], P[t, 3 + 3 * p]
             wf = P[t, 32 + 16 * p: 48 + 16 * p]
             wait[t] += we - wb
-            (hot if p < nhot[t] else rem)[t] += pe - we
+            (rem if p < nrem[t] else hot)[t] += pe - we  # inline remote parts run first
             imb[t] += pe - wf.mean()
     fin = t26 - t25
     print(f"cfg{args.config}: {nt} tiles, rows/tile {g.info['rows_per_tile']}, parts/tile {nparts.mean():.2f} "
