@@ -260,12 +260,36 @@ __device__ __forceinline__ void run_remote(const uint4* __restrict__ q, uint32_t
   sy = y0 + y1;
 }
 
+// k_remote's loop: as run_remote, but two groups (8 z gathers per lane) in
+// flight at once; missing groups read the zero sentinel z[sent] (sent = n).
+__device__ __forceinline__ void run_remote_deep(const uint4* __restrict__ q, uint32_t ng, uint32_t sent,
+                                                const double2* __restrict__ z, uint64_t pol, double& sx, double& sy) {
+  double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
+  const uint4 s4 = make_uint4(sent, sent, sent, sent);
+  uint4 b0 = ng > 0 ? ldg_stream(q, pol) : s4;
+  uint4 b1 = ng > 1 ? ldg_stream(q + 32, pol) : s4;
+  for (uint32_t g = 0; g < ng; g += 2) {
+    const uint4 c0 = b0, c1 = b1;
+    const uint4* qn = q + (size_t)(g + 2) * 32;
+    b0 = g + 2 < ng ? ldg_stream(qn, pol) : s4;
+    b1 = g + 3 < ng ? ldg_stream(qn + 32, pol) : s4;
+    const double2 a0 = __ldg(z + c0.x), a1 = __ldg(z + c0.y), a2 = __ldg(z + c0.z), a3 = __ldg(z + c0.w);
+    const double2 a4 = __ldg(z + c1.x), a5 = __ldg(z + c1.y), a6 = __ldg(z + c1.z), a7 = __ldg(z + c1.w);
+    x0 += a0.x; y0 += a0.y; x1 += a1.x; y1 += a1.y;
+    x0 += a2.x; y0 += a2.y; x1 += a3.x; y1 += a3.y;
+    x0 += a4.x; y0 += a4.y; x1 += a5.x; y1 += a5.y;
+    x0 += a6.x; y0 += a6.y; x1 += a7.x; y1 += a7.y;
+  }
+  sx = x0 + x1;
+  sy = y0 + y1;
+}
+
 // The chunks of one part (P:562-570 complement entries subtracted, P:538-542
 // non-zero entries added into the tile's row sums Ws), snake order over the
 // NWARPS warps (chunks are sorted longest first); the next chunk's descriptor
 // is requested before the current chunk is gathered.  Hot parts gather from the
 // staged window zs, remote parts from global z.
-template <bool COHERENT>
+template <bool COHERENT, bool DEEP = false>
 __device__ __forceinline__ void run_part(const DevPlan& dp, const PartDesc& P, bool hot, const double2* zs,
                                          const double2* __restrict__ z, double2* Ws, uint64_t pol, int warp,
                                          int lane) {
@@ -279,6 +303,7 @@ __device__ __forceinline__ void run_part(const DevPlan& dp, const PartDesc& P, b
       const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
       double sx, sy;
       if (hot) run_hot(q + HDR_UNITS, cd.y, lane, zs, pol, sx, sy);
+      else if (DEEP) run_remote_deep(q + HDR_UNITS + lane, cd.y, (uint32_t)dp.n, z, pol, sx, sy);
       else run_remote<COHERENT>(q + HDR_UNITS + lane, cd.y, z, pol, sx, sy);
       const int lp = P.neg >> 8;  // row pieces: 2^lp consecutive lanes hold one row
       for (int o = 1; o < (1 << lp); o <<= 1) {
@@ -602,7 +627,7 @@ __global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const S
 // separate launch before k_stage: with up to 4 CTAs per SM (no window in
 // shared memory) the random gathers get four times the memory-level
 // parallelism they have between k_stage's shared-memory gathers.
-__global__ void __launch_bounds__(NTHREADS, 3) k_remote(const DevPlan dp, const double2* __restrict__ zin) {
+__global__ void __launch_bounds__(NTHREADS, 2) k_remote(const DevPlan dp, const double2* __restrict__ zin) {
   extern __shared__ __align__(16) double2 Wrs[];
   const TileDesc T = dp.tiles[dp.order[blockIdx.x]];
   if (T.nparts == T.nhot) return;
@@ -612,7 +637,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_remote(const DevPlan dp, const 
   const uint64_t pol = evict_first_policy();
   for (int p = T.part0 + T.nhot; p < T.part0 + T.nparts; ++p) {
     const PartDesc P = dp.parts[p];
-    run_part<false>(dp, P, false, nullptr, zin, Wrs, pol, warp, lane);
+    run_part<false, true>(dp, P, false, nullptr, zin, Wrs, pol, warp, lane);
     __syncthreads();
   }
   for (int r = tid; r < T.nrows; r += NTHREADS) dp.Wr[(T.row0 - dp.row_begin) + r] = Wrs[r];
