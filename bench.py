@@ -44,12 +44,12 @@ def _measured_peaks():
 
 
 def _ncu_traffic(cfg):
-    """Per-launch dram bytes of the dominant kernel from the committed ncu capture, or None."""
+    """DRAM bytes of one RHS evaluation (k_remote + k_stage) from the committed ncu captures, or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
         v = t.get(f"cfg{cfg}")
-        return None if v is None else float(v["dram_bytes_per_launch"])
+        return None if v is None else float(v["dram_bytes_per_rhs"])
     except Exception:
         return None
 
@@ -245,7 +245,9 @@ def main():
     achieved = bytes_launch / (stage_ms / 1e3) / 1e9
     traffic = _ncu_traffic(args.config) if world == 1 else None  # the capture is a 1-GPU launch
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "k_stage (fused RK4 stage)", "peak_source": peak_src,
+                "traffic": traffic, "peak_source": peak_src,
+                "kernel": ("k_remote + k_stage" if info["remote_pass"] else "k_stage") + " (one RHS evaluation = "
+                          "one fused RK4 stage)",
                 "bytes_per_launch": bytes_launch,
                 "bytes_formula": "SURVEY 8(d): 16N z + 4 n_idx + 8N offsets + 8N omega + 24N RK stage",
                 "avg_launch_ms": stage_ms, "stage_share_of_step": tm["stage_ms"] / ms if ms > 0 else None,
@@ -307,7 +309,8 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 1 + tm["prologue_n"] + tm["stage_n"] + (2 * (tm["prologue_n"] + tm["stage_n"]) if world > 1 else 0),
+            "gpu_launches": 1 + tm["prologue_n"] + tm["stage_n"] * (2 if info["remote_pass"] else 1)
+                            + (2 * (tm["prologue_n"] + tm["stage_n"]) if world > 1 else 0),
             "clocks": clk.result(),
             "host": {"gen_s": gen_s, "build_s": build_s, "nproc": os.cpu_count()},
             "plan": {k: info[k] for k in ("n_idx_hot", "n_idx_remote", "n_slots_hot", "n_slots_remote",

@@ -141,6 +141,9 @@ typedef struct {
   int64_t bytes_per_rhs;       /* algorithmic HBM bytes of one RHS */
   int64_t bytes_pool;          /* device bytes of the index pool (incl. padding) */
   double build_seconds;        /* host time of kur_graph_build */
+  int32_t remote_pass;         /* 1: remote entries summed by the separate k_remote pass before each
+                                  stage kernel (2 launches per RHS), 0: inline */
+  int32_t reserved0;
 } kur_graph_info_t;
 
 typedef struct kur_graph kur_graph; /* opaque; owns all device data and workspace */

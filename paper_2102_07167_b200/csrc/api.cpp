@@ -311,6 +311,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   I.bytes_per_rhs = 2 * P.n_idx_hot + 4 * P.n_idx_remote + 64 * g->n_local;
   I.bytes_pool = pool_bytes;
   I.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  I.remote_pass = dp.has_remote;
   *out = g;
   return KUR_OK;
 }

@@ -50,7 +50,8 @@ class GraphInfo(ctypes.Structure):
                 ("n_idx", _i64), ("n_idx_hot", _i64), ("n_idx_remote", _i64), ("n_slots_hot", _i64),
                 ("n_slots_remote", _i64), ("n_dense_blocks", _i64), ("n_sparse_blocks", _i64),
                 ("n_tiles", _i64), ("n_hot_parts", _i64), ("n_window_loads", _i64), ("sincos_per_rhs", _i64),
-                ("bytes_per_rhs", _i64), ("bytes_pool", _i64), ("build_seconds", _d)]
+                ("bytes_per_rhs", _i64), ("bytes_pool", _i64), ("build_seconds", _d), ("remote_pass", _i32),
+                ("reserved0", _i32)]
 
 
 _lib.kur_graph_build.argtypes = [ctypes.POINTER(GraphDesc), ctypes.POINTER(DistDesc), _p, ctypes.POINTER(_p)]
