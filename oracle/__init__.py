@@ -46,6 +46,9 @@ def _load():
     lib.orc_set_num_threads.argtypes = [ctypes.c_int]
     lib.orc_step_method.argtypes = [p, ctypes.c_int, ctypes.c_int, d, d, i64, i32, p, p, p, d, i32]
     lib.orc_step_method.restype = ctypes.c_int
+    lib.orc_integrate_adaptive.argtypes = [p, ctypes.c_int, d, d, d, d, d, d, d, d, d, d, i64, p, p, i64, p, p, p,
+                                           p]
+    lib.orc_integrate_adaptive.restype = i64
     return lib
 
 
@@ -142,6 +145,31 @@ def step_method(g: Graph, method, theta0, omega, K, h, nsteps, record_every=1, m
     if rc:
         raise ValueError("orc_step_method failed")
     return th, rt[:nrec]
+
+
+ADAPTIVE_DEFAULTS = dict(h_min=1e-8, h_max=1.0, atol=1e-9, rtol=1e-9, safety=0.9, fac_min=0.2, fac_max=4.0,
+                         max_trials=100000)
+
+
+def integrate_adaptive(g: Graph, theta0, omega, K, t_end, h0, mode="matvec", cap=100000, **ctrl):
+    """Variable-step RK4 with step doubling (reading R25).
+
+    Returns (theta(t_end), t[acc], h[acc], rpsi[acc, 2], n_rejected)."""
+    c = dict(ADAPTIVE_DEFAULTS, **ctrl)
+    th = np.array(theta0, np.float64, copy=True)
+    omega = np.ascontiguousarray(omega, np.float64)
+    t_out = np.zeros(cap)
+    h_out = np.zeros(cap)
+    rp = np.zeros((cap, 2))
+    rej = ctypes.c_int64(0)
+    acc = lib().orc_integrate_adaptive(g._h, _MODES[mode], float(K), float(t_end), float(h0), float(c["h_min"]),
+                                       float(c["h_max"]), float(c["atol"]), float(c["rtol"]), float(c["safety"]),
+                                       float(c["fac_min"]), float(c["fac_max"]), int(c["max_trials"]), _p(th),
+                                       _p(omega), int(cap), _p(t_out), _p(h_out), _p(rp), ctypes.byref(rej))
+    if acc < 0:
+        raise ValueError(f"orc_integrate_adaptive failed ({acc})")
+    k = min(acc, cap)
+    return th, t_out[:k], h_out[:k], rp[:k], int(rej.value)
 
 
 def potential(g: Graph, theta, omega, K):

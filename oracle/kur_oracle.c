@@ -363,6 +363,69 @@ int orc_step_method(const orc_graph *g, int method, int mode, double K, double h
   return 0;
 }
 
+/* Variable-step classical RK4 ("a variable stepsize fourth-order explicit
+ * Runge-Kutta method"; the controller is unstated, reading R25 follows
+ * SPEC S:309): from (t = 0, theta) to t_end.  Each trial step of size
+ * h (h = t_end - t for the last step, i.e. when t + h >= t_end - 1e-12 h) computes y1 = one RK4 step of h and y2 = two RK4 steps
+ * of h/2 (step doubling), the error
+ *     err = sqrt( (1/N) sum_m ((y2_m - y1_m) / (atol + rtol |y2_m|))^2 ) / 15
+ * (the sum sequential in m), accepts iff err <= 1 (theta = y2, t += h), and sets
+ *     h <- clamp(h * min(fac_max, max(fac_min, safety * err^(-1/5))), h_min, h_max)
+ * (factor fac_max when err = 0).  Accepted (t, h, r, psi) are written to the
+ * out arrays (capacity cap).  Returns the number of accepted steps, -1 if a
+ * rejected step had h <= h_min, -2 on a non-finite error, -3 when max_trials
+ * trials did not reach t_end. */
+int64_t orc_integrate_adaptive(const orc_graph *g, int mode, double K, double t_end, double h0, double h_min,
+                               double h_max, double atol, double rtol, double safety, double fac_min, double fac_max,
+                               int64_t max_trials, double *theta, const double *omega, int64_t cap, double *t_out,
+                               double *h_out, double *rpsi_out, int64_t *n_rejected) {
+  const int64_t n = g->n;
+  double *y1 = (double *)malloc(sizeof(double) * (size_t)n);
+  double *y2 = (double *)malloc(sizeof(double) * (size_t)n);
+  double t = 0.0, h = h0;
+  int64_t acc = 0, rej = 0, trials = 0, rc = 0;
+  while (t < t_end) {
+    if (trials++ >= max_trials) { rc = -3; break; }
+    /* the last step lands exactly on t_end (also when t + h misses it by rounding only) */
+    const int last = !(t + h < t_end - 1e-12 * h);
+    const double hs = last ? t_end - t : h;
+    memcpy(y1, theta, sizeof(double) * (size_t)n);
+    orc_rk4(g, mode, K, hs, 1, 0, y1, omega, NULL, NULL);
+    memcpy(y2, theta, sizeof(double) * (size_t)n);
+    orc_rk4(g, mode, K, hs / 2.0, 2, 0, y2, omega, NULL, NULL);
+    double ss = 0.0;
+    for (int64_t m = 0; m < n; ++m) {
+      const double e = (y2[m] - y1[m]) / (atol + rtol * fabs(y2[m]));
+      ss += e * e;
+    }
+    const double err = sqrt(ss / (double)n) / 15.0;
+    if (!isfinite(err)) { rc = -2; break; }
+    if (err <= 1.0) {
+      memcpy(theta, y2, sizeof(double) * (size_t)n);
+      t = last ? t_end : t + hs;
+      if (acc < cap) {
+        if (t_out) t_out[acc] = t;
+        if (h_out) h_out[acc] = hs;
+        if (rpsi_out) orc_order_parameter(n, theta, rpsi_out + 2 * acc);
+      }
+      ++acc;
+    } else {
+      ++rej;
+      if (hs <= h_min) { rc = -1; break; }
+    }
+    double fac = err == 0.0 ? fac_max : safety * pow(err, -0.2);
+    if (fac > fac_max) fac = fac_max;
+    if (fac < fac_min) fac = fac_min;
+    h = hs * fac;
+    if (h > h_max) h = h_max;
+    if (h < h_min) h = h_min;
+  }
+  if (n_rejected) *n_rejected = rej;
+  free(y1);
+  free(y2);
+  return rc ? rc : acc;
+}
+
 /* Potential of the model on a graph (eq. ExtendedPotentialConservation;
  * P:221-233 for the complete graph), evaluated from its definition
  *     V = -sum_m omega_m theta_m + (K/2) sum_{m,l} (A_ml / M_m) (1 - cos(theta_l - theta_m)),
