@@ -59,7 +59,9 @@ typedef enum {
   KUR_ERR_CUDA = 7,            /* a CUDA runtime error (message in kur_last_error) */
   KUR_ERR_NCCL = 8,            /* an NCCL error (message in kur_last_error) */
   KUR_ERR_NONFINITE = 9,       /* a non-finite phase was produced by kur_step (see kur_check) */
-  KUR_ERR_UNSUPPORTED = 10     /* valid request this build does not support (message says why) */
+  KUR_ERR_UNSUPPORTED = 10,    /* valid request this build does not support (message says why) */
+  KUR_ERR_STEPSIZE = 11        /* kur_integrate_adaptive: a step of h_min was rejected, or max_trials
+                                  trials did not reach t_end */
 } kur_status;
 
 /* Segment kinds of the row-segmented adjacency pattern. */
@@ -198,6 +200,35 @@ enum { KUR_RK4 = 0, KUR_EULER = 1, KUR_HEUN = 2, KUR_IMPLICIT_MIDPOINT = 3 };
 kur_status kur_step_method(kur_graph *g, int32_t method, double *theta, const double *omega, double K, double h,
                            int64_t nsteps, int32_t record_every, double *r_trace, double fp_tol,
                            int32_t fp_max_iter, void *stream);
+
+/* Variable-step classical RK4 ("a variable stepsize fourth-order explicit
+ * Runge-Kutta method leads to a reliable result"; the controller is unstated,
+ * DESIGN.md reading R25 follows the SPEC's step doubling).  Integrates theta
+ * in place from t = 0 to t_end.  A trial step of size hs (hs = t_end - t for the
+ * last step, i.e. when t + h >= t_end - 1e-12 h) computes on the device
+ * y1 = one RK4 step of hs and y2 = two RK4 steps of hs/2 from theta, then
+ *     err = sqrt( (1/N) sum_m ((y2_m - y1_m) / (atol + rtol |y2_m|))^2 ) / 15
+ * (per-tile partial sums on the device, added on the host in tile order); the
+ * step is accepted iff err <= 1 (theta = y2, t += hs), and
+ *     h <- clamp(hs * clamp(safety * err^(-1/5), fac_min, fac_max), h_min, h_max)
+ * (factor fac_max when err = 0).  Blocks: the controller runs on the host, one
+ * stream synchronisation per trial.  For each accepted step k < cap the host
+ * arrays t_out[k], h_out[k] and rpsi_out[2k..2k+1] (the order parameter of the
+ * accepted state) are written when non-NULL.  Errors: KUR_ERR_INVALID_ARG (bad
+ * controls), KUR_ERR_STEPSIZE, KUR_ERR_NONFINITE (non-finite error estimate),
+ * KUR_ERR_UNSUPPORTED for world > 1. */
+typedef struct {
+  double t_end;            /* > 0 */
+  double h0;               /* first trial step, > 0 */
+  double h_min, h_max;     /* 0 < h_min <= h_max */
+  double atol, rtol;       /* error weights atol + rtol |y2_m|; >= 0, atol + rtol > 0 */
+  double safety;           /* e.g. 0.9 */
+  double fac_min, fac_max; /* 0 < fac_min <= 1 <= fac_max */
+  int64_t max_trials;      /* >= 1 */
+} kur_adaptive_ctrl;
+kur_status kur_integrate_adaptive(kur_graph *g, double *theta, const double *omega, double K,
+                                  const kur_adaptive_ctrl *ctrl, int64_t cap, double *t_out, double *h_out,
+                                  double *rpsi_out, int64_t *n_accepted, int64_t *n_rejected, void *stream);
 
 /* r_psi[2] = (r, psi) of the complex order parameter r e^{i psi} =
  * (1/N) sum_k e^{i theta_k} (psi = 0 when r = 0).  local (may be

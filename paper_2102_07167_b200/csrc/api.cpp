@@ -111,6 +111,7 @@ const char* kur_status_string(kur_status s) {
     case KUR_ERR_NCCL: return "KUR_ERR_NCCL";
     case KUR_ERR_NONFINITE: return "KUR_ERR_NONFINITE";
     case KUR_ERR_UNSUPPORTED: return "KUR_ERR_UNSUPPORTED";
+    case KUR_ERR_STEPSIZE: return "KUR_ERR_STEPSIZE";
   }
   return "KUR_ERR_UNKNOWN";
 }
@@ -553,6 +554,91 @@ kur_status kur_step_method(kur_graph* g, int32_t method, double* theta, const do
   if (st != KUR_OK) return st;
   return step_impl(gs, {RankIO{theta, omega, nullptr, nullptr, nullptr}}, K, h, nsteps, record_every, {r_trace},
                    (cudaStream_t)stream, method, fp_tol, fp_max_iter);
+}
+
+kur_status kur_integrate_adaptive(kur_graph* g, double* theta, const double* omega, double K,
+                                  const kur_adaptive_ctrl* c, int64_t cap, double* t_out, double* h_out,
+                                  double* rpsi_out, int64_t* n_accepted, int64_t* n_rejected, void* stream) {
+  if (!g || !c) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  if (g->world != 1) return fail(KUR_ERR_UNSUPPORTED, "kur_integrate_adaptive: single-GPU handles only");
+  if (g->n_local > 0 && (!theta || !omega)) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  if (!(c->t_end > 0.0) || !std::isfinite(c->t_end) || !(c->h0 > 0.0) || !(c->h_min > 0.0) ||
+      !(c->h_max >= c->h_min) || !std::isfinite(c->h_max) || !(c->atol >= 0.0) || !(c->rtol >= 0.0) ||
+      !(c->atol + c->rtol > 0.0) || !(c->safety > 0.0) || !(c->fac_min > 0.0) || !(c->fac_min <= 1.0) ||
+      !(c->fac_max >= 1.0) || !std::isfinite(c->fac_max) || c->max_trials < 1 || cap < 0)
+    return fail(KUR_ERR_INVALID_ARG, "kur_integrate_adaptive: invalid controls");
+  if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
+  KUR_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nl = g->n_local;
+  const int nt = g->dp.ntiles;
+  // trial buffers (y1, y2) and the per-tile error partials, owned by this call
+  double *y1 = nullptr, *y2 = nullptr, *tss = nullptr;
+  auto cleanup = [&]() {
+    if (y1) cudaFree(y1);
+    if (y2) cudaFree(y2);
+    if (tss) cudaFree(tss);
+  };
+  const size_t vb = sizeof(double) * (size_t)std::max<int64_t>(nl, 1);
+  cudaError_t e;
+  if ((e = cudaMalloc((void**)&y1, vb)) != cudaSuccess || (e = cudaMalloc((void**)&y2, vb)) != cudaSuccess ||
+      (e = cudaMalloc((void**)&tss, sizeof(double) * (size_t)std::max(nt, 1))) != cudaSuccess) {
+    cleanup();
+    return e == cudaErrorMemoryAllocation ? fail(KUR_ERR_OOM, "kur_integrate_adaptive: out of device memory")
+                                          : cuda_fail(e, "kur_integrate_adaptive");
+  }
+  std::vector<double> hss((size_t)std::max(nt, 1));
+  std::vector<kur_graph*> gs{g};
+  double t = 0.0, h = c->h0, rpsi[2] = {0.0, 0.0};
+  int64_t acc = 0, rej = 0, trials = 0;
+  kur_status st = KUR_OK;
+  auto run = [&]() -> kur_status {
+    while (t < c->t_end) {
+      if (trials++ >= c->max_trials) return fail(KUR_ERR_STEPSIZE, "max_trials reached before t_end");
+      const bool last = !(t + h < c->t_end - 1e-12 * h);  // the last step lands exactly on t_end
+      const double hs = last ? c->t_end - t : h;
+      KUR_CUDA(cudaMemcpyAsync(y1, theta, sizeof(double) * (size_t)nl, cudaMemcpyDeviceToDevice, s));
+      kur_status r = step_impl(gs, {RankIO{y1, omega, nullptr, nullptr, nullptr}}, K, hs, 1, 0, {nullptr}, s);
+      if (r != KUR_OK) return r;
+      KUR_CUDA(cudaMemcpyAsync(y2, theta, sizeof(double) * (size_t)nl, cudaMemcpyDeviceToDevice, s));
+      r = step_impl(gs, {RankIO{y2, omega, nullptr, nullptr, nullptr}}, K, hs / 2.0, 2, 0, {nullptr}, s);
+      if (r != KUR_OK) return r;
+      KUR_CUDA(launch_errnorm(g->dp, y1, y2, c->atol, c->rtol, tss, s));
+      KUR_CUDA(cudaMemcpyAsync(hss.data(), tss, sizeof(double) * (size_t)nt, cudaMemcpyDeviceToHost, s));
+      KUR_CUDA(cudaMemcpyAsync(rpsi, g->ctrl->rpsi, sizeof(rpsi), cudaMemcpyDeviceToHost, s));  // (r, psi) of y2
+      KUR_CUDA(cudaStreamSynchronize(s));
+      double ss = 0.0;
+      for (int i = 0; i < nt; ++i) ss += hss[(size_t)i];  // fixed (tile) order
+      const double err = std::sqrt(ss / (double)g->n) / 15.0;
+      if (!std::isfinite(err)) return fail(KUR_ERR_NONFINITE, "non-finite error estimate in kur_integrate_adaptive");
+      if (err <= 1.0) {
+        KUR_CUDA(cudaMemcpyAsync(theta, y2, sizeof(double) * (size_t)nl, cudaMemcpyDeviceToDevice, s));
+        t = last ? c->t_end : t + hs;
+        if (acc < cap) {
+          if (t_out) t_out[acc] = t;
+          if (h_out) h_out[acc] = hs;
+          if (rpsi_out) {
+            rpsi_out[2 * acc] = rpsi[0];
+            rpsi_out[2 * acc + 1] = rpsi[1];
+          }
+        }
+        ++acc;
+      } else {
+        ++rej;
+        if (hs <= c->h_min) return fail(KUR_ERR_STEPSIZE, "a step of h_min was rejected");
+      }
+      double fac = err == 0.0 ? c->fac_max : c->safety * std::pow(err, -0.2);
+      fac = std::min(c->fac_max, std::max(c->fac_min, fac));
+      h = std::min(c->h_max, std::max(c->h_min, hs * fac));
+    }
+    return KUR_OK;
+  };
+  st = run();
+  cudaStreamSynchronize(s);
+  cleanup();
+  if (n_accepted) *n_accepted = acc;
+  if (n_rejected) *n_rejected = rej;
+  return st;
 }
 
 kur_status kur_order_parameter(kur_graph* g, const double* theta, double* r_psi, double* local, void* stream) {

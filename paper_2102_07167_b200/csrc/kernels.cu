@@ -770,6 +770,23 @@ __global__ void __launch_bounds__(NTHREADS) k_finish(const DevPlan dp, const Sta
   finish_reduce(dp, a);
 }
 
+// Variable-step RK4 (reading R25): per-tile partial of sum_m ((y2 - y1) / (atol + rtol |y2|))^2.
+__global__ void __launch_bounds__(NTHREADS) k_errnorm(const DevPlan dp, const double* __restrict__ y1,
+                                                      const double* __restrict__ y2, double atol, double rtol,
+                                                      double* __restrict__ tile_ss) {
+  __shared__ double2 red[NWARPS];
+  const TileDesc T = dp.tiles[blockIdx.x];
+  double ss = 0.0, dummy = 0.0;
+  for (int lr = threadIdx.x; lr < T.nrows; lr += NTHREADS) {
+    const int li = T.row0 + lr - dp.row_begin;
+    const double b = y2[li];
+    const double e = (b - y1[li]) / (atol + rtol * fabs(b));
+    ss += e * e;
+  }
+  block_sum2(ss, dummy, red);
+  if (threadIdx.x == 0) tile_ss[blockIdx.x] = ss;
+}
+
 __global__ void k_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, double fp_tol) {
   c->fp_tol = fp_tol;
   c->record_every = record_every;
@@ -867,6 +884,13 @@ cudaError_t launch_finish(const DevPlan& dp, const StageArgs& a, cudaStream_t s)
 cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, double fp_tol,
                             cudaStream_t s) {
   k_set_ctrl<<<1, 1, 0, s>>>(c, record_every, nrec_cap, r_trace, fp_tol);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_errnorm(const DevPlan& dp, const double* y1, const double* y2, double atol, double rtol,
+                           double* tile_ss, cudaStream_t s) {
+  if (dp.ntiles <= 0) return cudaSuccess;
+  k_errnorm<<<dp.ntiles, NTHREADS, 0, s>>>(dp, y1, y2, atol, rtol, tile_ss);
   return cudaGetLastError();
 }
 

@@ -107,5 +107,8 @@ cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_t
 cudaError_t launch_permute(const int32_t* perm, int64_t n, const double* in, double* out, int dir,
                            cudaStream_t s);
 size_t stage_smem_bytes(int rows_per_tile);
+// variable-step RK4: tile_ss[t] = sum over tile t's rows of ((y2 - y1) / (atol + rtol |y2|))^2
+cudaError_t launch_errnorm(const DevPlan& dp, const double* y1, const double* y2, double atol, double rtol,
+                           double* tile_ss, cudaStream_t s);
 
 }  // namespace kur

@@ -26,7 +26,7 @@ KUR_ONES, KUR_ZEROS = 0, 1
 USER_TO_INTERNAL, INTERNAL_TO_USER = 0, 1
 STATUS = {0: "KUR_OK", 1: "KUR_ERR_INVALID_ARG", 2: "KUR_ERR_INDEX_RANGE", 3: "KUR_ERR_DUPLICATE_INDEX",
           4: "KUR_ERR_PARTITION", 5: "KUR_ERR_SIZE_MISMATCH", 6: "KUR_ERR_OOM", 7: "KUR_ERR_CUDA",
-          8: "KUR_ERR_NCCL", 9: "KUR_ERR_NONFINITE", 10: "KUR_ERR_UNSUPPORTED"}
+          8: "KUR_ERR_NCCL", 9: "KUR_ERR_NONFINITE", 10: "KUR_ERR_UNSUPPORTED", 11: "KUR_ERR_STEPSIZE"}
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -54,6 +54,11 @@ class GraphInfo(ctypes.Structure):
                 ("reserved0", _i32)]
 
 
+class AdaptiveCtrl(ctypes.Structure):
+    _fields_ = [("t_end", _d), ("h0", _d), ("h_min", _d), ("h_max", _d), ("atol", _d), ("rtol", _d),
+                ("safety", _d), ("fac_min", _d), ("fac_max", _d), ("max_trials", _i64)]
+
+
 _lib.kur_graph_build.argtypes = [ctypes.POINTER(GraphDesc), ctypes.POINTER(DistDesc), _p, ctypes.POINTER(_p)]
 _lib.kur_graph_destroy.argtypes = [_p]
 _lib.kur_graph_info.argtypes = [_p, ctypes.POINTER(GraphInfo)]
@@ -69,6 +74,8 @@ _lib.kur_timing_read.argtypes = [_p, _p]
 _lib.kur_nccl_unique_id.argtypes = [_p]
 _lib.kur_group_rhs.argtypes = [_p, _i32, _p, _p, _d, _p, _p]
 _lib.kur_group_step.argtypes = [_p, _i32, _p, _p, _d, _d, _i64, _i32, _p, _p]
+_lib.kur_integrate_adaptive.argtypes = [_p, _p, _p, _d, ctypes.POINTER(AdaptiveCtrl), _i64, _p, _p, _p,
+                                        ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p]
 _lib.kur_step_method.argtypes = [_p, _i32, _p, _p, _d, _d, _i64, _i32, _p, _d, _i32, _p]
 _lib.kur_group_step_method.argtypes = [_p, _i32, _i32, _p, _p, _d, _d, _i64, _i32, _p, _d, _i32, _p]
 _lib.kur_status_string.restype = ctypes.c_char_p
@@ -77,13 +84,13 @@ _lib.kur_last_error.restype = ctypes.c_char_p
 for _f in ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
            "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id", "kur_timing",
            "kur_timing_read", "kur_group_rhs", "kur_group_step", "kur_potential", "kur_step_method",
-           "kur_group_step_method"):
+           "kur_group_step_method", "kur_integrate_adaptive"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
             "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id",
             "kur_status_string", "kur_last_error", "kur_timing", "kur_timing_read", "kur_group_rhs",
-            "kur_group_step", "kur_potential", "kur_step_method", "kur_group_step_method")
+            "kur_group_step", "kur_potential", "kur_step_method", "kur_group_step_method", "kur_integrate_adaptive")
 METHODS = {"rk4": 0, "euler": 1, "heun": 2, "implicit_midpoint": 3}
 
 
@@ -269,6 +276,28 @@ def step_method(g: Graph, method, theta, omega, K, h, nsteps, record_every=0, r_
     if check:
         _check(_lib.kur_check(g._h, _stream(stream)))
     return r_trace
+
+
+ADAPTIVE_DEFAULTS = dict(h_min=1e-8, h_max=1.0, atol=1e-9, rtol=1e-9, safety=0.9, fac_min=0.2, fac_max=4.0,
+                         max_trials=100000)
+
+
+def integrate_adaptive(g: Graph, theta, omega, K, t_end, h0, cap=100000, stream=None, **ctrl):
+    """kur_integrate_adaptive: variable-step RK4 (step doubling) from t = 0 to t_end, theta in place.
+
+    Returns (t[acc], h[acc], rpsi[acc, 2], n_rejected) as numpy arrays (host)."""
+    c = dict(ADAPTIVE_DEFAULTS, **ctrl)
+    cc = AdaptiveCtrl(t_end=float(t_end), h0=float(h0), h_min=float(c["h_min"]), h_max=float(c["h_max"]),
+                      atol=float(c["atol"]), rtol=float(c["rtol"]), safety=float(c["safety"]),
+                      fac_min=float(c["fac_min"]), fac_max=float(c["fac_max"]), max_trials=int(c["max_trials"]))
+    t_out, h_out, rp = np.zeros(cap), np.zeros(cap), np.zeros((cap, 2))
+    acc, rej = _i64(0), _i64(0)
+    _check(_lib.kur_integrate_adaptive(g._h, _dev_vec(theta, g.n_local, g.device, "theta"),
+                                       _dev_vec(omega, g.n_local, g.device, "omega"), float(K), ctypes.byref(cc),
+                                       int(cap), _np_ptr(t_out), _np_ptr(h_out), _np_ptr(rp), ctypes.byref(acc),
+                                       ctypes.byref(rej), _stream(stream)))
+    k = min(int(acc.value), cap)
+    return t_out[:k], h_out[:k], rp[:k], int(rej.value)
 
 
 def timing(g: Graph, enable: bool):
