@@ -26,7 +26,7 @@ def _gpu(run, method, nsteps, record_every=1, h=None, **kw):
 
 
 def _check(inst, method, nsteps=10, mode="naive", **kw):
-    run = Run(inst, **{k: v for k, v in kw.items() if k in ("dense_threshold", "tile_rows", "hot_min")})
+    run = Run(inst, **{k: v for k, v in kw.items() if k in ("dense_threshold", "tile_rows", "hot_min", "remote_pass")})
     fp = {k: v for k, v in kw.items() if k in ("fp_tol", "fp_max_iter")}
     th, rt = _gpu(run, method, nsteps, **fp)
     th_ref, rt_ref = oracle.step_method(oracle.Graph(inst), method, inst.theta0, inst.omega, inst.K, inst.h, nsteps,
@@ -54,6 +54,14 @@ def test_methods_complete_graph_cfg1(method):
 @pytest.mark.parametrize("method", METHODS)
 def test_methods_cfg3(method):
     _check(kurgen.config(3), method, mode="matvec")
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_methods_with_remote_pass(method):
+    """The separate k_remote pass (forced) under every integrator's stage epilogues."""
+    inst = kurgen.sbm([2500, 1500, 900], np.array([[0.96, 0.004, 0.02], [0.004, 0.9, 0.003],
+                                                    [0.02, 0.003, 0.25]]), 77, K=3.0, h=0.02)
+    _check(inst, method, tile_rows=512, remote_pass=True, hot_min=1024)
 
 
 @pytest.mark.parametrize("iters", [1, 2, 3])

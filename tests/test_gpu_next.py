@@ -14,15 +14,16 @@ from tests.helpers import Run, close, complex_rpsi
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("remote_pass", [None, True])
 @pytest.mark.parametrize("kind", ["ones", "zeros", "random"])
 @pytest.mark.parametrize("thr", [-1.0, 0.0, 1.0])
-def test_degree_scaling_small(kind, thr):
+def test_degree_scaling_small(kind, thr, remote_pass):
     A, labels = kurgen.random_dense(400, 4, seed=44, p_in=0.8, p_out=0.05, symmetric=False)
     np.fill_diagonal(A[:50, :50], 1)  # some stored self-loops (count in the degree, R22)
     A[3] = 0  # zero row (no self-loop either) -> theta' = omega exactly
     inst = kurgen.from_dense(A, labels, kind=kind, seed=9, K=2.0, scaling=1, self_loops=True)
     ref = oracle.rhs(oracle.Graph(inst), inst.theta0, inst.omega, inst.K, mode="naive")
-    got = Run(inst, dense_threshold=thr).rhs()
+    got = Run(inst, dense_threshold=thr, remote_pass=remote_pass, tile_rows=128).rhs()
     ok, err = close(got, ref, abs_tol=1e-13, rel_tol=1e-12)
     assert ok, err
     i3 = int(np.flatnonzero(np.arange(400) == 3)[0])
