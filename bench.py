@@ -225,13 +225,16 @@ def main():
     kur.timing(g, False)
     kur.check(g)
     if world > 1:
-        t = torch.tensor([ms, tm["stage_ms"]], device=dev)
+        t = torch.tensor([ms, tm["stage_ms"], tm["remote_ms"]], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0].item())
         tm["stage_ms"] = float(t[1].item())
+        tm["remote_ms"] = float(t[2].item())
     ms_per_step = ms / args.steps
     rhs_per_s = 4.0 * args.steps / (ms / 1e3)
-    stage_ms = tm["stage_ms"] / max(tm["stage_n"], 1)
+    kstage_ms = tm["stage_ms"] / max(tm["stage_n"], 1)
+    kremote_ms = tm["remote_ms"] / max(tm["stage_n"], 1)
+    stage_ms = kstage_ms + kremote_ms  # one RHS evaluation = [k_remote +] k_stage
 
     # ---- roofline of the dominant kernel (the fused RK stage = one RHS evaluation).
     # Algorithmic bytes per launch = SURVEY.md §8(d)'s per-unit figure: B_rhs = 16 N (z) + 4 n_idx
@@ -250,20 +253,32 @@ def main():
                           "one fused RK4 stage)",
                 "bytes_per_launch": bytes_launch,
                 "bytes_formula": "SURVEY 8(d): 16N z + 4 n_idx + 8N offsets + 8N omega + 24N RK stage",
-                "avg_launch_ms": stage_ms, "stage_share_of_step": tm["stage_ms"] / ms if ms > 0 else None,
+                "avg_launch_ms": stage_ms, "k_stage_ms": kstage_ms, "k_remote_ms": kremote_ms,
+                "stage_share_of_step": (tm["stage_ms"] + tm["remote_ms"]) / ms if ms > 0 else None,
                 "kernel_bytes_per_launch": kernel_bytes,
                 "kernel_bytes_gbs": kernel_bytes / (stage_ms / 1e3) / 1e9,
                 "kernel_bytes_frac": kernel_bytes / (stage_ms / 1e3) / 1e9 / peak,
                 "traffic_gbs": None if traffic is None else traffic / (stage_ms / 1e3) / 1e9}
+    # the bound k_stage actually meets: the L1/shared-memory data pipe: one 16-byte z
+    # read per hot entry from the staged window; nominal 128 B/clk/SM (B300_MICROARCH smem crossbar),
+    # of which tools/mb_lds.cu reaches 99 % with slot ids in registers
+    smem_peak = 128.0 * torch.cuda.get_device_properties(dev).multi_processor_count * (clk.max_mhz or 1965) * 1e6 / 1e9
+    hot_alg, hot_issued = 16.0 * int(info["n_idx_hot"]), 16.0 * int(info["n_slots_hot"])
+    smem_roofline = {"bound": "smem", "kernel": "k_stage", "unit": "GB/s", "peak": smem_peak,
+                     "peak_source": "nominal 128 B/clk/SM x SMs x max SM clock",
+                     "achieved": hot_alg / (kstage_ms / 1e3) / 1e9, "frac": hot_alg / (kstage_ms / 1e3) / 1e9 / smem_peak,
+                     "issued_frac": hot_issued / (kstage_ms / 1e3) / 1e9 / smem_peak,
+                     "bytes_per_launch": hot_alg, "bytes_formula": "16 B per hot (window-staged) entry"}
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        # the API works in internal order: the caller keeps its host vectors in that order
+        # the API works in internal order: the caller keeps its host state in that order.  The
+        # state theta is the step's input and output and travels every step; omega (like the
+        # graph) is a model parameter and stays resident on the device.
         th_hi = th.cpu().pin_memory()
-        om_hi = om.cpu().pin_memory()
         rt_h = torch.empty((2, 2), dtype=torch.float64).pin_memory()
-        kur.step(g, th_hi, om_hi, K, h, 1, 1)  # warm
+        kur.step(g, th_hi, om, K, h, 1, 1)  # warm
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -271,7 +286,7 @@ def main():
         ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ee0.record(stream)
         for _ in range(ne):
-            rt = kur.step(g, th_hi, om_hi, K, h, 1, 1)  # H2D theta+omega, 1 step, D2H theta
+            rt = kur.step(g, th_hi, om, K, h, 1, 1)  # H2D theta, 1 RK4 step, D2H theta and (r, psi)
             rt_h.copy_(rt)
         ee1.record(stream)
         torch.cuda.synchronize()
@@ -280,9 +295,11 @@ def main():
             t = torch.tensor([e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": 4.0 / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * inst.n,
-               "d2h_bytes_per_step": 8 * inst.n + 32 * world, "ms_per_step": e_ms, "steps": ne,
-               "path": "kur.step(host pinned theta, omega): H2D + kur_step(nsteps=1) + D2H theta and r"}
+        nl = int(info["row_end"] - info["row_begin"])
+        e2e = {"value": 4.0 / (e_ms / 1e3), "unit": UNIT,  # global RHS evaluations (strong scaling) "h2d_bytes_per_step": 8 * nl * world,
+               "d2h_bytes_per_step": (8 * nl + 32) * world, "ms_per_step": e_ms, "steps": ne,
+               "path": "kur.step(host pinned theta): H2D theta + kur_step(nsteps=1) + D2H theta and (r, psi); "
+                       "omega and the graph resident (model parameters)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -307,9 +324,10 @@ def main():
             "rk4_steps_per_s": 1e3 / ms_per_step,
             "algorithmic_gbs": achieved,
             "roofline": roofline,
+            "smem_roofline": smem_roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 1 + tm["prologue_n"] + tm["stage_n"] * (2 if info["remote_pass"] else 1)
+            "gpu_launches": 1 + tm["prologue_n"] + tm["stage_n"] + tm["remote_n"]
                             + (2 * (tm["prologue_n"] + tm["stage_n"]) if world > 1 else 0),
             "clocks": clk.result(),
             "host": {"gen_s": gen_s, "build_s": build_s, "nproc": os.cpu_count()},

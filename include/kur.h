@@ -293,11 +293,13 @@ kur_status kur_plan_destroy(kur_plan *p);
 
 /* Per-launch timing for measurement (bench.py): while enabled, kur_step
  * records a CUDA event pair around every kernel it launches, on `stream`.
- * kur_timing_read blocks until the last recorded event, writes out[4] =
- * {total ms of k_prologue launches, their count, total ms of RK-stage
- * launches, their count} and clears the record.  Enabling also clears it. */
+ * kur_timing_read blocks until the last recorded event, writes out[6] =
+ * {total ms of k_prologue launches, their count, total ms of k_stage (fused
+ * RK stage) launches, the RHS evaluations they did, total ms of k_remote
+ * launches (remote-pass plans; one per RHS evaluation), their count} and
+ * clears the record.  Enabling also clears it. */
 kur_status kur_timing(kur_graph *g, int32_t enable);
-kur_status kur_timing_read(kur_graph *g, double *out /* [4] */);
+kur_status kur_timing_read(kur_graph *g, double *out /* [6] */);
 
 /* Creates a 128-byte NCCL unique id (rank 0), to be broadcast by the caller. */
 kur_status kur_nccl_unique_id(void *id128);

@@ -70,7 +70,7 @@ struct kur_graph {
   // optional per-launch CUDA-event timing (kur_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev;        // pool, reused
-  std::vector<std::pair<int, int>> ev_kind;  // per recorded pair: (0 prologue | 1 stage, RHS evaluations)
+  std::vector<std::pair<int, int>> ev_kind;  // per recorded pair: (0 prologue | 1 k_stage | 2 k_remote, RHS evals)
   bool small = false;                 // whole kur_step in one single-CTA launch
   size_t ev_used = 0;
   cudaError_t mark(cudaStream_t s) {  // records the next event of the pool on s
@@ -418,6 +418,13 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
       a.Tin = z_from_A ? g->TA : g->TB;
       a.Tout = z_from_A ? g->TB : g->TA;
     }
+    if (g->timing && mode != PH_PROLOGUE && g->dp.has_remote) {  // time k_remote and k_stage separately
+      KUR_CUDA(g->mark(s));
+      KUR_CUDA(launch_remote(g->dp, a.zin, s));
+      KUR_CUDA(g->mark(s));
+      g->ev_kind.push_back({2, 1});
+      a.no_remote = 1;
+    }
     KUR_CUDA(g->mark(s));
     if (mode == PH_PROLOGUE) KUR_CUDA(launch_prologue(g->dp, a, s));
     else KUR_CUDA(launch_stage(mode, g->dp, a, s));
@@ -720,8 +727,8 @@ kur_status kur_timing(kur_graph* g, int32_t enable) {
 kur_status kur_timing_read(kur_graph* g, double* out) {
   if (!g || !out) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
   KUR_CUDA(cudaSetDevice(g->device));
-  double ms[2] = {0.0, 0.0};
-  int64_t cnt[2] = {0, 0};
+  double ms[3] = {0.0, 0.0, 0.0};
+  int64_t cnt[3] = {0, 0, 0};
   for (size_t i = 0; i < g->ev_kind.size(); ++i) {
     float t = 0.f;
     KUR_CUDA(cudaEventSynchronize(g->ev[2 * i + 1]));
@@ -733,6 +740,8 @@ kur_status kur_timing_read(kur_graph* g, double* out) {
   out[1] = (double)cnt[0];
   out[2] = ms[1];
   out[3] = (double)cnt[1];
+  out[4] = ms[2];
+  out[5] = (double)cnt[2];
   g->ev_used = 0;
   g->ev_kind.clear();
   return KUR_OK;

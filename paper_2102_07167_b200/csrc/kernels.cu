@@ -811,9 +811,8 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  if (dp.has_remote) {
-    k_remote<<<dp.ntiles, NTHREADS, sizeof(double2) * (size_t)dp.rows_per_tile, s>>>(dp, a.zin);
-    cudaError_t e = cudaGetLastError();
+  if (dp.has_remote && !a.no_remote) {
+    cudaError_t e = launch_remote(dp, a.zin, s);
     if (e != cudaSuccess) return e;
   }
   k_stage<MODE><<<dp.ntiles, NTHREADS, dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) : 0, s>>>(dp, a);
@@ -829,6 +828,12 @@ extern "C" int kur_prof_attach(unsigned long long* p) {
 }
 namespace kur {
 #endif
+
+cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s) {
+  if (!dp.has_remote || dp.ntiles <= 0) return cudaSuccess;
+  k_remote<<<dp.ntiles, NTHREADS, sizeof(double2) * (size_t)dp.rows_per_tile, s>>>(dp, zin);
+  return cudaGetLastError();
+}
 
 size_t stage_smem_bytes(int rows_per_tile) { return sizeof(double2) * (size_t)(WZ + 8 + rows_per_tile); }
 

@@ -90,9 +90,12 @@ struct StageArgs {
   const double* commit;   // prologue only: theta = commit (implicit midpoint step completion) or NULL
   int fp_reset;           // the finish clears ctrl->fp_done (implicit midpoint predictor M0)
   int fp_check;           // MODE_MI: tiles publish max |update|, the finish sets ctrl->fp_done
+  int no_remote;          // launch_stage: the caller launched k_remote itself (per-kernel timing)
 };
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
+// k_remote (plans with the remote pass); launch_stage runs it first unless a.no_remote
+cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s);
 cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaStream_t s);
 // world > 1: after the all-gather of the packed buffers (xrecv = world x xstride doubles),
 // z of every non-local row from its exchanged phase, all tile partials; then the
