@@ -295,10 +295,9 @@ def main():
             t = torch.tensor([e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        nl = int(info["row_end"] - info["row_begin"])
         # value: global RHS evaluations per second (strong scaling); bytes: all ranks' copies
-        e2e = {"value": 4.0 / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nl * world,
-               "d2h_bytes_per_step": (8 * nl + 32) * world, "ms_per_step": e_ms, "steps": ne,
+        e2e = {"value": 4.0 / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * inst.n,
+               "d2h_bytes_per_step": 8 * inst.n + 32 * world, "ms_per_step": e_ms, "steps": ne,
                "path": "kur.step(host pinned theta): H2D theta + kur_step(nsteps=1) + D2H theta and (r, psi); "
                        "omega and the graph resident (model parameters)"}
 
