@@ -265,3 +265,48 @@ def test_config5_sampled_rows_and_invariants():
         ok, err = close(th10[z["rows"]], z["theta10"])
         assert ok, err
         assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(z["r_trace"]))) <= R_TOL
+
+
+# ---------------------------------------------------------------- full configured trajectories
+def test_config2_full_trajectory_r_every_10():
+    """cfg2 as configured: 1000 RK4 steps, r(t) every 10 steps (101 samples), against the
+    oracle's order-parameter form; theta after 1000 steps."""
+    inst = kurgen.config(2)
+    og = oracle.Graph(inst)
+    run = Run(inst)
+    th_ref, _, rt_ref = oracle.rk4(og, inst.theta0, inst.omega, inst.K, inst.h, inst.nsteps, inst.record_every,
+                                   mode="op")
+    th, rt = run.step(inst.nsteps, inst.record_every)
+    assert rt.shape == (101, 2)
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(rt_ref))) <= R_TOL
+    ok, err = close(th, th_ref)
+    assert ok, err
+
+
+def test_config3_full_trajectory():
+    """cfg3 as configured: 200 RK4 steps of h = 0.005 against the oracle (P:443 form, O(nnz))."""
+    inst = kurgen.config(3)
+    og = oracle.Graph(inst)
+    run = Run(inst)
+    th_ref, _, rt_ref = oracle.rk4(og, inst.theta0, inst.omega, inst.K, inst.h, inst.nsteps, 1, mode="matvec")
+    th, rt = run.step(inst.nsteps, 1)
+    assert rt.shape == (inst.nsteps + 1, 2)
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(rt_ref))) <= R_TOL
+    ok, err = close(th, th_ref)
+    assert ok, err
+
+
+def test_config4_full_trajectory_golden():
+    """cfg4 as configured (200 steps): the committed oracle trajectory sample (if present,
+    tools/make_golden.py 4) — theta on sampled rows after 200 steps and r e^{i psi} at every step."""
+    gold = os.path.join(GOLDEN, "cfg4_oracle_trajectory.npz")
+    if not os.path.exists(gold):
+        pytest.skip("tests/golden/cfg4_oracle_trajectory.npz not generated")
+    inst = kurgen.config(4)
+    z = np.load(gold)
+    assert str(z["sha256"]) == inst.sha256()
+    run = Run(inst)
+    th, rt = run.step(int(z["nsteps"]), 1)
+    ok, err = close(th[z["rows"]], z["theta_final"])
+    assert ok, err
+    assert np.max(np.abs(complex_rpsi(rt) - complex_rpsi(z["r_trace"]))) <= R_TOL
