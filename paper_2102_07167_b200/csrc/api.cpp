@@ -67,6 +67,10 @@ struct kur_graph {
   int32_t *d_shard_row0 = nullptr, *d_shard_tile0 = nullptr;
   double *d_rowscale = nullptr, *d_potc = nullptr;
   double *xsend = nullptr, *xrecv = nullptr;  // world > 1: packed exchange buffers
+  double2* Wh = nullptr;                      // world > 1: phase-A row sums
+  cudaStream_t comm_stream = nullptr;         // NCCL: exchange + unpack + finish, overlapping phase A
+  cudaEvent_t ev_b = nullptr, ev_exch = nullptr;
+  bool exch_pending = false;                  // comm_stream holds an exchange the next phase B waits for
   // optional per-launch CUDA-event timing (kur_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev;        // pool, reused
@@ -88,11 +92,15 @@ struct kur_graph {
     cudaSetDevice(device);
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
-                    xsend, xrecv, d_rowscale, d_potc, pmax, Wr};
+                    xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (comm_stream) cudaStreamSynchronize(comm_stream);
     if (comm) ncclCommDestroy(comm);
+    if (ev_b) cudaEventDestroy(ev_b);
+    if (ev_exch) cudaEventDestroy(ev_exch);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
   }
 };
 
@@ -230,6 +238,8 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
     if ((e = cudaMalloc((void**)&g->xrecv, sizeof(double) * (size_t)xstride * (size_t)world)) != cudaSuccess)
       return bail(e, "xrecv");
     if ((e = cudaMemset(g->xsend, 0, sizeof(double) * (size_t)xstride)) != cudaSuccess) return bail(e, "xsend");
+    if ((e = cudaMalloc((void**)&g->Wh, sizeof(double2) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess)
+      return bail(e, "Wh");
     if (dist && dist->nccl_id) {
       ncclUniqueId id;
       std::memcpy(&id, dist->nccl_id, sizeof(id));
@@ -238,6 +248,12 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
         delete g;
         return fail(KUR_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(nr));
       }
+      int lo = 0, hi = 0;  // the exchange stream gets the highest priority: its few CTAs jump the queue
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if ((e = cudaStreamCreateWithPriority(&g->comm_stream, cudaStreamNonBlocking, hi)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&g->ev_exch, cudaEventDisableTiming)) != cudaSuccess)
+        return bail(e, "exchange stream");
     }
   }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "build sync");
@@ -418,6 +434,30 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
       a.Tin = z_from_A ? g->TA : g->TB;
       a.Tout = z_from_A ? g->TB : g->TA;
     }
+    a.Wh = g->Wh;
+  }
+  if (world > 1 && mode != PH_PROLOGUE) {
+    // phase A: own-community hot parts (local z only) -> Wh, while the previous stage's
+    // exchange may still be running on the exchange stream
+    for (size_t r = 0; r < gs.size(); ++r) {
+      kur_graph* g = gs[r];
+      StageArgs& a = args[r];
+      a.phase = PHASE_A;
+      KUR_CUDA(g->mark(s));
+      KUR_CUDA(launch_stage(mode, g->dp, a, s));
+      KUR_CUDA(g->mark(s));
+      if (g->timing) g->ev_kind.push_back({1, 0});
+      a.phase = PHASE_B;
+    }
+    for (kur_graph* g : gs)
+      if (g->exch_pending) {  // phase B needs the other ranks' z and the new block sums
+        KUR_CUDA(cudaStreamWaitEvent(s, g->ev_exch, 0));
+        g->exch_pending = false;
+      }
+  }
+  for (size_t r = 0; r < gs.size(); ++r) {
+    kur_graph* g = gs[r];
+    StageArgs& a = args[r];
     if (g->timing && mode != PH_PROLOGUE && g->dp.has_remote) {  // time k_remote and k_stage separately
       KUR_CUDA(g->mark(s));
       KUR_CUDA(launch_remote(g->dp, a.zin, s));
@@ -432,12 +472,36 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
     if (g->timing) g->ev_kind.push_back({mode == PH_PROLOGUE ? 0 : 1, mode == PH_PROLOGUE ? 0 : 1});
   }
   if (world == 1 || mode == MODE_RHS) return KUR_OK;
-  kur_status st = exchange(gs, s);
+  kur_graph* g0 = gs[0];
+  // NCCL: the exchange, unpack and fixed-order finish run on the exchange stream, so the next
+  // phase A overlaps them; the prologue (no phase A follows it on its own) is joined at once.
+  const bool async = g0->comm != nullptr;
+  cudaStream_t xs = async ? g0->comm_stream : s;
+  if (async) {
+    KUR_CUDA(cudaEventRecord(g0->ev_b, s));
+    KUR_CUDA(cudaStreamWaitEvent(xs, g0->ev_b, 0));
+  }
+  kur_status st = exchange(gs, xs);
   if (st != KUR_OK) return st;
   for (size_t r = 0; r < gs.size(); ++r) {
-    KUR_CUDA(launch_unpack(gs[r]->dp, gs[r]->xrecv, args[r].zout, s));
-    KUR_CUDA(launch_finish(gs[r]->dp, args[r], s));
+    KUR_CUDA(launch_unpack(gs[r]->dp, gs[r]->xrecv, args[r].zout, xs));
+    KUR_CUDA(launch_finish(gs[r]->dp, args[r], xs));
   }
+  if (async) {
+    KUR_CUDA(cudaEventRecord(g0->ev_exch, xs));
+    if (mode == PH_PROLOGUE) KUR_CUDA(cudaStreamWaitEvent(s, g0->ev_exch, 0));
+    else g0->exch_pending = true;
+  }
+  return KUR_OK;
+}
+
+// The caller's stream waits for an exchange still in flight (end of kur_step and friends).
+kur_status join_exchange(const std::vector<kur_graph*>& gs, cudaStream_t s) {
+  for (kur_graph* g : gs)
+    if (g->exch_pending) {
+      KUR_CUDA(cudaStreamWaitEvent(s, g->ev_exch, 0));
+      g->exch_pending = false;
+    }
   return KUR_OK;
 }
 
@@ -526,6 +590,7 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
         break;
     }
   }
+  if (st == KUR_OK) st = join_exchange(gs, s);
   return st;
 }
 
@@ -859,6 +924,7 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
           for (uint32_t pos = 0; pos < 4 * cd.ng; ++pos) {
             {
               int64_t col;
+              int8_t eneg = (int8_t)(pd.neg & 1);
               if (hot) {
                 const uint32_t e = hot_slot(cd, l, pos);
                 if (e >= HOT_SENT && e < HOT_SENT + 8) continue;
@@ -867,11 +933,12 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
               } else {
                 const uint32_t e = P.pool[(size_t)cd.ofs + HDR_UNITS + (size_t)(pos / 4) * 32 + (size_t)l].w[pos % 4];
                 if (e == (uint32_t)P.n) continue;
-                col = e;
+                col = e & 0x7FFFFFFFu;  // bit 31: complement entry (subtracted)
+                eneg = (int8_t)(e >> 31);
               }
               if (lr == EMPTY_LANE) return fail(KUR_ERR_INVALID_ARG, "plan: entry in an empty lane");
               if (col < 0 || col >= P.n) return fail(KUR_ERR_INVALID_ARG, "plan: column out of range");
-              ents.push_back(E{(int32_t)(T.row0 + lr - P.row_begin), (int32_t)col, (int8_t)(pd.neg & 1)});
+              ents.push_back(E{(int32_t)(T.row0 + lr - P.row_begin), (int32_t)col, eneg});
             }
           }
         }

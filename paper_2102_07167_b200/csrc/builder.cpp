@@ -597,7 +597,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     std::vector<Unit> units;
     std::vector<PartDesc> parts;    // chunk0 relative to the tile
     std::vector<ChunkDesc> chunks;  // ofs relative to the tile
-    int32_t nhot = 0;
+    int32_t nhot = 0, nown = 0;
     int64_t hot = 0, rem = 0, shot = 0, srem = 0, loads = 0;
   };
   std::vector<TileOut> outs((size_t)nt);
@@ -742,7 +742,8 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
                   const int p = (int)g * 4 + e;
                   uint32_t v = SENT_REMOTE;
                   const int32_t ri = lane_row[(size_t)lane];
-                  if (ri >= 0 && p < cnt[(size_t)ri]) v = (uint32_t)(src[k0 + (size_t)rb[(size_t)ri] + (size_t)p] & COLM);
+                  // remote entries keep their sign in bit 31 (1 = complement entry, subtracted)
+                  if (ri >= 0 && p < cnt[(size_t)ri]) v = (uint32_t)(src[k0 + (size_t)rb[(size_t)ri] + (size_t)p] & 0xFFFFFFFFULL);
                   U.w[e] = v;
                 }
               }
@@ -767,17 +768,26 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
           if (m > i) { emit_part((int32_t)w, 0, keys.data(), i, m); O.nhot++; }
           if (j > m) { emit_part((int32_t)w, 1, keys.data(), m, j); O.nhot++; }
           if ((int32_t)w != last_w) { O.loads++; last_w = (int32_t)w; }
-        } else {
-          for (size_t k = i; k < j; ++k) remk.push_back(keys[k] & ((1ULL << 44) - 1));
+        } else {  // remote: (row, sign in bit 31, column) -> one part per tile with per-entry signs
+          for (size_t k = i; k < j; ++k)
+            remk.push_back((keys[k] & (0x7FFULL << 32)) | (((keys[k] >> 43) & 1) << 31) | (keys[k] & COLM));
         }
         i = j;
       }
+      // canonical part order (partition independent): hot windows lying wholly
+      // inside the tile's own community first (always local to the rank), then the other hot
+      // windows in column order, then the single remote part
+      {
+        const int64_t c0 = S.moff[(size_t)T.comm], c1 = S.moff[(size_t)T.comm + 1];
+        auto own = [&](const PartDesc& pd) {
+          return (int64_t)pd.window * WZ >= c0 && (int64_t)(pd.window + 1) * WZ <= c1;
+        };
+        std::stable_partition(O.parts.begin(), O.parts.end(), own);
+        O.nown = (int32_t)std::count_if(O.parts.begin(), O.parts.end(), own);
+      }
       if (!remk.empty()) {
-        std::sort(remk.begin(), remk.end());  // (sign, row, column)
-        size_t m = 0;
-        while (m < remk.size() && !((remk[m] >> 43) & 1)) ++m;
-        if (m > 0) emit_part(-1, 0, remk.data(), 0, m);
-        if (remk.size() > m) emit_part(-1, 1, remk.data(), m, remk.size());
+        std::sort(remk.begin(), remk.end());  // (row, sign, column)
+        emit_part(-1, 0, remk.data(), 0, remk.size());
       }
     }
   }
@@ -805,6 +815,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     T.part0 = (int32_t)po;
     T.nparts = (int32_t)O.parts.size();
     T.nhot = O.nhot;
+    T.nown = O.nown;
     P.tiles[(size_t)lt] = T;
     uo += (int64_t)O.units.size();
     po += (int64_t)O.parts.size();

@@ -180,13 +180,21 @@ __device__ __forceinline__ double2 ldz(const double2* p) {
   return COHERENT ? __ldcg(p) : __ldg(p);
 }
 
+// Remote entry id: column in bits 0-30, bit 31 set for a complement entry (subtracted,
+// P:562-570), clear for a non-zero entry (added).  Negation is exact.
+template <bool COHERENT>
+__device__ __forceinline__ double2 ldz_signed(const double2* __restrict__ z, uint32_t id) {
+  const double2 v = ldz<COHERENT>(z + (id & 0x7FFFFFFFu));
+  return (id >> 31) ? make_double2(-v.x, -v.y) : v;
+}
+
 template <bool COHERENT>
 __device__ __forceinline__ void rem4(const uint4 v, const double2* __restrict__ z, double& x0,
                                      double& y0, double& x1, double& y1) {
-  const double2 a = ldz<COHERENT>(z + v.x);
-  const double2 b = ldz<COHERENT>(z + v.y);
-  const double2 c = ldz<COHERENT>(z + v.z);
-  const double2 d = ldz<COHERENT>(z + v.w);
+  const double2 a = ldz_signed<COHERENT>(z, v.x);
+  const double2 b = ldz_signed<COHERENT>(z, v.y);
+  const double2 c = ldz_signed<COHERENT>(z, v.z);
+  const double2 d = ldz_signed<COHERENT>(z, v.w);
   x0 += a.x;
   y0 += a.y;
   x1 += b.x;
@@ -273,8 +281,10 @@ __device__ __forceinline__ void run_remote_deep(const uint4* __restrict__ q, uin
     const uint4* qn = q + (size_t)(g + 2) * 32;
     b0 = g + 2 < ng ? ldg_stream(qn, pol) : s4;
     b1 = g + 3 < ng ? ldg_stream(qn + 32, pol) : s4;
-    const double2 a0 = __ldg(z + c0.x), a1 = __ldg(z + c0.y), a2 = __ldg(z + c0.z), a3 = __ldg(z + c0.w);
-    const double2 a4 = __ldg(z + c1.x), a5 = __ldg(z + c1.y), a6 = __ldg(z + c1.z), a7 = __ldg(z + c1.w);
+    const double2 a0 = ldz_signed<false>(z, c0.x), a1 = ldz_signed<false>(z, c0.y);
+    const double2 a2 = ldz_signed<false>(z, c0.z), a3 = ldz_signed<false>(z, c0.w);
+    const double2 a4 = ldz_signed<false>(z, c1.x), a5 = ldz_signed<false>(z, c1.y);
+    const double2 a6 = ldz_signed<false>(z, c1.z), a7 = ldz_signed<false>(z, c1.w);
     x0 += a0.x; y0 += a0.y; x1 += a1.x; y1 += a1.y;
     x0 += a2.x; y0 += a2.y; x1 += a3.x; y1 += a3.y;
     x0 += a4.x; y0 += a4.y; x1 += a5.x; y1 += a5.y;
@@ -494,12 +504,16 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
                                            double& dmax) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool parts = dp.has_parts;
-  // remote parts of the tile were summed by k_remote into Wr (SMALL: inline, below)
-  const bool split = !SMALL && dp.has_remote;  // small plans (k_small, or kur_rhs on them) stay inline
-  const bool pre = split && T.nparts > T.nhot;
+  // the remote part of the tile was summed by k_remote into Wr (added in the finalize);
+  // small plans (k_small, or kur_rhs on them) keep it inline
+  const bool split = !SMALL && dp.has_remote;
+  const bool addr = split && T.nparts > T.nhot && a.phase != PHASE_A;
+  // world > 1: phase A sums the own-community hot parts (local z only) into Wh while the
+  // previous stage's exchange is in flight; phase B continues from Wh (exact copy)
+  const bool from_wh = !SMALL && a.phase == PHASE_B && T.nown > 0;
   if (parts) {
     for (int r = tid; r < T.nrows; r += NTHREADS)
-      Ws[r] = pre ? __ldcg(dp.Wr + (T.row0 - dp.row_begin) + r) : make_double2(0.0, 0.0);
+      Ws[r] = from_wh ? __ldcg(a.Wh + (T.row0 - dp.row_begin) + r) : make_double2(0.0, 0.0);
     __syncthreads();
   }
   // ---- parts: hot ones gather from the staged window, remote ones from global memory
@@ -512,22 +526,23 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     g_prof[(size_t)blockIdx.x * PROF_STRIDE + 28] = (unsigned long long)T.nparts;
   }
 #endif
-  // Order: remote parts first (when inline), then the hot parts in window order,
-  // so W_j accumulates in the same sequence whether the remote parts run here or
-  // in k_remote (Ws then starts from Wr): bitwise identical results either way.
-  // The first hot window's TMA copy is issued up front and overlaps the remote parts.
+  // Canonical order (builder): own-community hot windows, other hot windows, then the
+  // single remote part (inline) — or its k_remote row sum Wr added in the finalize: one
+  // addition per row either way, so both modes and every world size are bitwise identical.
   const int nrem = split ? 0 : T.nparts - T.nhot;
+  const int pbeg = (!SMALL && a.phase == PHASE_B) ? T.nown : 0;
+  const int pend = (!SMALL && a.phase == PHASE_A) ? T.nown : T.nhot + nrem;
   bool pending = false;
 #ifdef KUR_PROFILE
   if (!SMALL && g_prof && tid == 0) g_prof[(size_t)blockIdx.x * PROF_STRIDE + 29] = (unsigned long long)nrem;
 #endif
-  if (T.nhot > 0) {
-    loaded = dp.parts[T.part0].window;
+  if (pbeg < T.nhot && pbeg < pend) {
+    loaded = dp.parts[T.part0 + pbeg].window;
     pending = true;
     if (tid == 0) tma_load_1d(zs, a.zin + (size_t)loaded * WZ, WZ * sizeof(double2), bar);
   }
-  for (int pi = 0; pi < nrem + T.nhot; ++pi) {
-    const int p = pi < nrem ? T.part0 + T.nhot + pi : T.part0 + (pi - nrem);
+  for (int pi = pbeg; pi < pend; ++pi) {
+    const int p = T.part0 + pi;
     const PartDesc P = dp.parts[p];
     const bool hot = P.window >= 0;
     if (!SMALL && pi < 8) PROF_T(1 + 3 * pi);
@@ -545,6 +560,11 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     if (!SMALL && pi < 8) PROF_T(3 + 3 * pi);
   }
   if (!SMALL) PROF_T(25);
+  if (!SMALL && a.phase == PHASE_A) {  // hand the own-community sums to phase B
+    for (int r = tid; r < T.nrows; r += NTHREADS) a.Wh[(T.row0 - dp.row_begin) + r] = Ws[r];
+    px = py = dmax = 0.0;
+    return false;
+  }
 
   // ---- finalize: k_j = omega_j + (K/N) Im(conj z_j W_j), fused RK4 stage
   const double2 Tc = __ldcg(a.Tin + T.comm);
@@ -555,7 +575,12 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   for (int lr = tid; lr < T.nrows; lr += NTHREADS) {
     const int row = T.row0 + lr;
     const int li = row - dp.row_begin;
-    const double2 w = parts ? Ws[lr] : make_double2(0.0, 0.0);
+    double2 w = parts ? Ws[lr] : make_double2(0.0, 0.0);
+    if (addr) {
+      const double2 r = __ldcg(dp.Wr + li);
+      w.x += r.x;
+      w.y += r.y;
+    }
     const double wx = Tc.x + w.x, wy = Tc.y + w.y;
     const double2 zj = SMALL ? __ldcg(a.zin + row) : a.zin[row];
     // K/M_m: uniform K/N, or K/deg_m for the degree scaling
@@ -653,9 +678,12 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __shared__ int s_nonfinite;
   const int tid = threadIdx.x;
   // implicit midpoint: iterations after convergence are no-ops (uniform: every CTA reads the same flag)
-  if (MODE == MODE_MI && *(volatile const int*)&dp.ctrl->fp_done) return;
+  // (phase A never skips: it may run before the finish that sets or clears the flag, and
+  // phase B, which does check it, then reads Wh)
+  if (MODE == MODE_MI && a.phase != PHASE_A && *(volatile const int*)&dp.ctrl->fp_done) return;
   const int lt = dp.order[blockIdx.x];
   const TileDesc T = dp.tiles[lt];
+  if (a.phase == PHASE_A && T.nown == 0) return;  // nothing local to pre-sum (phase B starts from 0)
   if (dp.has_parts && tid < 8) zs[WZ + tid] = make_double2(0.0, 0.0);
   if (tid == 0) {
     s_nonfinite = 0;
@@ -665,7 +693,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   uint32_t phase = 0;
   double px, py, dmax;
   const bool bad = stage_rows<MODE, false>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax);
-  if (MODE == MODE_RHS) return;
+  if (MODE == MODE_RHS || a.phase == PHASE_A) return;
   constexpr bool FINAL = MODE == MODE_S4 || MODE == MODE_E1 || MODE == MODE_H2;
   if (FINAL && bad) s_nonfinite = 1;
   __syncthreads();
@@ -811,7 +839,7 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  if (dp.has_remote && !a.no_remote) {
+  if (dp.has_remote && !a.no_remote && a.phase != PHASE_A) {
     cudaError_t e = launch_remote(dp, a.zin, s);
     if (e != cudaSuccess) return e;
   }

@@ -69,6 +69,7 @@ enum StageMode {
   MODE_E1 = 6, MODE_H1 = 7, MODE_H2 = 8, MODE_M0 = 9, MODE_MI = 10
 };
 enum RecordMode { REC_NONE = 0, REC_START = 1, REC_STEP = 2 };
+enum StagePhase { PHASE_FULL = 0, PHASE_A = 1, PHASE_B = 2 };
 
 struct StageArgs {
   double* theta;          // local rows: theta (prologue/RHS) or theta_n (RK stages; S4 writes theta_{n+1})
@@ -91,6 +92,9 @@ struct StageArgs {
   int fp_reset;           // the finish clears ctrl->fp_done (implicit midpoint predictor M0)
   int fp_check;           // MODE_MI: tiles publish max |update|, the finish sets ctrl->fp_done
   int no_remote;          // launch_stage: the caller launched k_remote itself (per-kernel timing)
+  int phase;              // PHASE_FULL, or world > 1: PHASE_A (own-community hot parts -> Wh, overlaps
+                          // the previous exchange) / PHASE_B (Wh + the rest of the tile, finalize)
+  double2* Wh;            // [local rows] phase-A row sums (world > 1)
 };
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);

@@ -59,12 +59,14 @@ struct TileDesc {   // 32 bytes; device array
   int32_t part0;    // first part of the tile
   int32_t nparts;   // hot parts first (by window), then remote parts
   int32_t nhot;     // number of hot parts
-  int32_t pad0, pad1;
+  int32_t nown;     // of which the first nown lie wholly inside the tile's own community
+  int32_t pad1;
 };
 
 struct PartDesc {   // 16 bytes; device array
   int32_t window;   // window id (hot) or -1 (remote)
-  int32_t neg;      // 1: complement entries (subtracted), 0: non-zero entries (added)
+  int32_t neg;      // hot: 1 complement entries (subtracted), 0 non-zero entries (added), bits 8+: row
+                    // pieces; remote (one part per tile): 0, the sign is per entry (bit 31 of the id)
   uint32_t chunk0;  // first chunk in the chunk table
   uint32_t nchunks;
 };

@@ -50,7 +50,7 @@ def main():
             wb, we, pe = P[t, 1 + 3 * p], P[t, 2 + 3 * p], P[t, 3 + 3 * p]
             wf = P[t, 32 + 16 * p: 48 + 16 * p]
             wait[t] += we - wb
-            (rem if p < nrem[t] else hot)[t] += pe - we  # inline remote parts run first
+            (hot if p < nhot[t] else rem)[t] += pe - we  # the inline remote part runs last
             imb[t] += pe - wf.mean()
     fin = t26 - t25
     print(f"cfg{args.config}: {nt} tiles, rows/tile {g.info['rows_per_tile']}, parts/tile {nparts.mean():.2f} "
