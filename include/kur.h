@@ -290,6 +290,11 @@ kur_status kur_plan_sizes(const kur_plan *p, int64_t *sizes /* [16] */);
 kur_status kur_plan_export(const kur_plan *p, int32_t *perm, int32_t *D_ptr, int32_t *D_idx, int64_t *row_ptr,
                            int32_t *cols, int8_t *neg, int32_t *shard_row0);
 kur_status kur_plan_destroy(kur_plan *p);
+/* Tile and part structure of the plan (host): tiles[n_tiles][6] = {row0 (internal), nrows,
+ * community, nparts, nhot, nown}: the tile's parts are its nown own-community hot windows,
+ * then nhot - nown other hot windows, then at most one remote part;
+ * part_window[sum nparts] = window id of each part in that order (-1 = remote), or NULL. */
+kur_status kur_plan_tiles(const kur_plan *p, int32_t *tiles, int32_t *part_window);
 
 /* Per-launch timing for measurement (bench.py): while enabled, kur_step
  * records a CUDA event pair around every kernel it launches, on `stream`.

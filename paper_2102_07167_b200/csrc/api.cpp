@@ -969,6 +969,20 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
   return KUR_OK;
 }
 
+kur_status kur_plan_tiles(const kur_plan* p, int32_t* tiles, int32_t* part_window) {
+  if (!p || !tiles) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  const HostPlan& P = p->P;
+  size_t k = 0;
+  for (size_t t = 0; t < P.tiles.size(); ++t) {
+    const TileDesc& T = P.tiles[t];
+    const int32_t v[6] = {T.row0, T.nrows, T.comm, T.nparts, T.nhot, T.nown};
+    std::memcpy(tiles + 6 * t, v, sizeof(v));
+    if (part_window)
+      for (int32_t q = 0; q < T.nparts; ++q) part_window[k++] = P.parts[(size_t)(T.part0 + q)].window;
+  }
+  return KUR_OK;
+}
+
 kur_status kur_plan_destroy(kur_plan* p) {
   delete p;
   return KUR_OK;

@@ -393,9 +393,10 @@ _lib.kur_plan_build.argtypes = [ctypes.POINTER(GraphDesc), _i32, _i32, _i32, cty
 _lib.kur_plan_sizes.argtypes = [_p, _p]
 _lib.kur_plan_export.argtypes = [_p] + [_p] * 7
 _lib.kur_plan_destroy.argtypes = [_p]
-for _f in ("kur_plan_build", "kur_plan_sizes", "kur_plan_export", "kur_plan_destroy"):
+_lib.kur_plan_tiles.argtypes = [_p, _p, _p]
+for _f in ("kur_plan_build", "kur_plan_sizes", "kur_plan_export", "kur_plan_destroy", "kur_plan_tiles"):
     getattr(_lib, _f).restype = ctypes.c_int
-EXPORTED = EXPORTED + ("kur_plan_build", "kur_plan_sizes", "kur_plan_export", "kur_plan_destroy")
+EXPORTED = EXPORTED + ("kur_plan_build", "kur_plan_sizes", "kur_plan_export", "kur_plan_destroy", "kur_plan_tiles")
 
 
 def _desc_from(inst, dense_threshold=-1.0, hot_min=0, tile_rows=0):
@@ -437,6 +438,12 @@ def plan_export(inst, *, rank=0, world=1, sm_count=148, dense_threshold=-1.0, ho
         _check(_lib.kur_plan_sizes(h, _np_ptr(sz)))
         out.update(conflicts=int(sz[10]), slots_hot=int(sz[11]), idx_hot=int(sz[12]), slots_remote=int(sz[13]),
                    idx_remote=int(sz[14]), window_loads=int(sz[15]))
+        tiles = np.zeros((max(nt, 1), 6), np.int32)
+        _check(_lib.kur_plan_tiles(h, ctypes.c_void_p(tiles.ctypes.data), None))
+        pw = np.zeros(max(int(tiles[:nt, 3].sum()), 1), np.int32)
+        _check(_lib.kur_plan_tiles(h, ctypes.c_void_p(tiles.ctypes.data), ctypes.c_void_p(pw.ctypes.data)))
+        out["tiles"] = tiles[:nt]
+        out["part_window"] = pw[:int(tiles[:nt, 3].sum())]
         return out
     finally:
         _lib.kur_plan_destroy(h)

@@ -237,3 +237,29 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     assert set(kur.EXPORTED) <= names
     assert kur._lib.kur_status_string(9) == b"KUR_ERR_NONFINITE"
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_canonical_part_order(world):
+    """per tile, the nown own-community hot windows first (each lying wholly inside
+    the tile's community — local at any world size), then the other hot windows, then at most
+    one remote part; the order does not depend on the partition into ranks."""
+    sizes = [5000, 4096, 700, 9000, 33]
+    inst = kurgen.sbm(sizes, np.array(
+        [[0.97, 0.002, 0.6, 0.0, 0.1], [0.002, 0.9, 0.0, 0.001, 0.0], [0.6, 0.0, 0.98, 0.0, 0.0],
+         [0.0, 0.001, 0.0, 0.95, 0.02], [0.1, 0.0, 0.0, 0.02, 0.5]]), 31)
+    out = kur.plan_export(inst, world=world, rank=world - 1, tile_rows=512)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    k = 0
+    seen_remote_first = False
+    for row0, nrows, comm, nparts, nhot, nown in out["tiles"]:
+        w = out["part_window"][k:k + nparts]
+        k += nparts
+        assert 0 <= nown <= nhot <= nparts <= nhot + 1
+        assert np.all(w[:nhot] >= 0) and np.all(w[nhot:] == -1)
+        for q in range(nhot):
+            inside = w[q] * 4096 >= off[comm] and (w[q] + 1) * 4096 <= off[comm + 1]
+            assert inside == (q < nown), (comm, q, w[q])
+        seen_remote_first |= nparts > nhot
+    assert seen_remote_first  # the instance exercises the remote part
+    assert any(t[5] > 0 for t in out["tiles"]) and any(t[4] > t[5] for t in out["tiles"])
