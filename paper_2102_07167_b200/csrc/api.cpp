@@ -61,6 +61,8 @@ struct kur_graph {
   double* acc = nullptr;
   double* pmax = nullptr;
   double2* Wr = nullptr;
+  uint32_t* d_rchunks = nullptr;
+  uint8_t* d_rem_lp = nullptr;
   Ctrl* ctrl = nullptr;
   ncclComm_t comm = nullptr;
   int world = 1;
@@ -92,7 +94,7 @@ struct kur_graph {
     cudaSetDevice(device);
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
-                    xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh};
+                    xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh, d_rchunks, d_rem_lp};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -275,11 +277,17 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
     if (T.nparts > 0) dp.has_parts = 1;
     if (T.nparts > T.nhot && P.split_remote) dp.has_remote = 1;
   }
-  if (dp.has_remote) {
-    if ((e = cudaMalloc((void**)&g->Wr, sizeof(double2) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess)
+  if (dp.has_remote) {  // rows without remote entries keep Wr = 0 for good
+    if ((e = cudaMalloc((void**)&g->Wr, sizeof(double2) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess ||
+        (e = cudaMemset(g->Wr, 0, sizeof(double2) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess)
       return bail(e, "Wr");
+    if ((e = upload(&g->d_rchunks, P.rchunks)) != cudaSuccess) return bail(e, "rchunks");
+    if ((e = upload(&g->d_rem_lp, P.rem_lp)) != cudaSuccess) return bail(e, "rem_lp");
   }
   dp.Wr = g->Wr;
+  dp.rchunks = g->d_rchunks;
+  dp.rem_lp = g->d_rem_lp;
+  dp.n_rchunks = (int32_t)(P.rem_lp.size());
   // tiny graphs run a whole trajectory in one CTA (launch latency dominates otherwise)
   g->small = P.small;
   dp.shard_row0 = g->d_shard_row0;

@@ -829,8 +829,8 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   }
   // Remote parts (global z gathers, ~1 L1 wavefront each) are summed by a separate
   // k_remote pass before k_stage when they are numerous and concentrated: then the
-  // latency-bound gathers get 3 CTAs per SM of their own instead of stalling a
-  // tile between its shared-memory gathers.  Measured on B200 (RK stage time):
+  // latency-bound gathers get warps of their own instead of stalling a tile between
+  // its shared-memory gathers.  Measured on B200 (RK stage time):
   // config 5 (42 M remote slots, 20 K per tile) 1.226 -> 1.181 ms with the pass;
   // config 4 (7.7 M, 7 K per tile) 0.312 -> 0.350 ms and config 3 (4.3 M, 17 K per
   // tile, 44 us stage) 0.044 -> 0.049 ms, so those stay inline.
@@ -851,6 +851,24 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
       P.chunks[(size_t)cofs[(size_t)lt] + c] = cd;
     }
     std::vector<Unit>().swap(O.units);
+  }
+  if (P.split_remote) {  // flat list of every remote chunk (one warp each in k_remote), longest first
+    std::vector<std::array<uint32_t, 4>> rc;
+    for (const TileDesc& T : P.tiles) {
+      if (T.nparts == T.nhot) continue;
+      const PartDesc& pd = P.parts[(size_t)(T.part0 + T.nhot)];
+      for (uint32_t c = 0; c < pd.nchunks; ++c)
+        rc.push_back({P.chunks[(size_t)(pd.chunk0 + c)].ng, pd.chunk0 + c, (uint32_t)(T.row0 - P.row_begin),
+                      (uint32_t)(pd.neg >> 8)});
+    }
+    std::stable_sort(rc.begin(), rc.end(), [](const auto& x, const auto& y) { return x[0] > y[0]; });
+    P.rchunks.resize(2 * rc.size());
+    P.rem_lp.resize(rc.size());
+    for (size_t k = 0; k < rc.size(); ++k) {
+      P.rchunks[2 * k] = rc[k][1];
+      P.rchunks[2 * k + 1] = rc[k][2];
+      P.rem_lp[k] = (uint8_t)rc[k][3];
+    }
   }
   // per local row: scale 1/M_m for the degree scaling (0 for a zero
   // row) and the potential constant ones_off + [z_m inside W_m]

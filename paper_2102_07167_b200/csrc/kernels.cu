@@ -647,25 +647,30 @@ __global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const S
   tile_partial_and_finish(dp, a, lt, x, y, red);
 }
 
-// a3, remote half: the remote parts of every tile (global z gathers, latency
-// bound), W_r = -sum_{Z_j remote} z_k + sum_{NZ_j remote} z_k, into Wr.  A
-// separate launch before k_stage: with up to 4 CTAs per SM (no window in
-// shared memory) the random gathers get four times the memory-level
-// parallelism they have between k_stage's shared-memory gathers.
-__global__ void __launch_bounds__(NTHREADS, 2) k_remote(const DevPlan dp, const double2* __restrict__ zin) {
-  extern __shared__ __align__(16) double2 Wrs[];
-  const TileDesc T = dp.tiles[dp.order[blockIdx.x]];
-  if (T.nparts == T.nhot) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int r = tid; r < T.nrows; r += NTHREADS) Wrs[r] = make_double2(0.0, 0.0);
-  __syncthreads();
-  const uint64_t pol = evict_first_policy();
-  for (int p = T.part0 + T.nhot; p < T.part0 + T.nparts; ++p) {
-    const PartDesc P = dp.parts[p];
-    run_part<false, true>(dp, P, false, nullptr, zin, Wrs, pol, warp, lane);
-    __syncthreads();
+// a3, remote half: W_r,j = sum over the row's remote entries (signed, P:562-570 /
+// P:538-542) into Wr.  One warp per remote chunk (32 rows), all tiles' chunks in
+// one flat list, longest first: every row lies in exactly one remote chunk of its
+// tile (one remote part per tile), so the row sum is written, not accumulated, and
+// rows without remote entries keep the zero Wr was initialised with.  Thousands of
+// independent warps keep the latency-bound random z gathers in flight.
+constexpr int KREM_THREADS = 256;
+__global__ void __launch_bounds__(KREM_THREADS, 4) k_remote(const DevPlan dp, const double2* __restrict__ zin) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (KREM_THREADS / 32) + (threadIdx.x >> 5);
+  if (w >= dp.n_rchunks) return;
+  const uint2 rc = __ldg(reinterpret_cast<const uint2*>(dp.rchunks) + w);  // {chunk id, tile row base}
+  const uint2 cd = __ldg(dp.chunks + rc.x);
+  const uint4* q = dp.pool + cd.x;
+  const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
+  double sx, sy;
+  run_remote_deep(q + HDR_UNITS + lane, cd.y, (uint32_t)dp.n, zin, evict_first_policy(), sx, sy);
+  const int lp = dp.rem_lp[w];  // row pieces of the chunk's part
+  for (int o = 1; o < (1 << lp); o <<= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
   }
-  for (int r = tid; r < T.nrows; r += NTHREADS) dp.Wr[(T.row0 - dp.row_begin) + r] = Wrs[r];
+  // 0 + s: the same single rounding-free addition the inline path does into a zeroed sum
+  if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) dp.Wr[rc.y + row] = make_double2(0.0 + sx, 0.0 + sy);
 }
 
 template <int MODE>
@@ -858,8 +863,9 @@ namespace kur {
 #endif
 
 cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s) {
-  if (!dp.has_remote || dp.ntiles <= 0) return cudaSuccess;
-  k_remote<<<dp.ntiles, NTHREADS, sizeof(double2) * (size_t)dp.rows_per_tile, s>>>(dp, zin);
+  if (!dp.has_remote || dp.n_rchunks <= 0) return cudaSuccess;
+  constexpr int wpb = KREM_THREADS / 32;
+  k_remote<<<(unsigned)((dp.n_rchunks + wpb - 1) / wpb), KREM_THREADS, 0, s>>>(dp, zin);
   return cudaGetLastError();
 }
 

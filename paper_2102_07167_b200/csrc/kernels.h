@@ -50,6 +50,9 @@ struct DevPlan {
   double2* partial;           // [ntiles_all] per-tile sums of z (global tile ids)
   double* pmax;               // [ntiles_all] per-tile max |fixed-point update| (implicit midpoint)
   double2* Wr;                // [local rows] remote-part row sums of the current stage (k_remote -> k_stage)
+  const uint32_t* rchunks;    // [n_rchunks][2] remote pass: {chunk id, local row of the tile's row 0}
+  const uint8_t* rem_lp;      // [n_rchunks] row-piece shift of each chunk's part
+  int32_t n_rchunks;
   double2* S;                 // [C] block sums S_b of the last reduction
   Ctrl* ctrl;
 };

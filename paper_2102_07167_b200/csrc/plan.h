@@ -99,6 +99,9 @@ struct HostPlan {
   std::vector<ChunkDesc> chunks;    // this rank's chunks
   std::vector<Unit> pool;           // index data
   std::vector<int32_t> tile_order;  // launch order (local tile ids, decreasing work)
+  std::vector<uint32_t> rchunks;    // remote pass: [2k] chunk id, [2k+1] local row of the chunk's tile row 0,
+                                    // all tiles' remote chunks, longest first
+  std::vector<uint8_t> rem_lp;      // remote pass: row-piece shift (PartDesc.neg >> 8) per listed chunk
   std::vector<double> rowscale;     // [local rows] 1/M_m (degree scaling only; empty = uniform K/N)
   std::vector<double> potc;         // [local rows] off-diagonal ones + [z_m inside W_m] (kur_potential)
   std::vector<int32_t> shard_row0;  // [world+1] internal row ranges of all ranks
