@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "kernels.h"
 
@@ -837,12 +838,14 @@ __global__ void k_permute(const int32_t* __restrict__ perm, int64_t n, const dou
 
 template <int MODE>
 cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
-  static bool attr_set = false;
+  static std::atomic<uint64_t> attr_set{0};  // one bit per device (the attribute is per device context)
   const size_t smem = stage_smem_bytes(MAX_TILE_ROWS);
-  if (!attr_set) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!((attr_set.load() >> (dev & 63)) & 1)) {
     cudaError_t e = cudaFuncSetAttribute(k_stage<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.fetch_or(1ull << (dev & 63));
   }
   if (dp.has_remote && !a.no_remote && a.phase != PHASE_A) {
     cudaError_t e = launch_remote(dp, a.zin, s);
@@ -897,12 +900,14 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
 
 cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, double2* zB, double2* TA, double2* TB,
                          long long nsteps, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};  // one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!((attr_set.load() >> (dev & 63)) & 1)) {
     cudaError_t e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)stage_smem_bytes(MAX_TILE_ROWS));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.fetch_or(1ull << (dev & 63));
   }
   k_small<<<1, NTHREADS, dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) : 0, s>>>(dp, a, zA, zB, TA, TB, nsteps);
   return cudaGetLastError();
