@@ -170,6 +170,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile-rows", type=int, default=0, help="tuning: force the tile size (rows)")
     ap.add_argument("--hot-min", type=int, default=0, help="tuning: window staging threshold")
+    ap.add_argument("--dense-threshold", type=float, default=-1.0,
+                    help="ablation (SURVEY 8(d)): 0 forces direct summation (plain CSR), <0 the paper's rule")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -194,9 +196,10 @@ def main():
         obj = [kur.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         g = kur.graph_build(inst, device=local, dist=(rank, world, obj[0]), tile_rows=args.tile_rows,
-                            hot_min=args.hot_min)
+                            hot_min=args.hot_min, dense_threshold=args.dense_threshold)
     else:
-        g = kur.graph_build(inst, device=local, tile_rows=args.tile_rows, hot_min=args.hot_min)
+        g = kur.graph_build(inst, device=local, tile_rows=args.tile_rows, hot_min=args.hot_min,
+                            dense_threshold=args.dense_threshold)
     build_s = time.perf_counter() - t0
     info = g.info
     th = g.local(g.to_internal(torch.from_numpy(inst.theta0).to(dev))).clone()
@@ -320,7 +323,8 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": inst.name, "n": inst.n, "n_comm": inst.n_comm, "K": K, "h": h,
                        "nnz": int(info["nnz"]), "n_idx": int(info["n_idx"]), "seed": inst.seed,
-                       "instance_sha256": inst.sha256()[:16], "l2": l2_note, "parallelism": f"communities x{world}"},
+                       "instance_sha256": inst.sha256()[:16], "l2": l2_note, "parallelism": f"communities x{world}",
+                       "dense_threshold": args.dense_threshold},
             "rk4_steps_per_s": 1e3 / ms_per_step,
             "algorithmic_gbs": achieved,
             "roofline": roofline,
