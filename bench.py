@@ -273,6 +273,30 @@ def main():
                      "issued_frac": hot_issued / (kstage_ms / 1e3) / 1e9 / smem_peak,
                      "bytes_per_launch": hot_alg, "bytes_formula": "16 B per hot (window-staged) entry"}
 
+    # ---- SURVEY 8(d) protocol (i): back-to-back kur_rhs calls (z of the state, block sums, one
+    # RHS; no RK epilogue), captured once in a CUDA graph and replayed (world 1 only)
+    rhs_calls = None
+    if world == 1 and not args.no_e2e:
+        f_out = torch.empty_like(th)
+        kur.rhs(g, th, om, K, out=f_out)
+        torch.cuda.synchronize()
+        ncall = 100 if inst.n >= (1 << 20) else 1000
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(10):
+                kur.rhs(g, th, om, K, out=f_out)
+        graph.replay()
+        torch.cuda.synchronize()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record()
+        for _ in range(ncall // 10):
+            graph.replay()
+        r1.record()
+        torch.cuda.synchronize()
+        r_ms = r0.elapsed_time(r1) / ncall
+        rhs_calls = {"value": 1e3 / r_ms, "unit": UNIT, "calls": ncall, "ms_per_call": r_ms,
+                     "path": "kur_rhs x 10 captured in a CUDA graph, replayed (prologue + [k_remote] + k_stage<RHS>)"}
+
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -331,6 +355,7 @@ def main():
             "smem_roofline": smem_roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "rhs_calls": rhs_calls,
             "gpu_launches": 1 + tm["prologue_n"] + tm["stage_n"] + tm["remote_n"]
                             + (2 * (tm["prologue_n"] + tm["stage_n"]) if world > 1 else 0),
             "clocks": clk.result(),
