@@ -340,7 +340,7 @@ __device__ __forceinline__ void run_part(const DevPlan& dp, const PartDesc& P, b
 // partials, T_a, the order parameter and its recording.
 __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
   __shared__ double2 fred[NWARPS];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   constexpr int BIG = 64;  // communities with more tiles are reduced by the whole CTA
   if (a.v_out) {  // kur_potential: V = sum of the tile partials in tile order (fixed shape)
     double x = 0.0, y = 0.0;
@@ -360,17 +360,18 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
     if (tid == 0) dp.ctrl->fp_done = a.fp_check ? (d <= dp.ctrl->fp_tol) : 0;
     __syncthreads();
   }
-  for (int c = warp; c < dp.C; c += NWARPS) {  // S_b = sum of its tiles' partials
+  // S_b = sum of its tiles' partials: one thread per community, tiles in order
+  // (the loads of a community are independent and pipeline); > BIG tiles: block reduction
+  for (int c = tid; c < dp.C; c += NTHREADS) {
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
     if (t1 - t0 > BIG) continue;
     double x = 0.0, y = 0.0;
-    for (int t = t0 + lane; t < t1; t += 32) {
+    for (int t = t0; t < t1; ++t) {
       const double2 v = __ldcg(dp.partial + t);
       x += v.x;
       y += v.y;
     }
-    warp_sum2(x, y);
-    if (lane == 0) dp.S[c] = make_double2(x, y);
+    dp.S[c] = make_double2(x, y);
   }
   for (int c = 0; c < dp.C; ++c) {  // large communities (uniform branch): fixed-shape block reduction
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
@@ -474,22 +475,31 @@ __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const
 // a1 for one tile: z = e^{i theta} of its rows; returns this thread's partial sums.
 __device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs& a, const TileDesc& T, double& x,
                                               double& y) {
+  // all of this thread's phases are loaded before the first sincos (memory-level parallelism);
+  // summation order of the partials unchanged (rows in increasing lr)
+  constexpr int R = MAX_TILE_ROWS / NTHREADS;
+  const double* src = a.commit ? a.commit : a.theta;  // implicit midpoint: theta_{n+1} = the fixed point
+  double th[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int lr = threadIdx.x + k * NTHREADS;
+    th[k] = lr < T.nrows ? src[T.row0 + lr - dp.row_begin] : 0.0;
+  }
   x = 0.0;
   y = 0.0;
-  for (int lr = threadIdx.x; lr < T.nrows; lr += NTHREADS) {
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int lr = threadIdx.x + k * NTHREADS;
+    if (lr >= T.nrows) break;
     const int row = T.row0 + lr;
-    double s, c;
-    double th;
-    if (a.commit) {  // implicit midpoint: theta_{n+1} = the converged fixed point
-      th = a.commit[row - dp.row_begin];
-      a.theta[row - dp.row_begin] = th;
-      if (!isfinite(th)) dp.ctrl->nonfinite = 1;
-    } else {
-      th = a.theta[row - dp.row_begin];
+    if (a.commit) {
+      a.theta[row - dp.row_begin] = th[k];
+      if (!isfinite(th[k])) dp.ctrl->nonfinite = 1;
     }
-    sincos(th, &s, &c);  // z = e^{i theta}
+    double s, c;
+    sincos(th[k], &s, &c);  // z = e^{i theta}
     a.zout[row] = make_double2(c, s);
-    if (a.xsend) a.xsend[row - dp.row_begin] = th;
+    if (a.xsend) a.xsend[row - dp.row_begin] = th[k];
     x += c;
     y += s;
   }
