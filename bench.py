@@ -170,6 +170,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile-rows", type=int, default=0, help="tuning: force the tile size (rows)")
     ap.add_argument("--hot-min", type=int, default=0, help="tuning: window staging threshold")
+    ap.add_argument("--peer-exchange", action="store_true",
+                    help="N > 1: fused peer-store exchange from the stage kernel instead of ncclAllGather")
     ap.add_argument("--dense-threshold", type=float, default=-1.0,
                     help="ablation (SURVEY 8(d)): 0 forces direct summation (plain CSR), <0 the paper's rule")
     args = ap.parse_args()
@@ -195,7 +197,8 @@ def main():
     if world > 1:
         obj = [kur.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        g = kur.graph_build(inst, device=local, dist=(rank, world, obj[0]), tile_rows=args.tile_rows,
+        g = kur.graph_build(inst, device=local, dist=(rank, world, obj[0], kur.DIST_PEER_EXCHANGE if
+                                                      args.peer_exchange else 0), tile_rows=args.tile_rows,
                             hot_min=args.hot_min, dense_threshold=args.dense_threshold)
     else:
         g = kur.graph_build(inst, device=local, tile_rows=args.tile_rows, hot_min=args.hot_min,
@@ -348,7 +351,9 @@ def main():
             "config": {"workload": inst.name, "n": inst.n, "n_comm": inst.n_comm, "K": K, "h": h,
                        "nnz": int(info["nnz"]), "n_idx": int(info["n_idx"]), "seed": inst.seed,
                        "instance_sha256": inst.sha256()[:16], "l2": l2_note, "parallelism": f"communities x{world}",
-                       "dense_threshold": args.dense_threshold},
+                       "dense_threshold": args.dense_threshold,
+                       "exchange": ("peer stores (fused)" if info["peer_exchange"] else "ncclAllGather")
+                       if world > 1 else None},
             "rk4_steps_per_s": 1e3 / ms_per_step,
             "algorithmic_gbs": achieved,
             "roofline": roofline,

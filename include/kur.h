@@ -123,7 +123,16 @@ typedef struct {
   int32_t world;
   int32_t device;
   const void *nccl_id;
+  int32_t flags;    /* 0, or KUR_DIST_PEER_EXCHANGE: the fused RK-stage kernel stores its phases
+                       and tile partials straight into every rank's receive buffer (NVLink peer
+                       memory, CUDA IPC handles exchanged over NCCL at build) and signals an
+                       arrival counter there; the next stage's unpack waits on its counter — no
+                       separate all-gather.  Falls back to ncclAllGather when peer mapping fails
+                       (kur_graph_info.peer_exchange says which).  Group handles (nccl_id NULL):
+                       in-process peers. */
+  int32_t reserved;
 } kur_dist_desc;
+enum { KUR_DIST_PEER_EXCHANGE = 1 };
 
 typedef struct {
   int64_t n, n_comm;
@@ -145,7 +154,7 @@ typedef struct {
   double build_seconds;        /* host time of kur_graph_build */
   int32_t remote_pass;         /* 1: remote entries summed by the separate k_remote pass before each
                                   stage kernel (2 launches per RHS), 0: inline */
-  int32_t reserved0;
+  int32_t peer_exchange;       /* world > 1: 1 = fused peer-store exchange active, 0 = all-gather */
 } kur_graph_info_t;
 
 typedef struct kur_graph kur_graph; /* opaque; owns all device data and workspace */

@@ -73,6 +73,14 @@ struct kur_graph {
   cudaStream_t comm_stream = nullptr;         // NCCL: exchange + unpack + finish, overlapping phase A
   cudaEvent_t ev_b = nullptr, ev_exch = nullptr;
   bool exch_pending = false;                  // comm_stream holds an exchange the next phase B waits for
+  // fused peer-store exchange (KUR_DIST_PEER_EXCHANGE)
+  bool peer_req = false, peer_on = false;
+  unsigned int* d_flag = nullptr;             // this rank's arrival counter (peers increment it)
+  unsigned int* d_xticket = nullptr;
+  double** d_peer_x = nullptr;                // [world] device array of receive-buffer pointers
+  unsigned int** d_peer_flag = nullptr;       // [world] device array of counter pointers
+  std::vector<void*> ipc_opened;              // peer allocations mapped through CUDA IPC
+  unsigned int xepoch = 0;                    // exchanges completed on this handle
   // optional per-launch CUDA-event timing (kur_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev;        // pool, reused
@@ -94,11 +102,13 @@ struct kur_graph {
     cudaSetDevice(device);
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
-                    xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh, d_rchunks, d_rem_lp};
+                    xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh, d_rchunks, d_rem_lp, d_flag, d_xticket,
+                    d_peer_x, d_peer_flag};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     if (comm_stream) cudaStreamSynchronize(comm_stream);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (comm) ncclCommDestroy(comm);
     if (ev_b) cudaEventDestroy(ev_b);
     if (ev_exch) cudaEventDestroy(ev_exch);
@@ -237,11 +247,22 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   if ((e = upload(&g->d_shard_tile0, P.shard_tile0)) != cudaSuccess) return bail(e, "shard_tile0");
   if (world > 1) {
     if ((e = cudaMalloc((void**)&g->xsend, sizeof(double) * (size_t)xstride)) != cudaSuccess) return bail(e, "xsend");
-    if ((e = cudaMalloc((void**)&g->xrecv, sizeof(double) * (size_t)xstride * (size_t)world)) != cudaSuccess)
+    const bool peer = dist && (dist->flags & KUR_DIST_PEER_EXCHANGE);  // two halves by exchange parity
+    if ((e = cudaMalloc((void**)&g->xrecv, sizeof(double) * (size_t)xstride * (size_t)world * (peer ? 2 : 1))) !=
+        cudaSuccess)
       return bail(e, "xrecv");
     if ((e = cudaMemset(g->xsend, 0, sizeof(double) * (size_t)xstride)) != cudaSuccess) return bail(e, "xsend");
     if ((e = cudaMalloc((void**)&g->Wh, sizeof(double2) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess)
       return bail(e, "Wh");
+    g->peer_req = dist && (dist->flags & KUR_DIST_PEER_EXCHANGE);
+    if (g->peer_req) {
+      if ((e = cudaMalloc((void**)&g->d_flag, 256)) != cudaSuccess || (e = cudaMemset(g->d_flag, 0, 256)) != cudaSuccess ||
+          (e = cudaMalloc((void**)&g->d_xticket, sizeof(unsigned int))) != cudaSuccess ||
+          (e = cudaMemset(g->d_xticket, 0, sizeof(unsigned int))) != cudaSuccess ||
+          (e = cudaMalloc((void**)&g->d_peer_x, sizeof(double*) * (size_t)world)) != cudaSuccess ||
+          (e = cudaMalloc((void**)&g->d_peer_flag, sizeof(unsigned int*) * (size_t)world)) != cudaSuccess)
+        return bail(e, "peer exchange buffers");
+    }
     if (dist && dist->nccl_id) {
       ncclUniqueId id;
       std::memcpy(&id, dist->nccl_id, sizeof(id));
@@ -256,6 +277,58 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
           (e = cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming)) != cudaSuccess ||
           (e = cudaEventCreateWithFlags(&g->ev_exch, cudaEventDisableTiming)) != cudaSuccess)
         return bail(e, "exchange stream");
+      if (g->peer_req) {
+        // map every rank's receive buffer and arrival counter into this process: CUDA IPC
+        // handles all-gathered over NCCL; any failure keeps the all-gather exchange
+        cudaIpcMemHandle_t mine[2];
+        bool ok = cudaIpcGetMemHandle(&mine[0], g->xrecv) == cudaSuccess &&
+                  cudaIpcGetMemHandle(&mine[1], g->d_flag) == cudaSuccess;
+        std::vector<cudaIpcMemHandle_t> all((size_t)world * 2);
+        char* dbuf = nullptr;
+        const size_t hb = sizeof(mine);
+        ok = ok && cudaMalloc((void**)&dbuf, hb * (size_t)(world + 1)) == cudaSuccess;
+        ok = ok && cudaMemcpy(dbuf, mine, hb, cudaMemcpyHostToDevice) == cudaSuccess;
+        ok = ok && ncclAllGather(dbuf, dbuf + hb, hb, ncclChar, g->comm, g->comm_stream) == ncclSuccess;
+        ok = ok && cudaStreamSynchronize(g->comm_stream) == cudaSuccess;
+        ok = ok && cudaMemcpy(all.data(), dbuf + hb, hb * (size_t)world, cudaMemcpyDeviceToHost) == cudaSuccess;
+        if (dbuf) cudaFree(dbuf);
+        std::vector<double*> px((size_t)world, nullptr);
+        std::vector<unsigned int*> pf((size_t)world, nullptr);
+        for (int32_t r = 0; r < world && ok; ++r) {
+          if (r == rank) {
+            px[(size_t)r] = g->xrecv;
+            pf[(size_t)r] = g->d_flag;
+            continue;
+          }
+          void* a = nullptr;
+          void* b = nullptr;
+          ok = cudaIpcOpenMemHandle(&a, all[2 * (size_t)r], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+          if (ok) g->ipc_opened.push_back(a);
+          ok = ok && cudaIpcOpenMemHandle(&b, all[2 * (size_t)r + 1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+          if (ok) g->ipc_opened.push_back(b);
+          px[(size_t)r] = (double*)a;
+          pf[(size_t)r] = (unsigned int*)b;
+        }
+        // every rank must agree, or the ranks would disagree on the exchange protocol
+        int flag_ok = ok ? 1 : 0, *dflag = nullptr;
+        int all_ok = 0;
+        if (cudaMalloc((void**)&dflag, sizeof(int)) == cudaSuccess &&
+            cudaMemcpy(dflag, &flag_ok, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+            ncclAllReduce(dflag, dflag, 1, ncclInt, ncclMin, g->comm, g->comm_stream) == ncclSuccess &&
+            cudaStreamSynchronize(g->comm_stream) == cudaSuccess &&
+            cudaMemcpy(&all_ok, dflag, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess) {
+        }
+        if (dflag) cudaFree(dflag);
+        cudaGetLastError();  // clear a failed IPC call's sticky-free error state
+        if (all_ok) {
+          if ((e = cudaMemcpy(g->d_peer_x, px.data(), sizeof(double*) * (size_t)world, cudaMemcpyHostToDevice)) !=
+                  cudaSuccess ||
+              (e = cudaMemcpy(g->d_peer_flag, pf.data(), sizeof(unsigned int*) * (size_t)world,
+                              cudaMemcpyHostToDevice)) != cudaSuccess)
+            return bail(e, "peer pointers");
+          g->peer_on = true;
+        }
+      }
     }
   }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "build sync");
@@ -285,6 +358,9 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
     if ((e = upload(&g->d_rem_lp, P.rem_lp)) != cudaSuccess) return bail(e, "rem_lp");
   }
   dp.Wr = g->Wr;
+  dp.peer_x = g->peer_on ? g->d_peer_x : nullptr;
+  dp.peer_flag = g->d_peer_flag;
+  dp.xticket = g->d_xticket;
   dp.rchunks = g->d_rchunks;
   dp.rem_lp = g->d_rem_lp;
   dp.n_rchunks = (int32_t)(P.rem_lp.size());
@@ -337,6 +413,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   I.bytes_pool = pool_bytes;
   I.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   I.remote_pass = dp.has_remote;
+  I.peer_exchange = g->peer_on ? 1 : 0;
   *out = g;
   return KUR_OK;
 }
@@ -443,6 +520,7 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
       a.Tout = z_from_A ? g->TB : g->TA;
     }
     a.Wh = g->Wh;
+    a.xpar = (int)((g->xepoch + 1) & 1u);  // parity of the exchange this phase produces
   }
   if (world > 1 && mode != PH_PROLOGUE) {
     // phase A: own-community hot parts (local z only) -> Wh, while the previous stage's
@@ -489,11 +567,18 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
     KUR_CUDA(cudaEventRecord(g0->ev_b, s));
     KUR_CUDA(cudaStreamWaitEvent(xs, g0->ev_b, 0));
   }
-  kur_status st = exchange(gs, xs);
-  if (st != KUR_OK) return st;
+  // fused peer-store exchange: the kernels above already stored every record into every rank's
+  // receive buffer and counted their arrival; k_unpack waits for the count instead of an all-gather
+  if (!g0->peer_on) {
+    kur_status st = exchange(gs, xs);
+    if (st != KUR_OK) return st;
+  }
   for (size_t r = 0; r < gs.size(); ++r) {
-    KUR_CUDA(launch_unpack(gs[r]->dp, gs[r]->xrecv, args[r].zout, xs));
-    KUR_CUDA(launch_finish(gs[r]->dp, args[r], xs));
+    kur_graph* g = gs[r];
+    const unsigned int expect = g->peer_on ? (++g->xepoch) * (unsigned int)world : 0u;
+    const double* xr = g->xrecv + (g->peer_on ? (size_t)(g->xepoch & 1u) * (size_t)world * g->dp.xstride : 0);
+    KUR_CUDA(launch_unpack(g->dp, xr, args[r].zout, expect, xs));
+    KUR_CUDA(launch_finish(g->dp, args[r], xs));
   }
   if (async) {
     KUR_CUDA(cudaEventRecord(g0->ev_exch, xs));
@@ -521,6 +606,28 @@ kur_status check_group(const std::vector<kur_graph*>& gs) {
   if (gs.size() > 1) {
     for (size_t r = 0; r < gs.size(); ++r)
       if (gs[r]->dp.rank != (int)r || gs[r]->comm) return fail(KUR_ERR_INVALID_ARG, "group handles must be ranks 0..world-1 without NCCL");
+    // in-process fused exchange: link every rank handle to the others' receive buffers and counters
+    bool want = true, linked = true;
+    for (kur_graph* g : gs) {
+      want = want && g->peer_req;
+      linked = linked && g->peer_on;
+    }
+    if (want && !linked) {
+      std::vector<double*> px;
+      std::vector<unsigned int*> pf;
+      for (kur_graph* g : gs) {
+        px.push_back(g->xrecv);
+        pf.push_back(g->d_flag);
+      }
+      KUR_CUDA(cudaSetDevice(gs[0]->device));
+      for (kur_graph* g : gs) {
+        KUR_CUDA(cudaMemcpy(g->d_peer_x, px.data(), sizeof(double*) * px.size(), cudaMemcpyHostToDevice));
+        KUR_CUDA(cudaMemcpy(g->d_peer_flag, pf.data(), sizeof(unsigned int*) * pf.size(), cudaMemcpyHostToDevice));
+        g->peer_on = true;
+        g->dp.peer_x = g->d_peer_x;
+        g->info.peer_exchange = 1;
+      }
+    }
   }
   return KUR_OK;
 }
@@ -824,6 +931,9 @@ kur_status kur_check(kur_graph* g, void* stream) {
   if (!g) return fail(KUR_ERR_INVALID_ARG, "graph is NULL");
   KUR_CUDA(cudaSetDevice(g->device));
   KUR_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  int xt = 0;
+  KUR_CUDA(cudaMemcpy(&xt, &g->ctrl->xtimeout, sizeof(int), cudaMemcpyDeviceToHost));
+  if (xt) return fail(KUR_ERR_NCCL, "fused peer exchange: timed out waiting for the other ranks' records");
   int flag = 0;
   KUR_CUDA(cudaMemcpy(&flag, &g->ctrl->nonfinite, sizeof(int), cudaMemcpyDeviceToHost));
   if (flag) {

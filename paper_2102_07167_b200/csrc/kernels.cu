@@ -336,6 +336,37 @@ __device__ __forceinline__ void run_part(const DevPlan& dp, const PartDesc& P, b
     }
 }
 
+// world > 1: one double of this rank's packed exchange record [phases | per tile (sum z, max
+// |update|)] at offset off — into the send buffer (all-gather), or, with the fused peer-store
+// exchange, straight into every rank's receive buffer over NVLink (slot `rank` of each).
+__device__ __forceinline__ void xput(const DevPlan& dp, const StageArgs& a, int off, double v) {
+  if (dp.peer_x) {
+    // double-buffered by exchange parity: a fast rank's next record cannot overwrite a record a
+    // slow rank is still unpacking (the next-but-one exchange needs that rank's arrival first)
+    const size_t base = ((size_t)a.xpar * dp.world + dp.rank) * dp.xstride;
+    for (int r = 0; r < dp.world; ++r) dp.peer_x[r][base + off] = v;
+  } else {
+    a.xsend[off] = v;
+  }
+}
+
+// Fused exchange: after every tile of this launch stored its record, the last CTA signals every
+// rank's arrival counter (release at system scope: each CTA fenced its peer stores before its ticket).
+__device__ __forceinline__ void peer_arrive(const DevPlan& dp) {
+  __shared__ bool s_lastx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned int t = atomicAdd(dp.xticket, 1u);
+    s_lastx = (t == gridDim.x - 1);
+    if (s_lastx) {
+      *dp.xticket = 0;
+      __threadfence_system();
+      for (int r = 0; r < dp.world; ++r) atomicAdd_system(dp.peer_flag[r], 1u);
+    }
+  }
+}
+
 // Executed by every thread of the LAST CTA of a grid: S_b from the per-tile
 // partials, T_a, the order parameter and its recording.
 __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
@@ -454,9 +485,9 @@ __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const
     dp.partial[dp.tile_base + lt] = make_double2(x, y);
     if (a.fp_check) dp.pmax[dp.tile_base + lt] = dmax;
     if (a.xsend) {
-      a.xsend[dp.xrows + 3 * lt] = x;
-      a.xsend[dp.xrows + 3 * lt + 1] = y;
-      a.xsend[dp.xrows + 3 * lt + 2] = dmax;
+      xput(dp, a, dp.xrows + 3 * lt, x);
+      xput(dp, a, dp.xrows + 3 * lt + 1, y);
+      xput(dp, a, dp.xrows + 3 * lt + 2, dmax);
     }
     s_last = false;
     if (dp.world == 1) {  // world > 1: the reduction runs after the exchange
@@ -499,7 +530,7 @@ __device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs
     double s, c;
     sincos(th[k], &s, &c);  // z = e^{i theta}
     a.zout[row] = make_double2(c, s);
-    if (a.xsend) a.xsend[row - dp.row_begin] = th[k];
+    if (a.xsend) xput(dp, a, row - dp.row_begin, th[k]);
     x += c;
     y += s;
   }
@@ -641,7 +672,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       double s, c;
       sincos(ts, &s, &c);
       a.zout[row] = make_double2(c, s);
-      if (a.xsend) a.xsend[li] = ts;
+      if (a.xsend) xput(dp, a, li, ts);
       px += c;
       py += s;
     }
@@ -656,6 +687,7 @@ __global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const S
   double x, y;
   prologue_rows(dp, a, T, x, y);
   tile_partial_and_finish(dp, a, lt, x, y, red);
+  if (dp.peer_x && a.xsend) peer_arrive(dp);
 }
 
 // a3, remote half: W_r,j = sum over the row's remote entries (signed, P:562-570 /
@@ -696,7 +728,16 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   // implicit midpoint: iterations after convergence are no-ops (uniform: every CTA reads the same flag)
   // (phase A never skips: it may run before the finish that sets or clears the flag, and
   // phase B, which does check it, then reads Wh)
-  if (MODE == MODE_MI && a.phase != PHASE_A && *(volatile const int*)&dp.ctrl->fp_done) return;
+  if (MODE == MODE_MI && a.phase != PHASE_A && *(volatile const int*)&dp.ctrl->fp_done) {
+    if (dp.peer_x && a.xsend) {  // re-publish this rank's previous record (the all-gather path
+      // re-sends the unchanged send buffer) into the current receive half of every rank
+      const double* prev = dp.peer_x[dp.rank] + ((size_t)(1 - a.xpar) * dp.world + dp.rank) * dp.xstride;
+      for (int i = blockIdx.x * NTHREADS + threadIdx.x; i < dp.xstride; i += gridDim.x * NTHREADS)
+        xput(dp, a, i, prev[i]);
+      peer_arrive(dp);
+    }
+    return;
+  }
   const int lt = dp.order[blockIdx.x];
   const TileDesc T = dp.tiles[lt];
   if (a.phase == PHASE_A && T.nown == 0) return;  // nothing local to pre-sum (phase B starts from 0)
@@ -716,6 +757,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   if (FINAL && tid == 0 && s_nonfinite) dp.ctrl->nonfinite = 1;
   PROF_T(26);
   tile_partial_and_finish(dp, a, lt, px, py, red, dmax);
+  if (dp.peer_x && a.xsend) peer_arrive(dp);
 }
 
 // ---- single-CTA trajectory kernel for tiny graphs (world == 1): the whole
@@ -789,7 +831,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_small(const DevPlan dp, StageAr
 
 // world > 1: z of the non-local rows from the exchanged stage phases (the same
 // sincos the owner evaluated -> bitwise identical), and every tile partial.
-__global__ void k_unpack(const DevPlan dp, const double* __restrict__ xrecv, double2* __restrict__ zout) {
+__global__ void k_unpack(const DevPlan dp, const double* __restrict__ xrecv, double2* __restrict__ zout,
+                         unsigned int expect) {
+  if (dp.peer_x) {  // fused exchange: every rank's record of this stage has landed in xrecv
+    if (threadIdx.x == 0) {
+      unsigned int v;
+      uint64_t t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(dp.peer_flag[dp.rank]) : "memory");
+        if ((int)(v - expect) >= 0) break;
+        __nanosleep(64);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) {  // 20 s: a rank is gone; fail loudly instead of hanging
+          dp.ctrl->xtimeout = 1;
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < dp.n) {
     int r = 0;
@@ -808,6 +869,12 @@ __global__ void k_unpack(const DevPlan dp, const double* __restrict__ xrecv, dou
     dp.partial[i] = make_double2(src[0], src[1]);
     dp.pmax[i] = src[2];
   }
+}
+
+// A rank without tiles still signals its (empty) contribution to a fused exchange.
+__global__ void k_arrive(const DevPlan dp) {
+  __threadfence_system();
+  for (int r = 0; r < dp.world; ++r) atomicAdd_system(dp.peer_flag[r], 1u);
 }
 
 __global__ void __launch_bounds__(NTHREADS) k_finish(const DevPlan dp, const StageArgs a) {
@@ -885,13 +952,19 @@ cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s)
 size_t stage_smem_bytes(int rows_per_tile) { return sizeof(double2) * (size_t)(WZ + 8 + rows_per_tile); }
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
-  if (dp.ntiles <= 0) return cudaSuccess;
+  if (dp.ntiles <= 0) {
+    if (dp.peer_x && a.xsend) k_arrive<<<1, 1, 0, s>>>(dp);
+    return cudaGetLastError();
+  }
   k_prologue<<<dp.ntiles, NTHREADS, 0, s>>>(dp, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
-  if (dp.ntiles <= 0) return cudaSuccess;
+  if (dp.ntiles <= 0) {  // no rows here; a fused exchange still counts this rank's arrival
+    if (dp.peer_x && a.xsend && mode != MODE_RHS && a.phase != PHASE_A) k_arrive<<<1, 1, 0, s>>>(dp);
+    return cudaGetLastError();
+  }
   switch (mode) {
     case MODE_RHS: return launch_stage_m<MODE_RHS>(dp, a, s);
     case MODE_S1: return launch_stage_m<MODE_S1>(dp, a, s);
@@ -923,10 +996,11 @@ cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, dou
   return cudaGetLastError();
 }
 
-cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, cudaStream_t s) {
+cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, unsigned int expect,
+                          cudaStream_t s) {
   const int64_t m = std::max<int64_t>(dp.n, (int64_t)1);
   const int bs = 256;
-  k_unpack<<<(unsigned)((m + bs - 1) / bs), bs, 0, s>>>(dp, xrecv, zout);
+  k_unpack<<<(unsigned)((m + bs - 1) / bs), bs, 0, s>>>(dp, xrecv, zout, expect);
   return cudaGetLastError();
 }
 

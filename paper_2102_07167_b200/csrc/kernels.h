@@ -14,6 +14,7 @@ struct Ctrl {             // device-resident control block
   int nrec_cap;           // capacity of r_trace in pairs
   long long step;         // n of the current theta_n inside kur_step
   int fp_done;            // implicit midpoint: the fixed-point iteration of this step converged
+  int xtimeout;           // fused exchange: an unpack gave up waiting for the peers' records
   int fp_pad;
   double fp_tol;          // implicit midpoint: stop when max_m |theta^{(i+1)}_m - theta^{(i)}_m| <= fp_tol
   double* r_trace;        // [nrec_cap][2]
@@ -50,6 +51,9 @@ struct DevPlan {
   double2* partial;           // [ntiles_all] per-tile sums of z (global tile ids)
   double* pmax;               // [ntiles_all] per-tile max |fixed-point update| (implicit midpoint)
   double2* Wr;                // [local rows] remote-part row sums of the current stage (k_remote -> k_stage)
+  double* const* peer_x;      // fused exchange: [world] every rank's receive buffer (peer memory) or NULL
+  unsigned int* const* peer_flag;  // [world] every rank's arrival counter (peer memory)
+  unsigned int* xticket;      // this rank's last-CTA ticket for the arrival signal
   const uint32_t* rchunks;    // [n_rchunks][2] remote pass: {chunk id, local row of the tile's row 0}
   const uint8_t* rem_lp;      // [n_rchunks] row-piece shift of each chunk's part
   int32_t n_rchunks;
@@ -98,6 +102,7 @@ struct StageArgs {
   int phase;              // PHASE_FULL, or world > 1: PHASE_A (own-community hot parts -> Wh, overlaps
                           // the previous exchange) / PHASE_B (Wh + the rest of the tile, finalize)
   double2* Wh;            // [local rows] phase-A row sums (world > 1)
+  int xpar;               // fused exchange: receive half (exchange parity) this launch stores into
 };
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
@@ -110,7 +115,9 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
 // world == 1, tiny graphs: the whole kur_step in one single-CTA launch.
 cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, double2* zB, double2* TA, double2* TB,
                          long long nsteps, cudaStream_t s);
-cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, cudaStream_t s);
+// expect: with the fused peer-store exchange, the arrival count that completes this exchange
+cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, unsigned int expect,
+                          cudaStream_t s);
 cudaError_t launch_finish(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
 cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_trace, double fp_tol,
                             cudaStream_t s);

@@ -41,7 +41,8 @@ class GraphDesc(ctypes.Structure):
 
 
 class DistDesc(ctypes.Structure):
-    _fields_ = [("rank", _i32), ("world", _i32), ("device", _i32), ("nccl_id", _p)]
+    _fields_ = [("rank", _i32), ("world", _i32), ("device", _i32), ("nccl_id", _p), ("flags", _i32),
+                ("reserved", _i32)]
 
 
 class GraphInfo(ctypes.Structure):
@@ -51,7 +52,7 @@ class GraphInfo(ctypes.Structure):
                 ("n_slots_remote", _i64), ("n_dense_blocks", _i64), ("n_sparse_blocks", _i64),
                 ("n_tiles", _i64), ("n_hot_parts", _i64), ("n_window_loads", _i64), ("sincos_per_rhs", _i64),
                 ("bytes_per_rhs", _i64), ("bytes_pool", _i64), ("build_seconds", _d), ("remote_pass", _i32),
-                ("reserved0", _i32)]
+                ("peer_exchange", _i32)]
 
 
 class AdaptiveCtrl(ctypes.Structure):
@@ -151,6 +152,13 @@ class Graph:
         _check(_lib.kur_graph_permutation(self._h, _np_ptr(perm)))
         self.perm = perm  # internal position -> user id
 
+    def refresh_info(self):
+        """Re-read kur_graph_info (e.g. peer_exchange after the first group call linked the ranks)."""
+        info = GraphInfo()
+        _check(_lib.kur_graph_info(self._h, ctypes.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in GraphInfo._fields_}
+        return self.info
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             _lib.kur_graph_destroy(self._h)
@@ -216,10 +224,11 @@ def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, remo
         device = torch.cuda.current_device()
     dd = None
     if dist is not None:
-        rank, world, nccl_id = dist
+        rank, world, nccl_id = dist[:3]
+        flags = int(dist[3]) if len(dist) > 3 else 0
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         dd = DistDesc(rank=rank, world=world, device=device,
-                      nccl_id=ctypes.cast(idbuf, _p) if idbuf is not None else None)
+                      nccl_id=ctypes.cast(idbuf, _p) if idbuf is not None else None, flags=flags, reserved=0)
     h = ctypes.c_void_p()
     with torch.cuda.device(device):
         _check(_lib.kur_graph_build(ctypes.byref(desc), ctypes.byref(dd) if dd is not None else None,
@@ -319,9 +328,13 @@ def _ptr_array(ptrs):
     return arr
 
 
-def group_build(inst, world, device=None, **kw):
+DIST_PEER_EXCHANGE = 1
+
+
+def group_build(inst, world, device=None, peer_exchange=False, **kw):
     """world rank handles on ONE device for the single-process group calls (kur_group_*)."""
-    return [graph_build(inst, device=device, dist=(r, world, None), **kw) for r in range(world)]
+    fl = DIST_PEER_EXCHANGE if peer_exchange else 0
+    return [graph_build(inst, device=device, dist=(r, world, None, fl), **kw) for r in range(world)]
 
 
 def group_rhs(graphs, thetas, omegas, K, outs=None, stream=None):

@@ -92,8 +92,9 @@ def test_method_rk4_equals_kur_step():
     assert torch.equal(a, b) and torch.equal(r1, r2)
 
 
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("method", METHODS)
-def test_methods_group_bitwise(method):
+def test_methods_group_bitwise(method, peer):
     """Sharded path (world 3, device-copy all-gather) bitwise equal to world 1 for every method."""
     inst = kurgen.sbm([3000, 500, 2000, 77], np.array(
         [[0.95, 0.01, 0.0, 0.6], [0.01, 0.3, 0.02, 0.0], [0.0, 0.02, 0.97, 0.1], [0.6, 0.0, 0.1, 0.5]]), 29,
@@ -103,7 +104,7 @@ def test_methods_group_bitwise(method):
     om_full = g1.to_internal(torch.from_numpy(inst.omega).cuda())
     th1 = th_full.clone()
     rt1 = kur.step_method(g1, method, th1, om_full, inst.K, inst.h, 5, 1)
-    gs = kur.group_build(inst, 3)
+    gs = kur.group_build(inst, 3, peer_exchange=peer)
     ths = [th_full[g.row_begin:g.row_end].clone() for g in gs]
     oms = [om_full[g.row_begin:g.row_end].clone() for g in gs]
     rts = kur.group_step_method(gs, method, ths, oms, inst.K, inst.h, 5, 1)

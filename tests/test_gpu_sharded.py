@@ -21,9 +21,10 @@ def _instances():
     yield "cfg3", kurgen.config(3)
 
 
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("remote_pass", [None, True])
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_group_bitwise_equals_single(world, remote_pass):
+def test_group_bitwise_equals_single(world, remote_pass, peer):
     for name, inst in _instances():
         g1 = kur.graph_build(inst, remote_pass=remote_pass)
         dev = "cuda:0"
@@ -33,7 +34,7 @@ def test_group_bitwise_equals_single(world, remote_pass):
         th1 = th_full.clone()
         rt1 = kur.step(g1, th1, om_full, inst.K, inst.h, 6, 1)
 
-        gs = kur.group_build(inst, world, remote_pass=remote_pass)
+        gs = kur.group_build(inst, world, remote_pass=remote_pass, peer_exchange=peer)
         assert all(np.array_equal(g.perm, g1.perm) for g in gs)
         bounds = [(g.row_begin, g.row_end) for g in gs]
         assert bounds[0][0] == 0 and bounds[-1][1] == inst.n
@@ -44,6 +45,7 @@ def test_group_bitwise_equals_single(world, remote_pass):
         assert torch.equal(torch.cat(fs), f1), (name, world, "rhs")
         rts = kur.group_step(gs, ths, oms, inst.K, inst.h, 6, 1)
         torch.cuda.synchronize()
+        assert all(g.refresh_info()["peer_exchange"] == int(peer) for g in gs)
         assert torch.equal(torch.cat(ths), th1), (name, world, "theta after 6 steps")
         for rt in rts:
             assert torch.equal(rt, rt1), (name, world, "r_trace")
