@@ -38,7 +38,13 @@ prof: $(KUR_SRCS) $(KUR_HDRS)
 	  -Xcompiler -fPIC,-fopenmp,-O3 -shared -o $(PKG)/libkur_prof.so $(KUR_SRCS) \
 	  -L$(NCCL_LIB) -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_LIB) -lgomp
 
+# tooling: device-side bounds checks on every layout index (tests: KUR_LIB=$(PKG)/libkur_debug.so)
+debug: $(KUR_SRCS) $(KUR_HDRS)
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -DKUR_DEBUG_BOUNDS -Iinclude -I$(NCCL_INC) \
+	  -Xcompiler -fPIC,-fopenmp,-O3 -shared -o $(PKG)/libkur_debug.so $(KUR_SRCS) \
+	  -L$(NCCL_LIB) -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_LIB) -lgomp
+
 clean:
 	rm -f kurgen/libkurgen.so oracle/liboracle.so $(PKG)/libkur.so $(PKG)/ptxas.log
 
-.PHONY: all clean prof
+.PHONY: all clean prof debug

@@ -28,6 +28,14 @@
 #include "kernels.h"
 
 namespace kur {
+// Debug build only (make debug -> libkur_debug.so, tests via KUR_LIB): device-side bounds checks
+// on every index the layout feeds the kernels (compute-sanitizer is not available on this pool).
+#ifdef KUR_DEBUG_BOUNDS
+#define KUR_ASSERT(c) do { if (!(c)) { printf("KUR_ASSERT %s:%d %s\n", __FILE__, __LINE__, #c); __trap(); } } while (0)
+__device__ uint32_t g_dbg_zlen = 0xFFFFFFFFu;  // entries of the z buffers (set by the launchers)
+#else
+#define KUR_ASSERT(c) do {} while (0)
+#endif
 #ifdef KUR_PROFILE
 // Tooling build only (make prof): per-tile clock64 stamps of k_stage phases.
 __device__ unsigned long long* g_prof = nullptr;
@@ -148,6 +156,7 @@ __device__ __forceinline__ void hot8(const uint4 v, const double2* zs, double& x
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
+    KUR_ASSERT((w[q] & 0xFFFFu) < WZ + 8 && (w[q] >> 16) < WZ + 8);
     const double2 a = zs[w[q] & 0xFFFFu];
     const double2 b = zs[w[q] >> 16];
     x0 += a.x;
@@ -185,6 +194,9 @@ __device__ __forceinline__ double2 ldz(const double2* p) {
 // P:562-570), clear for a non-zero entry (added).  Negation is exact.
 template <bool COHERENT>
 __device__ __forceinline__ double2 ldz_signed(const double2* __restrict__ z, uint32_t id) {
+#ifdef KUR_DEBUG_BOUNDS
+  KUR_ASSERT((id & 0x7FFFFFFFu) < g_dbg_zlen);
+#endif
   const double2 v = ldz<COHERENT>(z + (id & 0x7FFFFFFFu));
   return (id >> 31) ? make_double2(-v.x, -v.y) : v;
 }
@@ -322,6 +334,7 @@ __device__ __forceinline__ void run_part(const DevPlan& dp, const PartDesc& P, b
         sy += __shfl_xor_sync(0xffffffffu, sy, o);
       }
       if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) {
+        KUR_ASSERT(row < dp.rows_per_tile);
         double2 w = Ws[row];
         if (P.neg & 1) {
           w.x -= sx;
@@ -713,6 +726,7 @@ __global__ void __launch_bounds__(KREM_THREADS, 4) k_remote(const DevPlan dp, co
     sy += __shfl_xor_sync(0xffffffffu, sy, o);
   }
   // 0 + s: the same single rounding-free addition the inline path does into a zeroed sum
+  KUR_ASSERT(row == EMPTY_LANE || (int)(rc.y + row) < dp.row_begin + dp.n + 1);
   if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) dp.Wr[rc.y + row] = make_double2(0.0 + sx, 0.0 + sy);
 }
 
@@ -961,6 +975,12 @@ cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t 
 }
 
 cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
+#ifdef KUR_DEBUG_BOUNDS
+  {
+    const uint32_t zl = (uint32_t)(dp.n + 1);  // real rows + the zero sentinel z[n]
+    cudaMemcpyToSymbolAsync(g_dbg_zlen, &zl, sizeof(zl), 0, cudaMemcpyHostToDevice, s);
+  }
+#endif
   if (dp.ntiles <= 0) {  // no rows here; a fused exchange still counts this rank's arrival
     if (dp.peer_x && a.xsend && mode != MODE_RHS && a.phase != PHASE_A) k_arrive<<<1, 1, 0, s>>>(dp);
     return cudaGetLastError();
