@@ -1,5 +1,5 @@
 // kernels.cu — sm_100a fp64 kernels of the localised-order-parameter RHS and
-// the fused classical RK4 stages (product code).
+// the fused integrator stages (product code).
 //
 // One CTA (16 warps, 512 threads) owns one community-aligned tile of up to
 // 2048 rows whose row sums W_j live in shared memory (plan.h describes the
@@ -10,16 +10,21 @@
 //               to the block sums S_b, T_a = sum_{b in D(a)} S_b,
 //               and the order parameter r e^{i psi} = (1/N) sum_b S_b
 //               (P:236-239).
+//   k_remote    (remote-pass plans) the remote part of every tile — random
+//               global z gathers, signed per entry — one warp per chunk, row
+//               sums into Wr.
 //   k_stage     W_j = T_{c(j)} - sum_{Z_j} z_k + sum_{NZ_j} z_k:
 //               hot parts gather z from a 64 KB shared-memory window
-//               (staged by a TMA bulk copy), remote parts from global
-//               memory; then
-//               k_j = omega_j + (K/N) Im(conj z_j W_j)
-//               and, fused, the RK4 stage update (acc, theta_next), the next
-//               stage's z and its per-tile partials; the last CTA forms the
-//               next S_b, T_a and (r, psi) exactly as k_prologue does.
+//               (staged by a TMA bulk copy), the remote part inline or from
+//               Wr; then k_j = omega_j + (K/N) Im(conj z_j W_j)
+//               and, fused, the integrator's stage update (RK4 / Euler / Heun
+//               / implicit midpoint), the next stage's z and its per-tile
+//               partials; the last CTA forms the next S_b, T_a and (r, psi)
+//               exactly as k_prologue does.  world > 1: phase A (own-community
+//               windows) / phase B, records packed for the exchange or stored
+//               straight into the peers' receive buffers.
 // All reductions are fixed-shape (no floating-point atomics): bitwise
-// reproducible run to run.
+// reproducible run to run and across world sizes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
