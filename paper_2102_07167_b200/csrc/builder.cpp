@@ -530,8 +530,8 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   P.small = world == 1 && n <= 8192 && total_len <= (1 << 18);
   // no stored entries (complete graphs: one dense block, empty complement lists) -> no shared
   // memory and nothing to balance: the largest tiles amortise the per-CTA latency (config 2:
-  // 25.7 -> 21.5 us per stage with 2048- instead of 1024-row tiles)
-  int rows_per_tile = force_rows ? force_rows : ((P.small || total_len == 0) ? MAX_TILE_ROWS : 0);
+  // 25.7 -> 21.5 us per stage with 2048- instead of 1024-row tiles, see the commit for 4096)
+  int rows_per_tile = force_rows ? force_rows : (P.small ? MAX_TILE_ROWS : total_len == 0 ? MAX_TILE_ROWS_NOPARTS : 0);
   for (int r = MAX_TILE_ROWS; r >= 256 && !rows_per_tile; r >>= 1) {
     int64_t nt = 0;
     for (int32_t c = 0; c < C; ++c) nt += (S.csize[(size_t)c] + r - 1) / r;

@@ -526,7 +526,7 @@ __device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs
                                               double& y) {
   // all of this thread's phases are loaded before the first sincos (memory-level parallelism);
   // summation order of the partials unchanged (rows in increasing lr)
-  constexpr int R = MAX_TILE_ROWS / NTHREADS;
+  constexpr int R = MAX_TILE_ROWS_NOPARTS / NTHREADS;
   const double* src = a.commit ? a.commit : a.theta;  // implicit midpoint: theta_{n+1} = the fixed point
   double th[R];
 #pragma unroll

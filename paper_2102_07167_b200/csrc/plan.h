@@ -49,6 +49,7 @@ constexpr uint32_t HOT_SENT = WZ;  // first of the 8 zero sentinel slots WZ..WZ+
 constexpr int DEFAULT_HOT_MIN = 2048;
 
 constexpr int MAX_TILE_ROWS = 2048;  // W_j of a tile live in shared memory (32 KB)
+constexpr int MAX_TILE_ROWS_NOPARTS = 4096;  // plans without stored entries keep no W_j in shared memory
 constexpr int HDR_UNITS = 4;         // 64-byte chunk header
 constexpr uint16_t EMPTY_LANE = 0xFFFF;
 
