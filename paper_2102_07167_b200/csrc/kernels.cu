@@ -848,6 +848,104 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_small(const DevPlan dp, StageAr
   if (threadIdx.x == 0 && s_bad) dp.ctrl->nonfinite = 1;
 }
 
+// Tiny entry-free plans (one tile, no stored entries: the classical all-to-all model of
+// P:130-255 at small N): the whole RK4 trajectory in one CTA with every row's state
+// (theta_n, omega, acc, z) in registers and the block sum reduced in shared memory — no
+// global round trips between stages.  W_j = T_c (P:557-561 with empty complement lists),
+// T_c = S_c when the diagonal block is dense, and the arithmetic is the general path's.
+__global__ void __launch_bounds__(NTHREADS, 1) k_small_dense(const DevPlan dp, StageArgs a, long long nsteps) {
+  constexpr int R = MAX_TILE_ROWS / NTHREADS;
+  __shared__ double2 red[NWARPS];
+  __shared__ double2 sS;
+  const int tid = threadIdx.x;
+  const TileDesc T = dp.tiles[0];
+  bool dense_self = false;
+  for (int i = dp.D_ptr[T.comm]; i < dp.D_ptr[T.comm + 1]; ++i) dense_self |= dp.D_idx[i] == T.comm;
+  double th[R], om[R], acc[R], zc[R], zsn[R], kn[R];
+  double x = 0.0, y = 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int lr = tid + k * NTHREADS;
+    const bool v = lr < T.nrows;
+    const int li = T.row0 + lr - dp.row_begin;
+    th[k] = v ? a.theta[li] : 0.0;
+    om[k] = v ? a.omega[li] : 0.0;
+    kn[k] = v ? (dp.rowscale ? a.K * dp.rowscale[li] : a.KN) : 0.0;
+    acc[k] = 0.0;
+    sincos(th[k], &zsn[k], &zc[k]);
+    if (v) {
+      x += zc[k];
+      y += zsn[k];
+    }
+  }
+  Ctrl* ct = dp.ctrl;
+  // block sum -> sS, order parameter (r, psi) = S_c / N, record when due
+  auto reduce = [&](bool record, long long step) {
+    block_sum2(x, y, red);
+    if (tid == 0) {
+      sS = make_double2(x, y);
+      const double cm = x / (double)dp.n, sm = y / (double)dp.n;
+      const double r = sqrt(cm * cm + sm * sm);
+      const double psi = r == 0.0 ? 0.0 : atan2(sm, cm);
+      ct->rpsi[0] = r;
+      ct->rpsi[1] = psi;
+      if (record && ct->record_every > 0 && ct->r_trace && step % ct->record_every == 0) {
+        const long long i = step / ct->record_every;
+        if (i < ct->nrec_cap) {
+          ct->r_trace[2 * i] = r;
+          ct->r_trace[2 * i + 1] = psi;
+        }
+      }
+    }
+    __syncthreads();
+    x = y = 0.0;
+  };
+  reduce(true, 0);
+  bool bad = false;
+  double thn[R];
+  for (long long n = 0; n < nsteps; ++n) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) thn[k] = th[k];
+#pragma unroll 1
+    for (int st = 1; st <= 4; ++st) {
+      const double2 Tc = dense_self ? sS : make_double2(0.0, 0.0);
+      const double wx = Tc.x + 0.0, wy = Tc.y + 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int lr = tid + k * NTHREADS;
+        if (lr >= T.nrows) break;
+        const double kk = om[k] + kn[k] * (zc[k] * wy - zsn[k] * wx);
+        double ts;
+        if (st == 1) {
+          acc[k] = kk;
+          ts = __dadd_rn(thn[k], __dmul_rn(a.h / 2.0, kk));
+        } else if (st == 2) {
+          acc[k] = __dadd_rn(acc[k], __dmul_rn(2.0, kk));
+          ts = __dadd_rn(thn[k], __dmul_rn(a.h / 2.0, kk));
+        } else if (st == 3) {
+          acc[k] = __dadd_rn(acc[k], __dmul_rn(2.0, kk));
+          ts = __dadd_rn(thn[k], __dmul_rn(a.h, kk));
+        } else {
+          ts = __dadd_rn(thn[k], __dmul_rn(a.h / 6.0, __dadd_rn(acc[k], kk)));
+          th[k] = ts;
+          bad |= !isfinite(ts);
+        }
+        sincos(ts, &zsn[k], &zc[k]);
+        x += zc[k];
+        y += zsn[k];
+      }
+      reduce(st == 4, n + 1);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int lr = tid + k * NTHREADS;
+    if (lr < T.nrows) a.theta[T.row0 + lr - dp.row_begin] = th[k];
+  }
+  if (bad) ct->nonfinite = 1;
+  if (tid == 0) ct->step = nsteps;
+}
+
 // world > 1: z of the non-local rows from the exchanged stage phases (the same
 // sincos the owner evaluated -> bitwise identical), and every tile partial.
 __global__ void k_unpack(const DevPlan dp, const double* __restrict__ xrecv, double2* __restrict__ zout,
@@ -1008,6 +1106,10 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
 
 cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, double2* zB, double2* TA, double2* TB,
                          long long nsteps, cudaStream_t s) {
+  if (!dp.has_parts && dp.ntiles == 1) {  // registers + shared-memory reductions only
+    k_small_dense<<<1, NTHREADS, 0, s>>>(dp, a, nsteps);
+    return cudaGetLastError();
+  }
   static std::atomic<uint64_t> attr_set{0};  // one bit per device
   int dev = 0;
   cudaGetDevice(&dev);
