@@ -170,6 +170,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile-rows", type=int, default=0, help="tuning: force the tile size (rows)")
     ap.add_argument("--hot-min", type=int, default=0, help="tuning: window staging threshold")
+    ap.add_argument("--remote-pass", default="auto", choices=["auto", "on", "off"],
+                    help="tuning: force the separate k_remote pass on/off")
     ap.add_argument("--peer-exchange", action="store_true",
                     help="N > 1: fused peer-store exchange from the stage kernel instead of ncclAllGather")
     ap.add_argument("--dense-threshold", type=float, default=-1.0,
@@ -194,15 +196,16 @@ def main():
     inst = kurgen.config(args.config)
     gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
+    rp = {"auto": None, "on": True, "off": False}[args.remote_pass]
     if world > 1:
         obj = [kur.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         g = kur.graph_build(inst, device=local, dist=(rank, world, obj[0], kur.DIST_PEER_EXCHANGE if
                                                       args.peer_exchange else 0), tile_rows=args.tile_rows,
-                            hot_min=args.hot_min, dense_threshold=args.dense_threshold)
+                            hot_min=args.hot_min, dense_threshold=args.dense_threshold, remote_pass=rp)
     else:
         g = kur.graph_build(inst, device=local, tile_rows=args.tile_rows, hot_min=args.hot_min,
-                            dense_threshold=args.dense_threshold)
+                            dense_threshold=args.dense_threshold, remote_pass=rp)
     build_s = time.perf_counter() - t0
     info = g.info
     th = g.local(g.to_internal(torch.from_numpy(inst.theta0).to(dev))).clone()
