@@ -57,7 +57,8 @@ typedef enum {
   KUR_ERR_SIZE_MISMATCH = 5,   /* pointer-array lengths inconsistent (e.g. idx_ptr not monotone) */
   KUR_ERR_OOM = 6,             /* host or device allocation failed */
   KUR_ERR_CUDA = 7,            /* a CUDA runtime error (message in kur_last_error) */
-  KUR_ERR_NCCL = 8,            /* an NCCL error (message in kur_last_error) */
+  KUR_ERR_NCCL = 8,            /* an NCCL error, or a fused peer exchange that timed out (message in
+                                  kur_last_error) */
   KUR_ERR_NONFINITE = 9,       /* a non-finite phase was produced by kur_step (see kur_check) */
   KUR_ERR_UNSUPPORTED = 10,    /* valid request this build does not support (message says why) */
   KUR_ERR_STEPSIZE = 11        /* kur_integrate_adaptive: a step of h_min was rejected, or max_trials
@@ -272,7 +273,8 @@ kur_status kur_potential(kur_graph *g, const double *theta, const double *omega,
                          void *stream);
 
 /* Synchronises `stream`; returns KUR_ERR_NONFINITE (and clears the flag) if a
- * previous kur_step produced a non-finite phase. */
+ * previous kur_step produced a non-finite phase, and KUR_ERR_NCCL if a fused
+ * peer-store exchange gave up waiting for another rank's record. */
 kur_status kur_check(kur_graph *g, void *stream);
 
 /* ---- Host-only plan introspection (no device needed; tests and tooling) ----
