@@ -225,8 +225,11 @@ kur_status kur_step_method(kur_graph *g, int32_t method, double *theta, const do
  * stream synchronisation per trial.  For each accepted step k < cap the host
  * arrays t_out[k], h_out[k] and rpsi_out[2k..2k+1] (the order parameter of the
  * accepted state) are written when non-NULL.  Errors: KUR_ERR_INVALID_ARG (bad
- * controls), KUR_ERR_STEPSIZE, KUR_ERR_NONFINITE (non-finite error estimate),
- * KUR_ERR_UNSUPPORTED for world > 1. */
+ * controls), KUR_ERR_STEPSIZE, KUR_ERR_NONFINITE (non-finite error estimate).
+ * Collective for world > 1 (the per-tile partials of all ranks are all-gathered
+ * and added on the host in global tile order, so every rank and every world size
+ * takes the same decisions); kur_group_integrate_adaptive drives in-process rank
+ * handles. */
 typedef struct {
   double t_end;            /* > 0 */
   double h0;               /* first trial step, > 0 */
@@ -239,6 +242,10 @@ typedef struct {
 kur_status kur_integrate_adaptive(kur_graph *g, double *theta, const double *omega, double K,
                                   const kur_adaptive_ctrl *ctrl, int64_t cap, double *t_out, double *h_out,
                                   double *rpsi_out, int64_t *n_accepted, int64_t *n_rejected, void *stream);
+kur_status kur_group_integrate_adaptive(kur_graph *const *g, int32_t world, double *const *theta,
+                                        const double *const *omega, double K, const kur_adaptive_ctrl *ctrl,
+                                        int64_t cap, double *t_out, double *h_out, double *rpsi_out,
+                                        int64_t *n_accepted, int64_t *n_rejected, void *stream);
 
 /* r_psi[2] = (r, psi) of the complex order parameter r e^{i psi} =
  * (1/N) sum_k e^{i theta_k} (psi = 0 when r = 0).  local (may be

@@ -49,6 +49,7 @@ struct kur_graph {
   int32_t C = 0;
   kur_graph_info_t info{};
   std::vector<int32_t> perm_host;
+  std::vector<int32_t> shard_tile0_host;  // [world+1] tile ranges of all ranks
   DevPlan dp{};
   // device allocations
   TileDesc* d_tiles = nullptr;
@@ -183,6 +184,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   g->n_local = P.row_end - P.row_begin;
   g->n_pad = ((P.n + 1 + WZ - 1) / WZ) * WZ + WZ;  // z[n..n_pad) stay zero (sentinels, window tails)
   g->perm_host = P.perm;
+  g->shard_tile0_host = P.shard_tile0;
   auto bail = [&](cudaError_t e, const char* what) {
     delete g;
     return e == cudaErrorMemoryAllocation ? fail(KUR_ERR_OOM, std::string(what) + ": out of device memory")
@@ -743,63 +745,105 @@ kur_status kur_step_method(kur_graph* g, int32_t method, double* theta, const do
                    (cudaStream_t)stream, method, fp_tol, fp_max_iter);
 }
 
-kur_status kur_integrate_adaptive(kur_graph* g, double* theta, const double* omega, double K,
-                                  const kur_adaptive_ctrl* c, int64_t cap, double* t_out, double* h_out,
-                                  double* rpsi_out, int64_t* n_accepted, int64_t* n_rejected, void* stream) {
-  if (!g || !c) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
-  if (g->world != 1) return fail(KUR_ERR_UNSUPPORTED, "kur_integrate_adaptive: single-GPU handles only");
-  if (g->n_local > 0 && (!theta || !omega)) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+}  // extern "C"
+
+namespace {
+// Variable-step RK4 over one handle (world 1), the in-process rank handles of a group, or one
+// rank of an NCCL job (collective).  The error estimate's per-tile partials of all ranks are
+// summed on the host in global tile order, so every rank (and every world size) takes the
+// same accept / step-size decisions.
+kur_status adaptive_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO>& io, double K,
+                         const kur_adaptive_ctrl* c, int64_t cap, double* t_out, double* h_out, double* rpsi_out,
+                         int64_t* n_accepted, int64_t* n_rejected, cudaStream_t s) {
+  if (!c) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  for (size_t r = 0; r < gs.size(); ++r)
+    if (gs[r]->n_local > 0 && (!io[r].theta || !io[r].omega)) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
   if (!(c->t_end > 0.0) || !std::isfinite(c->t_end) || !(c->h0 > 0.0) || !(c->h_min > 0.0) ||
       !(c->h_max >= c->h_min) || !std::isfinite(c->h_max) || !(c->atol >= 0.0) || !(c->rtol >= 0.0) ||
       !(c->atol + c->rtol > 0.0) || !(c->safety > 0.0) || !(c->fac_min > 0.0) || !(c->fac_min <= 1.0) ||
       !(c->fac_max >= 1.0) || !std::isfinite(c->fac_max) || c->max_trials < 1 || cap < 0)
     return fail(KUR_ERR_INVALID_ARG, "kur_integrate_adaptive: invalid controls");
   if (!std::isfinite(K)) return fail(KUR_ERR_INVALID_ARG, "K must be finite");
-  KUR_CUDA(cudaSetDevice(g->device));
-  cudaStream_t s = (cudaStream_t)stream;
-  const int64_t nl = g->n_local;
-  const int nt = g->dp.ntiles;
-  // trial buffers (y1, y2) and the per-tile error partials, owned by this call
-  double *y1 = nullptr, *y2 = nullptr, *tss = nullptr;
+  kur_graph* g0 = gs[0];
+  const int world = g0->world;
+  const bool nccl = g0->comm != nullptr;
+  if (world > 1 && !nccl && (int)gs.size() != world)
+    return fail(KUR_ERR_UNSUPPORTED, "this handle has world > 1 without NCCL: use kur_group_integrate_adaptive");
+  KUR_CUDA(cudaSetDevice(g0->device));
+  // per-rank trial buffers (y1, y2) and per-tile error partials, owned by this call; the NCCL
+  // case all-gathers the partials padded to the largest rank's tile count
+  int32_t xt = 0;
+  for (int32_t r = 0; r < world; ++r)
+    xt = std::max<int32_t>(xt, g0->shard_tile0_host[(size_t)r + 1] - g0->shard_tile0_host[(size_t)r]);
+  xt = std::max(xt, 1);
+  std::vector<double*> y1(gs.size(), nullptr), y2(gs.size(), nullptr), tss(gs.size(), nullptr);
+  double* gath = nullptr;
   auto cleanup = [&]() {
-    if (y1) cudaFree(y1);
-    if (y2) cudaFree(y2);
-    if (tss) cudaFree(tss);
+    for (size_t r = 0; r < gs.size(); ++r) {
+      if (y1[r]) cudaFree(y1[r]);
+      if (y2[r]) cudaFree(y2[r]);
+      if (tss[r]) cudaFree(tss[r]);
+    }
+    if (gath) cudaFree(gath);
   };
-  const size_t vb = sizeof(double) * (size_t)std::max<int64_t>(nl, 1);
-  cudaError_t e;
-  if ((e = cudaMalloc((void**)&y1, vb)) != cudaSuccess || (e = cudaMalloc((void**)&y2, vb)) != cudaSuccess ||
-      (e = cudaMalloc((void**)&tss, sizeof(double) * (size_t)std::max(nt, 1))) != cudaSuccess) {
+  cudaError_t e = cudaSuccess;
+  for (size_t r = 0; r < gs.size() && e == cudaSuccess; ++r) {
+    const size_t vb = sizeof(double) * (size_t)std::max<int64_t>(gs[r]->n_local, 1);
+    if ((e = cudaMalloc((void**)&y1[r], vb)) == cudaSuccess && (e = cudaMalloc((void**)&y2[r], vb)) == cudaSuccess &&
+        (e = cudaMalloc((void**)&tss[r], sizeof(double) * (size_t)xt)) == cudaSuccess)
+      e = cudaMemset(tss[r], 0, sizeof(double) * (size_t)xt);
+  }
+  if (e == cudaSuccess && nccl) e = cudaMalloc((void**)&gath, sizeof(double) * (size_t)xt * (size_t)world);
+  if (e != cudaSuccess) {
     cleanup();
     return e == cudaErrorMemoryAllocation ? fail(KUR_ERR_OOM, "kur_integrate_adaptive: out of device memory")
                                           : cuda_fail(e, "kur_integrate_adaptive");
   }
-  std::vector<double> hss((size_t)std::max(nt, 1));
-  std::vector<kur_graph*> gs{g};
+  std::vector<double> hss((size_t)xt * (size_t)world, 0.0);
+  std::vector<RankIO> io1(io), io2(io);
+  for (size_t r = 0; r < gs.size(); ++r) {
+    io1[r].theta = y1[r];
+    io2[r].theta = y2[r];
+  }
+  const std::vector<double*> no_trace(gs.size(), nullptr);
   double t = 0.0, h = c->h0, rpsi[2] = {0.0, 0.0};
   int64_t acc = 0, rej = 0, trials = 0;
-  kur_status st = KUR_OK;
   auto run = [&]() -> kur_status {
     while (t < c->t_end) {
       if (trials++ >= c->max_trials) return fail(KUR_ERR_STEPSIZE, "max_trials reached before t_end");
       const bool last = !(t + h < c->t_end - 1e-12 * h);  // the last step lands exactly on t_end
       const double hs = last ? c->t_end - t : h;
-      KUR_CUDA(cudaMemcpyAsync(y1, theta, sizeof(double) * (size_t)nl, cudaMemcpyDeviceToDevice, s));
-      kur_status r = step_impl(gs, {RankIO{y1, omega, nullptr, nullptr, nullptr}}, K, hs, 1, 0, {nullptr}, s);
-      if (r != KUR_OK) return r;
-      KUR_CUDA(cudaMemcpyAsync(y2, theta, sizeof(double) * (size_t)nl, cudaMemcpyDeviceToDevice, s));
-      r = step_impl(gs, {RankIO{y2, omega, nullptr, nullptr, nullptr}}, K, hs / 2.0, 2, 0, {nullptr}, s);
-      if (r != KUR_OK) return r;
-      KUR_CUDA(launch_errnorm(g->dp, y1, y2, c->atol, c->rtol, tss, s));
-      KUR_CUDA(cudaMemcpyAsync(hss.data(), tss, sizeof(double) * (size_t)nt, cudaMemcpyDeviceToHost, s));
-      KUR_CUDA(cudaMemcpyAsync(rpsi, g->ctrl->rpsi, sizeof(rpsi), cudaMemcpyDeviceToHost, s));  // (r, psi) of y2
+      for (size_t r = 0; r < gs.size(); ++r)
+        KUR_CUDA(cudaMemcpyAsync(y1[r], io[r].theta, sizeof(double) * (size_t)gs[r]->n_local, cudaMemcpyDeviceToDevice, s));
+      kur_status st = step_impl(gs, io1, K, hs, 1, 0, no_trace, s);
+      if (st != KUR_OK) return st;
+      for (size_t r = 0; r < gs.size(); ++r)
+        KUR_CUDA(cudaMemcpyAsync(y2[r], io[r].theta, sizeof(double) * (size_t)gs[r]->n_local, cudaMemcpyDeviceToDevice, s));
+      st = step_impl(gs, io2, K, hs / 2.0, 2, 0, no_trace, s);
+      if (st != KUR_OK) return st;
+      for (size_t r = 0; r < gs.size(); ++r) KUR_CUDA(launch_errnorm(gs[r]->dp, y1[r], y2[r], c->atol, c->rtol, tss[r], s));
+      if (nccl) {
+        ncclResult_t nr = ncclAllGather(tss[0], gath, (size_t)xt, ncclDouble, g0->comm, s);
+        if (nr != ncclSuccess) return fail(KUR_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
+        KUR_CUDA(cudaMemcpyAsync(hss.data(), gath, sizeof(double) * hss.size(), cudaMemcpyDeviceToHost, s));
+      } else {
+        for (size_t r = 0; r < gs.size(); ++r)
+          KUR_CUDA(cudaMemcpyAsync(hss.data() + r * (size_t)xt, tss[r], sizeof(double) * (size_t)xt,
+                                   cudaMemcpyDeviceToHost, s));
+      }
+      KUR_CUDA(cudaMemcpyAsync(rpsi, g0->ctrl->rpsi, sizeof(rpsi), cudaMemcpyDeviceToHost, s));  // (r, psi) of y2
       KUR_CUDA(cudaStreamSynchronize(s));
       double ss = 0.0;
-      for (int i = 0; i < nt; ++i) ss += hss[(size_t)i];  // fixed (tile) order
-      const double err = std::sqrt(ss / (double)g->n) / 15.0;
+      for (int32_t r = 0; r < world; ++r) {  // fixed global tile order
+        const int32_t ntr = g0->shard_tile0_host[(size_t)r + 1] - g0->shard_tile0_host[(size_t)r];
+        for (int32_t k = 0; k < ntr; ++k) ss += hss[(size_t)r * (size_t)xt + (size_t)k];
+      }
+      const double err = std::sqrt(ss / (double)g0->n) / 15.0;
       if (!std::isfinite(err)) return fail(KUR_ERR_NONFINITE, "non-finite error estimate in kur_integrate_adaptive");
       if (err <= 1.0) {
-        KUR_CUDA(cudaMemcpyAsync(theta, y2, sizeof(double) * (size_t)nl, cudaMemcpyDeviceToDevice, s));
+        for (size_t r = 0; r < gs.size(); ++r)
+          KUR_CUDA(cudaMemcpyAsync(io[r].theta, y2[r], sizeof(double) * (size_t)gs[r]->n_local,
+                                   cudaMemcpyDeviceToDevice, s));
         t = last ? c->t_end : t + hs;
         if (acc < cap) {
           if (t_out) t_out[acc] = t;
@@ -820,12 +864,39 @@ kur_status kur_integrate_adaptive(kur_graph* g, double* theta, const double* ome
     }
     return KUR_OK;
   };
-  st = run();
+  kur_status st = run();
   cudaStreamSynchronize(s);
   cleanup();
   if (n_accepted) *n_accepted = acc;
   if (n_rejected) *n_rejected = rej;
   return st;
+}
+}  // namespace
+
+extern "C" {
+
+kur_status kur_integrate_adaptive(kur_graph* g, double* theta, const double* omega, double K,
+                                  const kur_adaptive_ctrl* c, int64_t cap, double* t_out, double* h_out,
+                                  double* rpsi_out, int64_t* n_accepted, int64_t* n_rejected, void* stream) {
+  if (!g) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  std::vector<kur_graph*> gs{g};
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
+  return adaptive_impl(gs, {RankIO{theta, omega, nullptr, nullptr, nullptr}}, K, c, cap, t_out, h_out, rpsi_out,
+                       n_accepted, n_rejected, (cudaStream_t)stream);
+}
+
+kur_status kur_group_integrate_adaptive(kur_graph* const* g, int32_t world, double* const* theta,
+                                        const double* const* omega, double K, const kur_adaptive_ctrl* c,
+                                        int64_t cap, double* t_out, double* h_out, double* rpsi_out,
+                                        int64_t* n_accepted, int64_t* n_rejected, void* stream) {
+  if (!g || !theta || !omega || world < 1) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
+  std::vector<kur_graph*> gs(g, g + world);
+  kur_status st = check_group(gs);
+  if (st != KUR_OK) return st;
+  std::vector<RankIO> io;
+  for (int r = 0; r < world; ++r) io.push_back(RankIO{theta[r], omega[r], nullptr, nullptr, nullptr});
+  return adaptive_impl(gs, io, K, c, cap, t_out, h_out, rpsi_out, n_accepted, n_rejected, (cudaStream_t)stream);
 }
 
 kur_status kur_order_parameter(kur_graph* g, const double* theta, double* r_psi, double* local, void* stream) {

@@ -77,6 +77,8 @@ _lib.kur_group_rhs.argtypes = [_p, _i32, _p, _p, _d, _p, _p]
 _lib.kur_group_step.argtypes = [_p, _i32, _p, _p, _d, _d, _i64, _i32, _p, _p]
 _lib.kur_integrate_adaptive.argtypes = [_p, _p, _p, _d, ctypes.POINTER(AdaptiveCtrl), _i64, _p, _p, _p,
                                         ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p]
+_lib.kur_group_integrate_adaptive.argtypes = [_p, _i32, _p, _p, _d, ctypes.POINTER(AdaptiveCtrl), _i64, _p, _p, _p,
+                                              ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p]
 _lib.kur_step_method.argtypes = [_p, _i32, _p, _p, _d, _d, _i64, _i32, _p, _d, _i32, _p]
 _lib.kur_group_step_method.argtypes = [_p, _i32, _i32, _p, _p, _d, _d, _i64, _i32, _p, _d, _i32, _p]
 _lib.kur_status_string.restype = ctypes.c_char_p
@@ -85,13 +87,14 @@ _lib.kur_last_error.restype = ctypes.c_char_p
 for _f in ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
            "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id", "kur_timing",
            "kur_timing_read", "kur_group_rhs", "kur_group_step", "kur_potential", "kur_step_method",
-           "kur_group_step_method", "kur_integrate_adaptive"):
+           "kur_group_step_method", "kur_integrate_adaptive", "kur_group_integrate_adaptive"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ("kur_graph_build", "kur_graph_destroy", "kur_graph_info", "kur_graph_permutation", "kur_permute",
             "kur_rhs", "kur_step", "kur_order_parameter", "kur_check", "kur_nccl_unique_id",
             "kur_status_string", "kur_last_error", "kur_timing", "kur_timing_read", "kur_group_rhs",
-            "kur_group_step", "kur_potential", "kur_step_method", "kur_group_step_method", "kur_integrate_adaptive")
+            "kur_group_step", "kur_potential", "kur_step_method", "kur_group_step_method", "kur_integrate_adaptive",
+            "kur_group_integrate_adaptive")
 METHODS = {"rk4": 0, "euler": 1, "heun": 2, "implicit_midpoint": 3}
 
 
@@ -305,6 +308,24 @@ def integrate_adaptive(g: Graph, theta, omega, K, t_end, h0, cap=100000, stream=
                                        _dev_vec(omega, g.n_local, g.device, "omega"), float(K), ctypes.byref(cc),
                                        int(cap), _np_ptr(t_out), _np_ptr(h_out), _np_ptr(rp), ctypes.byref(acc),
                                        ctypes.byref(rej), _stream(stream)))
+    k = min(int(acc.value), cap)
+    return t_out[:k], h_out[:k], rp[:k], int(rej.value)
+
+
+def group_integrate_adaptive(graphs, thetas, omegas, K, t_end, h0, cap=100000, stream=None, **ctrl):
+    """kur_group_integrate_adaptive on per-rank local-row device tensors (in place)."""
+    c = dict(ADAPTIVE_DEFAULTS, **ctrl)
+    cc = AdaptiveCtrl(t_end=float(t_end), h0=float(h0), h_min=float(c["h_min"]), h_max=float(c["h_max"]),
+                      atol=float(c["atol"]), rtol=float(c["rtol"]), safety=float(c["safety"]),
+                      fac_min=float(c["fac_min"]), fac_max=float(c["fac_max"]), max_trials=int(c["max_trials"]))
+    t_out, h_out, rp = np.zeros(cap), np.zeros(cap), np.zeros((cap, 2))
+    acc, rej = _i64(0), _i64(0)
+    hs = _ptr_array([g._h for g in graphs])
+    th = _ptr_array([_dev_vec(t, g.n_local, g.device, "theta").value for g, t in zip(graphs, thetas)])
+    om = _ptr_array([_dev_vec(o, g.n_local, g.device, "omega").value for g, o in zip(graphs, omegas)])
+    _check(_lib.kur_group_integrate_adaptive(hs, len(graphs), th, om, float(K), ctypes.byref(cc), int(cap),
+                                             _np_ptr(t_out), _np_ptr(h_out), _np_ptr(rp), ctypes.byref(acc),
+                                             ctypes.byref(rej), _stream(stream)))
     k = min(int(acc.value), cap)
     return t_out[:k], h_out[:k], rp[:k], int(rej.value)
 

@@ -70,3 +70,23 @@ def test_adaptive_errors():
     with pytest.raises(kur.KurError) as e:  # impossible tolerance with a large h_min
         kur.integrate_adaptive(run.g, th, run.omega_int, 50.0, 1.0, 0.5, atol=1e-15, rtol=0.0, h_min=0.25)
     assert e.value.status == 11
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_adaptive_group_bitwise(peer):
+    """Sharded variable-step RK4 (world 3): the same accepted steps and bitwise the same state as world 1."""
+    inst = kurgen.sbm([3000, 500, 2000, 77], np.array(
+        [[0.95, 0.01, 0.0, 0.6], [0.01, 0.3, 0.02, 0.0], [0.0, 0.02, 0.97, 0.1], [0.6, 0.0, 0.1, 0.5]]), 29,
+        K=3.0)
+    g1 = kur.graph_build(inst)
+    full = g1.to_internal(torch.from_numpy(inst.theta0).cuda())
+    omf = g1.to_internal(torch.from_numpy(inst.omega).cuda())
+    th1 = full.clone()
+    t1, h1, rp1, rej1 = kur.integrate_adaptive(g1, th1, omf, inst.K, 0.3, 0.05, atol=1e-8, rtol=1e-8)
+    gs = kur.group_build(inst, 3, peer_exchange=peer)
+    ths = [full[g.row_begin:g.row_end].clone() for g in gs]
+    oms = [omf[g.row_begin:g.row_end].clone() for g in gs]
+    t3, h3, rp3, rej3 = kur.group_integrate_adaptive(gs, ths, oms, inst.K, 0.3, 0.05, atol=1e-8, rtol=1e-8)
+    torch.cuda.synchronize()
+    assert rej3 == rej1 and np.array_equal(t3, t1) and np.array_equal(h3, h1) and np.array_equal(rp3, rp1)
+    assert torch.equal(torch.cat(ths), th1)
