@@ -141,7 +141,7 @@ typedef struct {
   int64_t row_begin, row_end;  /* this rank's internal rows */
   int64_t nnz;                 /* ones of A, diagonal excluded (direct-CSR entry count) */
   int64_t n_idx;               /* stored list entries (complements + non-zeros), this rank */
-  int64_t n_idx_hot;           /* of which gathered from shared-memory windows (16-bit) */
+  int64_t n_idx_hot;           /* of which gathered from shared-memory windows (13-bit slots) */
   int64_t n_idx_remote;        /* of which gathered from global memory (32-bit) */
   int64_t n_slots_hot;         /* hot slots incl. padding */
   int64_t n_slots_remote;      /* remote slots incl. padding */

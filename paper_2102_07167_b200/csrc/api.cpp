@@ -409,9 +409,9 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   I.n_hot_parts = P.n_hot_parts;
   I.sincos_per_rhs = g->n_local;
   // algorithmic bytes of one fused RK stage (= one RHS evaluation), DESIGN.md §5:
-  // index stream (2 B per hot entry, 4 B per remote entry, no padding) plus per
+  // index stream (13 bits per hot entry, 4 B per remote entry, no padding) plus per
   // local row z_in 16 + z_out 16 + omega 8 + theta_n 8 + acc 16 = 64 B.
-  I.bytes_per_rhs = 2 * P.n_idx_hot + 4 * P.n_idx_remote + 64 * g->n_local;
+  I.bytes_per_rhs = (13 * P.n_idx_hot + 7) / 8 + 4 * P.n_idx_remote + 64 * g->n_local;
   I.bytes_pool = pool_bytes;
   I.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   I.remote_pass = dp.has_remote;
@@ -1083,13 +1083,25 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
   const int64_t nl = P.row_end - P.row_begin;
   struct E { int32_t row, col; int8_t neg; };
   std::vector<E> ents;
-  // hot chunk layout (plan.h): cd.ng half-groups of 4 slots per lane; full groups of 8
-  // 16-bit slots (16 bytes per lane), then one trailing half-group (8 bytes per lane) if odd
+  // hot chunk layout (plan.h): cd.ng = (G << 1) | tail; G groups of 9 positions as 13-bit slots
+  // packed in 16 bytes per lane, then (tail) 4 positions as 16-bit slots in 8 bytes per lane
+  auto hot_npos = [&](const ChunkDesc& cd) -> uint32_t { return 9 * (cd.ng >> 1) + 4 * (cd.ng & 1); };
   auto hot_slot = [&](const ChunkDesc& cd, int l, uint32_t pos) -> uint32_t {
-    const uint16_t* s16 = reinterpret_cast<const uint16_t*>(&P.pool[(size_t)cd.ofs + HDR_UNITS]);
-    const uint32_t g = pos / 8, full = cd.ng / 2;
-    const int ne = g < full ? 8 : 4;
-    return s16[(size_t)g * 256 + (size_t)l * ne + pos % 8];
+    const uint32_t G = cd.ng >> 1;
+    if (pos < 9 * G) {
+      const Unit& U = P.pool[(size_t)cd.ofs + HDR_UNITS + (size_t)(pos / 9) * 32 + (size_t)l];
+      uint64_t lo, hi;
+      std::memcpy(&lo, U.w, 8);
+      std::memcpy(&hi, U.w + 2, 8);
+      const int off = 13 * (int)(pos % 9);
+      uint64_t v;
+      if (off + 13 <= 64) v = lo >> off;
+      else if (off >= 64) v = hi >> (off - 64);
+      else v = (lo >> off) | (hi << (64 - off));
+      return (uint32_t)(v & 0x1FFF);
+    }
+    const uint16_t* t16 = reinterpret_cast<const uint16_t*>(&P.pool[(size_t)cd.ofs + HDR_UNITS + (size_t)G * 32]);
+    return t16[(size_t)l * 4 + (pos - 9 * G)];
   };
   for (const TileDesc& T : P.tiles) {
     for (int pi = T.part0; pi < T.part0 + T.nparts; ++pi) {
@@ -1109,8 +1121,8 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
               return fail(KUR_ERR_INVALID_ARG, "plan: bad chunk header");
             seen[lr] = 1;
           }
-          // hot: cd.ng half-groups of 4 slots; remote: cd.ng groups of 4 32-bit columns
-          for (uint32_t pos = 0; pos < 4 * cd.ng; ++pos) {
+          // hot: hot_npos positions; remote: cd.ng groups of 4 32-bit columns
+          for (uint32_t pos = 0; pos < (hot ? hot_npos(cd) : 4 * cd.ng); ++pos) {
             {
               int64_t col;
               int8_t eneg = (int8_t)(pd.neg & 1);
@@ -1132,7 +1144,7 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
           }
         }
         if (hot) {  // bank-conflict freedom: distinct slot residues per quarter-warp position
-          for (uint32_t pos = 0; pos < 4 * cd.ng; ++pos)
+          for (uint32_t pos = 0; pos < hot_npos(cd); ++pos)
             for (int qw = 0; qw < 4; ++qw) {
               int mask = 0;
               for (int l = qw * 8; l < qw * 8 + 8; ++l) {

@@ -714,23 +714,40 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
             }
             // H half-groups of 4 positions: H/2 full groups of 8 slots (uint4 per lane), then one
             // trailing half-group (uint2 per lane) when H is odd
-            const uint32_t ng = (uint32_t)((L + 3) / 4);
-            cd.ng = ng;
-            const uint32_t full = ng / 2;
-            O.units.resize(gbase + (size_t)full * 32 + (ng & 1u) * 16);
-            uint16_t* slots16 = reinterpret_cast<uint16_t*>(O.units.data() + gbase);
-            for (uint32_t g = 0; g < (ng + 1) / 2; ++g)
+            // G full groups of 9 positions (13-bit slots packed in 16 bytes per lane), then an
+            // optional tail of 4 positions (16-bit slots, 8 bytes per lane): L rounded up to 9G or 9G + 4
+            uint32_t G = (uint32_t)(L / 9), tail = 0;
+            const size_t rem = L - (size_t)G * 9;
+            if (rem > 4) ++G;
+            else if (rem > 0) tail = 1;
+            cd.ng = (G << 1) | tail;
+            O.units.resize(gbase + (size_t)G * 32 + tail * 16);
+            auto slot_at = [&](int lane, size_t p) -> uint32_t {
+              const std::vector<uint32_t>& P8 = qpos[(size_t)(lane / 8)];
+              return p < P8.size() / 8 ? P8[p * 8 + (size_t)(lane & 7)] : HOT_SENT + (uint32_t)(lane & 7);
+            };
+            for (uint32_t g = 0; g < G; ++g)
               for (int lane = 0; lane < 32; ++lane) {
-                const std::vector<uint32_t>& P8 = qpos[(size_t)(lane / 8)];
-                const size_t npos = P8.size() / 8;
-                const int ne = g < full ? 8 : 4;  // the trailing half-group holds 4 slots per lane
-                for (int e = 0; e < ne; ++e) {
-                  const size_t p = (size_t)g * 8 + (size_t)e;
-                  slots16[(size_t)g * 256 + (size_t)lane * ne + (size_t)e] =
-                      p < npos ? (uint16_t)P8[p * 8 + (size_t)(lane & 7)] : (uint16_t)(HOT_SENT + (uint32_t)(lane & 7));
+                uint64_t lo = 0, hi = 0;
+                for (int e = 0; e < 9; ++e) {
+                  const uint64_t v = slot_at(lane, (size_t)g * 9 + (size_t)e);
+                  const int off = 13 * e;
+                  if (off + 13 <= 64) lo |= v << off;
+                  else if (off >= 64) hi |= v << (off - 64);
+                  else {
+                    lo |= v << off;
+                    hi |= v >> (64 - off);
+                  }
                 }
+                std::memcpy(O.units[gbase + (size_t)g * 32 + (size_t)lane].w, &lo, 8);
+                std::memcpy(O.units[gbase + (size_t)g * 32 + (size_t)lane].w + 2, &hi, 8);
               }
-            O.shot += (int64_t)ng * 128;
+            if (tail) {
+              uint16_t* t16 = reinterpret_cast<uint16_t*>(O.units.data() + gbase + (size_t)G * 32);
+              for (int lane = 0; lane < 32; ++lane)
+                for (int e = 0; e < 4; ++e) t16[(size_t)lane * 4 + (size_t)e] = (uint16_t)slot_at(lane, (size_t)G * 9 + (size_t)e);
+            }
+            O.shot += (int64_t)(9 * G + 4 * tail) * 32;
           } else {
             int mx = 0;
             for (int l = 0; l < 32; ++l)

@@ -154,20 +154,34 @@ __device__ __forceinline__ double block_max(double d, double* red) {
   return d;
 }
 
-// Sum of the 8 window-local z entries named by one 16-byte unit (P:557-570:
-// complement or non-zero entries; the part's sign is applied by the caller).
-__device__ __forceinline__ void hot8(const uint4 v, const double2* zs, double& x0, double& y0,
+// Sum of the 9 window-local z entries named by one 16-byte unit of 13-bit slots
+// (complement or non-zero entries; the part's sign is applied by the
+// caller).  Slot e sits at bits 13e..13e+12 of the 128-bit unit; each field is
+// extracted directly as a byte offset (slot * 16) into the window.
+__device__ __forceinline__ void hot9(const uint4 v, const double2* zs, double& x0, double& y0,
                                      double& x1, double& y1) {
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  constexpr uint32_t M = 0x1FFF0u;
+  const uint32_t o[9] = {(v.x << 4) & M,
+                         (v.x >> 9) & M,
+                         __funnelshift_r(v.x, v.y, 22) & M,
+                         (v.y >> 3) & M,
+                         __funnelshift_r(v.y, v.z, 16) & M,
+                         (v.z << 3) & M,
+                         (v.z >> 10) & M,
+                         __funnelshift_r(v.z, v.w, 23) & M,
+                         (v.w >> 4) & M};
+  const char* zb = reinterpret_cast<const char*>(zs);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    KUR_ASSERT((w[q] & 0xFFFFu) < WZ + 8 && (w[q] >> 16) < WZ + 8);
-    const double2 a = zs[w[q] & 0xFFFFu];
-    const double2 b = zs[w[q] >> 16];
-    x0 += a.x;
-    y0 += a.y;
-    x1 += b.x;
-    y1 += b.y;
+  for (int e = 0; e < 9; ++e) {
+    KUR_ASSERT((o[e] >> 4) < WZ + 8);
+    const double2 a = *reinterpret_cast<const double2*>(zb + o[e]);
+    if (e & 1) {
+      x1 += a.x;
+      y1 += a.y;
+    } else {
+      x0 += a.x;
+      y0 += a.y;
+    }
   }
 }
 
@@ -223,9 +237,10 @@ __device__ __forceinline__ void rem4(const uint4 v, const double2* __restrict__ 
   y1 += d.y;
 }
 
-// Hot part of one chunk: H half-groups of 4 slots per lane starting at base (the
-// chunk's first group, no lane offset): H/2 full groups of 32 16-byte units, then
-// one trailing group of 32 8-byte units when H is odd.  Rotating software
+// Hot part of one chunk starting at base (the chunk's first group, no lane
+// offset), H = (G << 1) | tail: G full groups of 32 16-byte units (9 13-bit slots
+// per lane), then one trailing group of 32 8-byte units (4 16-bit slots per
+// lane) when tail is set.  Rotating software
 // pipeline: the unit of group g+4 is requested before group g is gathered, so
 // four 16-byte index loads per lane are always in flight and there is no serial
 // tail (loads past the last group are predicated off).
@@ -245,19 +260,19 @@ __device__ __forceinline__ void run_hot(const uint4* __restrict__ base, uint32_t
     const uint4* qn = q + (size_t)(g + 4) * 32;
     uint4 c = b0;
     if (g + 4 < ng) b0 = ldg_stream(qn, pol);
-    hot8(c, zs, x0, y0, x1, y1);
+    hot9(c, zs, x0, y0, x1, y1);
     if (g + 1 >= ng) break;
     c = b1;
     if (g + 5 < ng) b1 = ldg_stream(qn + 32, pol);
-    hot8(c, zs, x0, y0, x1, y1);
+    hot9(c, zs, x0, y0, x1, y1);
     if (g + 2 >= ng) break;
     c = b2;
     if (g + 6 < ng) b2 = ldg_stream(qn + 64, pol);
-    hot8(c, zs, x0, y0, x1, y1);
+    hot9(c, zs, x0, y0, x1, y1);
     if (g + 3 >= ng) break;
     c = b3;
     if (g + 7 < ng) b3 = ldg_stream(qn + 96, pol);
-    hot8(c, zs, x0, y0, x1, y1);
+    hot9(c, zs, x0, y0, x1, y1);
   }
   if (H & 1u) hot4(tail, zs, x0, y0, x1, y1);
   sx = x0 + x1;

@@ -23,10 +23,10 @@
 // 64-byte header (32 x uint16 local row ids, 0xFFFF = empty lane) followed by
 // the lane-interleaved entries.  Remote chunks: ng groups of 32 16-byte units,
 // unit (g, lane) = the lane's 32-bit columns at positions 4g..4g+3.  Hot chunks:
-// ng counts HALF-groups of 4 positions; ng/2 full groups of 32 16-byte units
-// (unit (g, lane) = 16-bit slots at positions 8g..8g+7), then, if ng is odd, one
-// trailing group of 32 8-byte units (positions 8(ng/2)..+3), so a chunk's length
-// is rounded up to 4 positions, not 8.  In hot parts the entries of
+// ng = (G << 1) | tail; G full groups of 32 16-byte units (unit (g, lane) = nine
+// 13-bit slots at positions 9g..9g+8, slot e in bits 13e..13e+12), then, if tail
+// is set, one trailing group of 32 8-byte units (four 16-bit slots at positions
+// 9G..9G+3), so a chunk's length is rounded up to 9G or 9G + 4 positions.  In hot parts the entries of
 // every quarter-warp (lanes 8q..8q+7) at one position have pairwise distinct
 // slot residues mod 8, i.e. they hit distinct 16-byte shared-memory bank
 // groups: every LDS.128 of the gather loop is bank-conflict free.  Padding
