@@ -263,3 +263,20 @@ def test_canonical_part_order(world):
         seen_remote_first |= nparts > nhot
     assert seen_remote_first  # the instance exercises the remote part
     assert any(t[5] > 0 for t in out["tiles"]) and any(t[4] > t[5] for t in out["tiles"])
+
+
+def test_hot_chunk_lengths_every_remainder():
+    """Hot chunks hold 9 positions per 16-byte unit plus an optional 4-position tail
+    (plan.h): rows of 1..27 entries inside one staged window hit every remainder
+    mod 9 and both tail cases; the exported layout must still decode to A."""
+    n = 27 * 32
+    rng = np.random.default_rng(913)
+    A = np.zeros((n, n), np.uint8)
+    for j in range(n):
+        L = 1 + (j % 27)
+        cols = rng.choice(np.delete(np.arange(n), j), size=L, replace=False)
+        A[j, cols] = 1
+    inst = kurgen.from_dense(A, np.zeros(n, np.int64), kind="ones")
+    plan = check_plan(inst, A, hot_min=1)
+    assert plan["idx_hot"] == int(A.sum())
+    assert plan["slots_hot"] >= plan["idx_hot"]

@@ -115,3 +115,17 @@ def test_ragged_tile_tails(n):
     inst = kurgen.sbm([n // 2, n - n // 2], [[0.93, 0.03], [0.03, 0.6]], n, K=2.0)
     for kw in ({}, {"tile_rows": 512}):
         _check(inst, **kw)
+
+
+@pytest.mark.parametrize("kind", ["ones", "zeros"])
+def test_hot_chunk_lengths_every_remainder(kind):
+    """Rows of 1..27 entries (non-zero or complement lists) inside one staged window:
+    every remainder mod 9 of the 13-bit slot groups and both tail cases (plan.h)."""
+    n = 27 * 32
+    rng = np.random.default_rng(914)
+    A = np.zeros((n, n), np.uint8) if kind == "ones" else np.ones((n, n), np.uint8)
+    for j in range(n):
+        cols = rng.choice(np.delete(np.arange(n), j), size=1 + (j % 27), replace=False)
+        A[j, cols] = 1 if kind == "ones" else 0
+    inst = kurgen.from_dense(A, np.zeros(n, np.int64), kind=kind, seed=5, K=3.0)
+    _check(inst, hot_min=1)
