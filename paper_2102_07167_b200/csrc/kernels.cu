@@ -638,7 +638,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
                      "r"((uint32_t)(WZ * sizeof(double2)))
                      : "memory");
     }
-    run_part<SMALL>(dp, P, hot, zs, a.zin, Ws, pol, warp, lane);
+    run_part<SMALL, !SMALL>(dp, P, hot, zs, a.zin, Ws, pol, warp, lane);
     if (!SMALL) PROF_W(pi, warp);
     __syncthreads();
     if (!SMALL && pi < 8) PROF_T(3 + 3 * pi);
