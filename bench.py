@@ -319,7 +319,7 @@ def main():
         ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ee0.record(stream)
         for _ in range(ne):
-            rt = kur.step(g, th_hi, om, K, h, 1, 1)  # H2D theta, 1 RK4 step, D2H theta and (r, psi)
+            rt = kur.step(g, th_hi, om, K, h, 1, 1)  # host theta in, 1 RK4 step, theta out (C ABI)
             rt_h.copy_(rt)
         ee1.record(stream)
         torch.cuda.synchronize()
@@ -331,8 +331,9 @@ def main():
         # value: global RHS evaluations per second (strong scaling); bytes: all ranks' copies
         e2e = {"value": 4.0 / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * inst.n,
                "d2h_bytes_per_step": 8 * inst.n + 32 * world, "ms_per_step": e_ms, "steps": ne,
-               "path": "kur.step(host pinned theta): H2D theta + kur_step(nsteps=1) + D2H theta and (r, psi); "
-                       "omega and the graph resident (model parameters)"}
+               "path": "kur_step on the pinned HOST theta buffer: the library copies theta in, runs one RK4 step "
+                       "and its last stage stores theta_{n+1} back through the buffer's device mapping; "
+                       "then D2H of (r, psi); omega and the graph resident (model parameters)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

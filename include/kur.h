@@ -186,7 +186,15 @@ kur_status kur_rhs(kur_graph *g, const double *theta, const double *omega, doubl
  * (r, psi) of theta_n is written to r_trace[2*(n/record_every)]
  * for every n = 0, record_every, 2*record_every, ... <= nsteps
  * (floor(nsteps/record_every)+1 pairs, replicated on every rank).
- * A non-finite phase raises a device flag reported by kur_check. */
+ * A non-finite phase raises a device flag reported by kur_check.
+ * Host buffers (world == 1): theta and/or omega may be HOST memory (pinned or
+ * pageable).  The library then copies them into device buffers it owns, runs
+ * the same kernels, and stores theta_{n+1} back into the host theta: for
+ * pinned memory the last step's final stage writes it through the buffer's
+ * device mapping (the device-to-host transfer overlaps that stage), otherwise
+ * one copy follows the steps.  The host result is complete when the stream is
+ * synchronised; it is bitwise the device-buffer result.  Same for
+ * kur_step_method.  KUR_ERR_UNSUPPORTED for host buffers with world > 1. */
 kur_status kur_step(kur_graph *g, double *theta, const double *omega, double K, double h,
                     int64_t nsteps, int32_t record_every, double *r_trace, void *stream);
 

@@ -60,6 +60,8 @@ struct kur_graph {
   int32_t *d_comm_tile0 = nullptr, *d_D_ptr = nullptr, *d_D_idx = nullptr, *d_csize = nullptr, *d_perm = nullptr;
   double2 *zA = nullptr, *zB = nullptr, *TA = nullptr, *TB = nullptr, *S = nullptr, *partial = nullptr;
   double* acc = nullptr;
+  double *theta_ws = nullptr, *omega_ws = nullptr;  // host-buffer kur_step: device copies of theta / omega
+  double* host_out = nullptr;  // device mapping of the caller's pinned theta for the final stage, or NULL
   double* pmax = nullptr;
   double2* Wr = nullptr;
   uint32_t* d_rchunks = nullptr;
@@ -104,7 +106,7 @@ struct kur_graph {
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
                     xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh, d_rchunks, d_rem_lp, d_flag, d_xticket,
-                    d_peer_x, d_peer_flag};
+                    d_peer_x, d_peer_flag, theta_ws, omega_ws};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -523,6 +525,7 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
     }
     a.Wh = g->Wh;
     a.xpar = (int)((g->xepoch + 1) & 1u);  // parity of the exchange this phase produces
+    a.theta_host = (mode == MODE_S4 || mode == MODE_E1 || mode == MODE_H2) ? g->host_out : nullptr;
   }
   if (world > 1 && mode != PH_PROLOGUE) {
     // phase A: own-community hot parts (local z only) -> Wh, while the previous stage's
@@ -647,7 +650,8 @@ kur_status rhs_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO>
 
 kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO>& io, double K, double h,
                      int64_t nsteps, int32_t record_every, const std::vector<double*>& r_trace, cudaStream_t s,
-                     int method = KUR_RK4, double fp_tol = 0.0, int32_t fp_max_iter = 0) {
+                     int method = KUR_RK4, double fp_tol = 0.0, int32_t fp_max_iter = 0,
+                     double* host_out = nullptr) {
   if (method < KUR_RK4 || method > KUR_IMPLICIT_MIDPOINT) return fail(KUR_ERR_INVALID_ARG, "unknown method");
   if (method == KUR_IMPLICIT_MIDPOINT && (!(fp_tol >= 0.0) || !std::isfinite(fp_tol) || fp_max_iter < 1))
     return fail(KUR_ERR_INVALID_ARG, "implicit midpoint needs fp_tol >= 0 (finite) and fp_max_iter >= 1");
@@ -688,6 +692,7 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
     return r;
   };
   for (int64_t n = 0; n < nsteps && st == KUR_OK; ++n) {
+    if (host_out && n + 1 == nsteps) gs[0]->host_out = host_out;  // the last step's final stage stores it
     switch (method) {
       case KUR_RK4:
         for (int m = MODE_S1; m <= MODE_S4 && st == KUR_OK; ++m) st = stage(m, m == MODE_S4 ? REC_STEP : REC_NONE);
@@ -707,8 +712,62 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
         break;
     }
   }
+  gs[0]->host_out = nullptr;
   if (st == KUR_OK) st = join_exchange(gs, s);
   return st;
+}
+
+// kur_step / kur_step_method with theta (and possibly omega) in HOST memory (one handle,
+// world 1): theta is copied into the handle's device buffer, the steps run there, and
+// theta_{n+1} goes back -- for pinned (page-locked, device-mapped) memory stored by the
+// last step's final stage itself through the mapping, so the device-to-host transfer
+// overlaps that stage; otherwise (pageable memory, the implicit midpoint commit, the
+// single-CTA path) with one copy after the steps.
+int mem_kind(const void* p) {  // 0 device / managed, 1 pinned host, 2 pageable host
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 2;
+  }
+  if (at.type == cudaMemoryTypeHost) return at.devicePointer ? 1 : 2;
+  return at.type == cudaMemoryTypeUnregistered ? 2 : 0;
+}
+
+kur_status host_step(kur_graph* g, int method, double* theta, const double* omega, double K, double h,
+                     int64_t nsteps, int32_t record_every, double* r_trace, cudaStream_t s, double fp_tol,
+                     int32_t fp_max_iter, bool* handled) {
+  *handled = false;
+  if (g->n_local == 0 || !theta || !omega) return KUR_OK;
+  KUR_CUDA(cudaSetDevice(g->device));
+  const int kt = mem_kind(theta), ko = mem_kind(omega);
+  if (kt == 0 && ko == 0) return KUR_OK;
+  *handled = true;
+  if (g->world > 1) return fail(KUR_ERR_UNSUPPORTED, "host theta/omega buffers need world == 1");
+  const size_t bytes = sizeof(double) * (size_t)g->n_local;
+  double* th = theta;
+  if (kt != 0) {
+    if (!g->theta_ws && cudaMalloc(&g->theta_ws, bytes) != cudaSuccess) return fail(KUR_ERR_OOM, "theta buffer");
+    th = g->theta_ws;
+    KUR_CUDA(cudaMemcpyAsync(th, theta, bytes, cudaMemcpyHostToDevice, s));
+  }
+  const double* om = omega;
+  if (ko != 0) {
+    if (!g->omega_ws && cudaMalloc(&g->omega_ws, bytes) != cudaSuccess) return fail(KUR_ERR_OOM, "omega buffer");
+    KUR_CUDA(cudaMemcpyAsync(g->omega_ws, omega, bytes, cudaMemcpyHostToDevice, s));
+    om = g->omega_ws;
+  }
+  double* mapped = nullptr;
+  if (kt == 1 && !g->small && method != KUR_IMPLICIT_MIDPOINT && nsteps > 0) {
+    cudaPointerAttributes at{};
+    KUR_CUDA(cudaPointerGetAttributes(&at, theta));
+    mapped = static_cast<double*>(at.devicePointer);
+  }
+  std::vector<kur_graph*> gs{g};
+  kur_status st = step_impl(gs, {RankIO{th, om, nullptr, nullptr, nullptr}}, K, h, nsteps, record_every, {r_trace},
+                            s, method, fp_tol, fp_max_iter, mapped);
+  if (st != KUR_OK) return st;
+  if (kt != 0 && !mapped && nsteps > 0) KUR_CUDA(cudaMemcpyAsync(theta, th, bytes, cudaMemcpyDeviceToHost, s));
+  return KUR_OK;
 }
 
 }  // namespace
@@ -730,6 +789,10 @@ kur_status kur_step(kur_graph* g, double* theta, const double* omega, double K, 
   std::vector<kur_graph*> gs{g};
   kur_status st = check_group(gs);
   if (st != KUR_OK) return st;
+  bool handled;
+  st = host_step(g, KUR_RK4, theta, omega, K, h, nsteps, record_every, r_trace, (cudaStream_t)stream, 0.0, 0,
+                 &handled);
+  if (handled) return st;
   return step_impl(gs, {RankIO{theta, omega, nullptr, nullptr, nullptr}}, K, h, nsteps, record_every, {r_trace},
                    (cudaStream_t)stream);
 }
@@ -741,6 +804,11 @@ kur_status kur_step_method(kur_graph* g, int32_t method, double* theta, const do
   std::vector<kur_graph*> gs{g};
   kur_status st = check_group(gs);
   if (st != KUR_OK) return st;
+  if (method < KUR_RK4 || method > KUR_IMPLICIT_MIDPOINT) return fail(KUR_ERR_INVALID_ARG, "unknown method");
+  bool handled;
+  st = host_step(g, method, theta, omega, K, h, nsteps, record_every, r_trace, (cudaStream_t)stream, fp_tol,
+                 fp_max_iter, &handled);
+  if (handled) return st;
   return step_impl(gs, {RankIO{theta, omega, nullptr, nullptr, nullptr}}, K, h, nsteps, record_every, {r_trace},
                    (cudaStream_t)stream, method, fp_tol, fp_max_iter);
 }

@@ -692,10 +692,12 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       } else if (MODE == MODE_S4) {  // theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
         ts = __dadd_rn(thn, __dmul_rn(a.h / 6.0, __dadd_rn(a.acc[li], k)));
         a.theta[li] = ts;
+        if (a.theta_host) a.theta_host[li] = ts;
         bad |= !isfinite(ts);
       } else if (MODE == MODE_E1) {  // explicit Euler: theta_{n+1} = theta_n + h k
         ts = __dadd_rn(thn, __dmul_rn(a.h, k));
         a.theta[li] = ts;
+        if (a.theta_host) a.theta_host[li] = ts;
         bad |= !isfinite(ts);
       } else if (MODE == MODE_H1) {  // Heun: k1, stage state theta_n + h k1
         a.acc[li] = k;
@@ -703,6 +705,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       } else if (MODE == MODE_H2) {  // theta_{n+1} = theta_n + (h/2)(k1 + k2)
         ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, __dadd_rn(a.acc[li], k)));
         a.theta[li] = ts;
+        if (a.theta_host) a.theta_host[li] = ts;
         bad |= !isfinite(ts);
       } else {  // MODE_M0 / MODE_MI: implicit midpoint fixed point on tp (kept in acc)
         const double nv = __dadd_rn(thn, __dmul_rn(a.h, k));

@@ -103,6 +103,9 @@ struct StageArgs {
                           // the previous exchange) / PHASE_B (Wh + the rest of the tile, finalize)
   double2* Wh;            // [local rows] phase-A row sums (world > 1)
   int xpar;               // fused exchange: receive half (exchange parity) this launch stores into
+  double* theta_host;     // final stages (S4, E1, H2): theta_{n+1} also stored here -- the device
+                          // mapping of the caller's pinned host buffer (end-to-end path: the
+                          // device-to-host copy rides on the stage) -- or NULL
 };
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);

@@ -131,6 +131,16 @@ def _dev_vec(x, n, device, name):
     return ctypes.c_void_p(x.data_ptr())
 
 
+def _dev_or_host_vec(x, n, device, name):
+    """A device vector as _dev_vec, or a contiguous CPU float64 tensor (host buffer: kur_step
+    copies it in and back itself; pinned memory gets the result stored by the final stage)."""
+    if isinstance(x, torch.Tensor) and not x.is_cuda:
+        if x.dtype != torch.float64 or not x.is_contiguous() or x.numel() != n:
+            raise ValueError(f"{name} must be a contiguous float64 tensor with {n} entries")
+        return ctypes.c_void_p(x.data_ptr())
+    return _dev_vec(x, n, device, name)
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(_lib.kur_nccl_unique_id(buf))
@@ -252,26 +262,21 @@ def rhs(g: Graph, theta, omega, K, out=None, stream=None):
 def step(g: Graph, theta, omega, K, h, nsteps, record_every=0, r_trace=None, stream=None, check=False):
     """nsteps RK4 steps in place on theta (this rank's rows, internal order).
 
-    Host (CPU) tensors are accepted: they are copied to the device and back
-    (the end-to-end path).  Returns r_trace ([nrec, 2] device tensor) or None.
+    Host (CPU) tensors are accepted and handed to kur_step as host pointers: the
+    library copies theta in and stores the result back (pinned memory: written by the
+    last stage through its device mapping) -- the end-to-end path.  The host result is
+    complete once the stream is synchronised.  Returns r_trace ([nrec, 2] device
+    tensor) or None.
     """
-    host = isinstance(theta, torch.Tensor) and not theta.is_cuda
-    if host:
-        th_h = theta
-        theta = theta.to(f"cuda:{g.device}", non_blocking=True)
-        if not omega.is_cuda:
-            omega = omega.to(f"cuda:{g.device}", non_blocking=True)
     if record_every and r_trace is None:
         r_trace = torch.zeros((int(nsteps) // int(record_every) + 1, 2), dtype=torch.float64,
                               device=f"cuda:{g.device}")
     rt = ctypes.c_void_p(r_trace.data_ptr()) if r_trace is not None else None
-    _check(_lib.kur_step(g._h, _dev_vec(theta, g.n_local, g.device, "theta"),
-                         _dev_vec(omega, g.n_local, g.device, "omega"), float(K), float(h), int(nsteps),
+    _check(_lib.kur_step(g._h, _dev_or_host_vec(theta, g.n_local, g.device, "theta"),
+                         _dev_or_host_vec(omega, g.n_local, g.device, "omega"), float(K), float(h), int(nsteps),
                          int(record_every), rt, _stream(stream)))
     if check:
         _check(_lib.kur_check(g._h, _stream(stream)))
-    if host:
-        th_h.copy_(theta, non_blocking=False)
     return r_trace
 
 
@@ -282,8 +287,8 @@ def step_method(g: Graph, method, theta, omega, K, h, nsteps, record_every=0, r_
         r_trace = torch.zeros((int(nsteps) // int(record_every) + 1, 2), dtype=torch.float64,
                               device=f"cuda:{g.device}")
     rt = ctypes.c_void_p(r_trace.data_ptr()) if r_trace is not None else None
-    _check(_lib.kur_step_method(g._h, METHODS[method], _dev_vec(theta, g.n_local, g.device, "theta"),
-                                _dev_vec(omega, g.n_local, g.device, "omega"), float(K), float(h), int(nsteps),
+    _check(_lib.kur_step_method(g._h, METHODS[method], _dev_or_host_vec(theta, g.n_local, g.device, "theta"),
+                                _dev_or_host_vec(omega, g.n_local, g.device, "omega"), float(K), float(h), int(nsteps),
                                 int(record_every), rt, float(fp_tol), int(fp_max_iter), _stream(stream)))
     if check:
         _check(_lib.kur_check(g._h, _stream(stream)))
