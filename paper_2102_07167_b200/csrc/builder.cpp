@@ -531,7 +531,13 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   // no stored entries (complete graphs: one dense block, empty complement lists) -> no shared
   // memory and nothing to balance: the largest tiles amortise the per-CTA latency (config 2:
   // 25.7 -> 21.5 us per stage with 2048- instead of 1024-row tiles, see the commit for 4096)
-  int rows_per_tile = force_rows ? force_rows : (P.small ? MAX_TILE_ROWS : total_len == 0 ? MAX_TILE_ROWS_NOPARTS : 0);
+  // Their tile is sized so the tiles fill exactly one wave of 2 CTAs per SM (config 2: 296
+  // tiles of 3552 rows instead of 256 of 4096, which left 40 SMs with one CTA).
+  int rows_per_tile = force_rows ? force_rows : P.small ? MAX_TILE_ROWS : 0;
+  if (!rows_per_tile && total_len == 0) {
+    const int64_t per = (n / world + 2LL * sm_count - 1) / (2LL * sm_count);
+    rows_per_tile = (int)std::min<int64_t>(MAX_TILE_ROWS_NOPARTS, std::max<int64_t>(256, (per + 31) / 32 * 32));
+  }
   for (int r = MAX_TILE_ROWS; r >= 256 && !rows_per_tile; r >>= 1) {
     int64_t nt = 0;
     for (int32_t c = 0; c < C; ++c) nt += (S.csize[(size_t)c] + r - 1) / r;
