@@ -661,7 +661,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     const int li = row - dp.row_begin;
     double2 w = parts ? Ws[lr] : make_double2(0.0, 0.0);
     if (addr) {
-      const double2 r = __ldcg(dp.Wr + li);
+      const double2 r = __ldcs(dp.Wr + li);
       w.x += r.x;
       w.y += r.y;
     }
@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(KREM_THREADS, 4) k_remote(const DevPlan dp, co
   }
   // 0 + s: the same single rounding-free addition the inline path does into a zeroed sum
   KUR_ASSERT(row == EMPTY_LANE || (int)(rc.y + row) < dp.row_begin + dp.n + 1);
-  if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) dp.Wr[rc.y + row] = make_double2(0.0 + sx, 0.0 + sy);
+  if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) __stcs(dp.Wr + rc.y + row, make_double2(0.0 + sx, 0.0 + sy));  // streaming: keep z in L2
 }
 
 template <int MODE>
