@@ -756,8 +756,12 @@ kur_status host_step(kur_graph* g, int method, double* theta, const double* omeg
     KUR_CUDA(cudaMemcpyAsync(g->omega_ws, omega, bytes, cudaMemcpyHostToDevice, s));
     om = g->omega_ws;
   }
+  // Stores through the mapping run at ~25 GB/s against ~50 GB/s for the copy engine: they
+  // pay only when the final stage outlasts the copy, i.e. when it moves >= 60x the bytes of
+  // theta (~3 TB/s vs ~50 GB/s; config 5 673 -> 747 RHS/s end to end, config 2 would lose).
+  const bool long_stage = g->info.bytes_per_rhs >= 60 * 8 * g->n_local;
   double* mapped = nullptr;
-  if (kt == 1 && !g->small && method != KUR_IMPLICIT_MIDPOINT && nsteps > 0) {
+  if (kt == 1 && long_stage && !g->small && method != KUR_IMPLICIT_MIDPOINT && nsteps > 0) {
     cudaPointerAttributes at{};
     KUR_CUDA(cudaPointerGetAttributes(&at, theta));
     mapped = static_cast<double*>(at.devicePointer);
