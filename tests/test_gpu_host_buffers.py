@@ -20,14 +20,25 @@ def _device_run(g, th0, om, inst, method, nsteps):
     return th.cpu(), rt.cpu()
 
 
-@pytest.mark.parametrize("which", ["sbm", "tiny"])
+def _instance(which):
+    if which == "sbm":  # short lists: theta goes back with one copy after the steps
+        return kurgen.sbm([700, 900, 400], [[0.9, 0.01, 0.02], [0.01, 0.7, 0.0], [0.02, 0.0, 0.95]], 31, K=3.0)
+    if which == "long":  # long lists (~700 entries per row): the final stage stores through the mapping
+        return kurgen.sbm([2000, 2000], [[0.3, 0.05], [0.05, 0.3]], 34, K=3.0)
+    return kurgen.sbm([20, 13], [[0.8, 0.1], [0.1, 0.9]], 32, K=2.0)  # single-CTA path
+
+
+@pytest.mark.parametrize("which", ["sbm", "long", "tiny"])
 @pytest.mark.parametrize("method", ["rk4", "euler", "heun", "implicit_midpoint"])
 @pytest.mark.parametrize("pinned", [True, False])
 @pytest.mark.parametrize("omega_host", [False, True])
 def test_host_theta_matches_device(which, method, pinned, omega_host):
-    inst = (kurgen.sbm([700, 900, 400], [[0.9, 0.01, 0.02], [0.01, 0.7, 0.0], [0.02, 0.0, 0.95]], 31, K=3.0)
-            if which == "sbm" else kurgen.sbm([20, 13], [[0.8, 0.1], [0.1, 0.9]], 32, K=2.0))
+    inst = _instance(which)
     g = kur.graph_build(inst)
+    if which == "long":  # the rule in api.cpp host_step: kernel bytes per RHS >= 60 x the bytes of theta
+        assert g.info["bytes_per_rhs"] >= 60 * 8 * g.n_local
+    elif which == "sbm":
+        assert g.info["bytes_per_rhs"] < 60 * 8 * g.n_local
     th0 = g.to_internal(torch.from_numpy(inst.theta0).cuda())
     om = g.to_internal(torch.from_numpy(inst.omega).cuda())
     want_th, want_rt = _device_run(g, th0, om, inst, method, 3)
