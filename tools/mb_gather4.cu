@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(NT, 1) k_tma(const __grid_constant__ CUtensorM
 }
 
 int main(int argc, char** argv) {
-  const long long n = 1 << 22, E = argc > 1 ? atoll(argv[1]) : (1LL << 26);
+  const long long n = argc > 2 ? atoll(argv[2]) : (1LL << 22), E = argc > 1 ? atoll(argv[1]) : (1LL << 26);
   const long long ngroups = E / 128;
   std::vector<double2> hz(n + 64);
   srand(1);
