@@ -114,9 +114,13 @@ int main(int argc, char** argv) {
   for (auto& v : hz) v = make_double2(rand() / (double)RAND_MAX, rand() / (double)RAND_MAX);
   std::vector<uint32_t> idx(E);
   uint64_t s = 88172645463325252ull;
-  for (auto& i : idx) {
+  // optional third argument: percentage of "padding" entries that all name one sentinel
+  // column n (the layout's zero padding), placed in the last group of each 128-entry block
+  const int pad_pct = argc > 3 ? atoi(argv[3]) : 0;
+  for (size_t k = 0; k < idx.size(); ++k) {
     s ^= s << 13; s ^= s >> 7; s ^= s << 17;
-    i = (uint32_t)(s % n);
+    idx[k] = (uint32_t)(s % n);
+    if ((int)((k % 128) * 100 / 128) >= 100 - pad_pct) idx[k] = (uint32_t)n;
   }
   double2* dz; uint4* du; double* dout;
   CK(cudaMalloc(&dz, sizeof(double2) * (n + 64)));
