@@ -307,12 +307,12 @@ __device__ __forceinline__ void run_remote(const uint4* __restrict__ q, uint32_t
 
 // k_remote's loop: as run_remote, but two groups (8 z gathers per lane) in
 // flight at once; missing groups read the zero sentinel z[sent] (sent = n).
-__device__ __forceinline__ void run_remote_deep(const uint4* __restrict__ q, uint32_t ng, uint32_t sent,
-                                                const double2* __restrict__ z, uint64_t pol, double& sx, double& sy) {
+// b0, b1: the chunk's first two index units, already requested by the caller.
+__device__ __forceinline__ void run_remote_deep_pre(const uint4* __restrict__ q, uint32_t ng, uint32_t sent,
+                                                    const double2* __restrict__ z, uint64_t pol, uint4 b0, uint4 b1,
+                                                    double& sx, double& sy) {
   double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
   const uint4 s4 = make_uint4(sent, sent, sent, sent);
-  uint4 b0 = ng > 0 ? ldg_stream(q, pol) : s4;
-  uint4 b1 = ng > 1 ? ldg_stream(q + 32, pol) : s4;
   for (uint32_t g = 0; g < ng; g += 2) {
     const uint4 c0 = b0, c1 = b1;
     const uint4* qn = q + (size_t)(g + 2) * 32;
@@ -329,6 +329,14 @@ __device__ __forceinline__ void run_remote_deep(const uint4* __restrict__ q, uin
   }
   sx = x0 + x1;
   sy = y0 + y1;
+}
+
+__device__ __forceinline__ void run_remote_deep(const uint4* __restrict__ q, uint32_t ng, uint32_t sent,
+                                                const double2* __restrict__ z, uint64_t pol, double& sx, double& sy) {
+  const uint4 s4 = make_uint4(sent, sent, sent, sent);
+  const uint4 b0 = ng > 0 ? ldg_stream(q, pol) : s4;
+  const uint4 b1 = ng > 1 ? ldg_stream(q + 32, pol) : s4;
+  run_remote_deep_pre(q, ng, sent, z, pol, b0, b1, sx, sy);
 }
 
 // The chunks of one part (P:562-570 complement entries subtracted, P:538-542
@@ -740,30 +748,77 @@ __global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const S
 }
 
 // a3, remote half: W_r,j = sum over the row's remote entries (signed, P:562-570 /
-// P:538-542) into Wr.  One warp per remote chunk (32 rows), all tiles' chunks in
-// one flat list, longest first: every row lies in exactly one remote chunk of its
-// tile (one remote part per tile), so the row sum is written, not accumulated, and
-// rows without remote entries keep the zero Wr was initialised with.  Thousands of
-// independent warps keep the latency-bound random z gathers in flight.
+// P:538-542) into Wr.  A warp sums one remote chunk (32 rows) at a time; all tiles'
+// chunks form one flat list, longest first, which the grid's warps stride over: every
+// row lies in exactly one remote chunk of its tile (one remote part per tile), so the
+// row sum is written, not accumulated, and rows without remote entries keep the zero
+// Wr was initialised with.  3 CTAs of 8 warps per SM (80 registers: the next chunk's
+// index units are in flight with the current gathers; 4 CTAs at 64 registers: slower).
 constexpr int KREM_THREADS = 256;
-__global__ void __launch_bounds__(KREM_THREADS, 4) k_remote(const DevPlan dp, const double2* __restrict__ zin) {
+constexpr int KREM_CTAS_PER_SM = 3;
+__global__ void __launch_bounds__(KREM_THREADS, KREM_CTAS_PER_SM) k_remote(const DevPlan dp,
+                                                                           const double2* __restrict__ zin) {
+  // Persistent warps striding over the chunk list.  The next chunk's header and first two
+  // index units are requested before the current chunk's gathers (and its list entry /
+  // descriptor two and one chunks ahead), so a warp never waits on an index load between
+  // chunks; only the drain of the current gathers before its row sums remains.
   const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * (KREM_THREADS / 32) + (threadIdx.x >> 5);
-  if (w >= dp.n_rchunks) return;
-  const uint2 rc = __ldg(reinterpret_cast<const uint2*>(dp.rchunks) + w);  // {chunk id, tile row base}
-  const uint2 cd = __ldg(dp.chunks + rc.x);
+  const int nw = (int)gridDim.x * (KREM_THREADS / 32);
+  int w = (int)blockIdx.x * (KREM_THREADS / 32) + (threadIdx.x >> 5);
+  const int n = dp.n_rchunks;
+  if (w >= n) return;
+  const uint2* rcs = reinterpret_cast<const uint2*>(dp.rchunks);  // {chunk id, tile row base}
+  const uint64_t pol = evict_first_policy();
+  const uint32_t sent = (uint32_t)dp.n;
+  const uint4 s4 = make_uint4(sent, sent, sent, sent);
+  uint2 rc = __ldg(rcs + w);
+  uint2 cd = __ldg(dp.chunks + rc.x);
   const uint4* q = dp.pool + cd.x;
-  const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
-  double sx, sy;
-  run_remote_deep(q + HDR_UNITS + lane, cd.y, (uint32_t)dp.n, zin, evict_first_policy(), sx, sy);
-  const int lp = dp.rem_lp[w];  // row pieces of the chunk's part
-  for (int o = 1; o < (1 << lp); o <<= 1) {
-    sx += __shfl_xor_sync(0xffffffffu, sx, o);
-    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+  uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
+  int lp = dp.rem_lp[w];
+  uint4 b0 = cd.y > 0 ? ldg_stream(q + HDR_UNITS + lane, pol) : s4;
+  uint4 b1 = cd.y > 1 ? ldg_stream(q + HDR_UNITS + lane + 32, pol) : s4;
+  uint2 rc1 = make_uint2(0, 0), cd1 = make_uint2(0, 0);
+  if (w + nw < n) {
+    rc1 = __ldg(rcs + w + nw);
+    cd1 = __ldg(dp.chunks + rc1.x);
   }
-  // 0 + s: the same single rounding-free addition the inline path does into a zeroed sum
-  KUR_ASSERT(row == EMPTY_LANE || (int)(rc.y + row) < dp.row_begin + dp.n + 1);
-  if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) __stcs(dp.Wr + rc.y + row, make_double2(0.0 + sx, 0.0 + sy));  // streaming: keep z in L2
+  for (;;) {
+    const bool more = w + nw < n;
+    const uint4* q1 = dp.pool + cd1.x;
+    uint16_t row1 = EMPTY_LANE;
+    int lp1 = 0;
+    uint4 b0n = s4, b1n = s4;
+    if (more) {
+      row1 = reinterpret_cast<const uint16_t*>(q1)[lane];
+      lp1 = dp.rem_lp[w + nw];
+      if (cd1.y > 0) b0n = ldg_stream(q1 + HDR_UNITS + lane, pol);
+      if (cd1.y > 1) b1n = ldg_stream(q1 + HDR_UNITS + lane + 32, pol);
+    }
+    const uint2 rc2 = w + 2 * nw < n ? __ldg(rcs + w + 2 * nw) : make_uint2(0, 0);
+    double sx, sy;
+    run_remote_deep_pre(q + HDR_UNITS + lane, cd.y, sent, zin, pol, b0, b1, sx, sy);
+    const uint2 cd2 = w + 2 * nw < n ? __ldg(dp.chunks + rc2.x) : make_uint2(0, 0);
+    for (int o = 1; o < (1 << lp); o <<= 1) {
+      sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    }
+    // 0 + s: the same single rounding-free addition the inline path does into a zeroed sum
+    KUR_ASSERT(row == EMPTY_LANE || (int)(rc.y + row) < dp.row_begin + dp.n + 1);
+    if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0)
+      __stcs(dp.Wr + rc.y + row, make_double2(0.0 + sx, 0.0 + sy));  // streaming: keep z in L2
+    if (!more) break;
+    w += nw;
+    rc = rc1;
+    cd = cd1;
+    q = q1;
+    row = row1;
+    lp = lp1;
+    b0 = b0n;
+    b1 = b1n;
+    rc1 = rc2;
+    cd1 = cd2;
+  }
 }
 
 template <int MODE>
@@ -1093,7 +1148,17 @@ namespace kur {
 cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s) {
   if (!dp.has_remote || dp.n_rchunks <= 0) return cudaSuccess;
   constexpr int wpb = KREM_THREADS / 32;
-  k_remote<<<(unsigned)((dp.n_rchunks + wpb - 1) / wpb), KREM_THREADS, 0, s>>>(dp, zin);
+  static thread_local int dev_cached = -1, sms = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev != dev_cached) {
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    dev_cached = dev;
+  }
+  const long long need = (dp.n_rchunks + wpb - 1) / wpb, full = (long long)KREM_CTAS_PER_SM * sms;
+  k_remote<<<(unsigned)(need < full ? need : full), KREM_THREADS, 0, s>>>(dp, zin);
   return cudaGetLastError();
 }
 
