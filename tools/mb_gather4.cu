@@ -36,6 +36,18 @@ __device__ __forceinline__ double2 ldz(const double2* p) {
   return r;
 }
 
+// KIND 4: z via __ldg, index units as k_remote loads them (L1::no_allocate + L2 evict_first)
+__device__ __forceinline__ uint4 ldg_idx(const uint4* p, int kind) {
+  if (kind != 4) return __ldg(p);
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(NT, 2) k_ldg(const uint4* __restrict__ units, long long ngroups,
                                                const double2* __restrict__ z, double* out) {
@@ -43,8 +55,8 @@ __global__ void __launch_bounds__(NT, 2) k_ldg(const uint4* __restrict__ units, 
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * NW + (threadIdx.x >> 5), nw = (long long)gridDim.x * NW;
   for (long long g = w; g < ngroups; g += nw) {
-    const uint4 u = __ldg(units + g * 32 + lane);
-    const double2 a = ldz<KIND>(z + u.x), b = ldz<KIND>(z + u.y), c = ldz<KIND>(z + u.z), d = ldz<KIND>(z + u.w);
+    const uint4 u = ldg_idx(units + g * 32 + lane, KIND);
+    const double2 a = ldz<KIND == 4 ? 0 : KIND>(z + u.x), b = ldz<KIND == 4 ? 0 : KIND>(z + u.y), c = ldz<KIND == 4 ? 0 : KIND>(z + u.z), d = ldz<KIND == 4 ? 0 : KIND>(z + u.w);
     x += a.x + b.x + c.x + d.x;
     y += a.y + b.y + c.y + d.y;
   }
@@ -146,7 +158,7 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
   double sums[2];
-  for (int which = 0; which < 5; ++which) {
+  for (int which = 0; which < 6; ++which) {
     float best = 1e30f;
     for (int rep = 0; rep < 6; ++rep) {
       cudaEventRecord(a);
@@ -155,6 +167,7 @@ int main(int argc, char** argv) {
       if (which == 2) k_ldg<1><<<grid, NT>>>(du, ngroups, dz, dout);
       if (which == 3) k_ldg<2><<<grid, NT>>>(du, ngroups, dz, dout);
       if (which == 4) k_ldg<3><<<grid, NT>>>(du, ngroups, dz, dout);
+      if (which == 5) k_ldg<4><<<grid, NT>>>(du, ngroups, dz, dout);
       cudaEventRecord(b);
       CK(cudaEventSynchronize(b));
       float ms; cudaEventElapsedTime(&ms, a, b);
@@ -165,7 +178,8 @@ int main(int argc, char** argv) {
     if (which == 1) for (int i = grid / 2 * NT; i < grid * NT; ++i) ho[i] = 0;
     double t = 0; for (double v : ho) t += v;
     if (which < 2) sums[which] = t;
-    const char* nm[5] = {"ldg.nc", "tma_gather4", "ldg.cg", "ldg.nc.L1::no_allocate", "ldg.nc.L1::evict_first"};
+    const char* nm[6] = {"ldg.nc", "tma_gather4", "ldg.cg", "ldg.nc.L1::no_allocate", "ldg.nc.L1::evict_first",
+                         "ldg.nc, index streamed (no_allocate + L2 evict_first)"};
     printf("%s: %.3f ms for %lld entries = %.2f G entries/s, sum %.10e\n", nm[which], best, E, E / (best * 1e6), t);
   }
   double ref = 0;
