@@ -103,6 +103,32 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+
+
+def _relaunch_distributed(n):
+    """`bench.py --gpus N` without a torchrun environment: run N ranks (one per GPU) under
+    torch.distributed.run on this node and return its exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -178,6 +204,10 @@ def main():
                     help="ablation (SURVEY 8(d)): 0 forces direct summation (plain CSR), <0 the paper's rule")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_relaunch_distributed(args.gpus))
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}: one rank per GPU")
     if args.impl == "reference":
         return run_reference(args)
 
@@ -191,6 +221,11 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if world > 1:
+        # NCCL's INIT lines (communicator size and rank of every process) on stderr, so the rank
+        # count is verifiable while stdout keeps the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     t0 = time.perf_counter()
     inst = kurgen.config(args.config)
@@ -368,7 +403,7 @@ def main():
             "gpu_launches": 1 + tm["prologue_n"] + tm["stage_n"] + tm["remote_n"]
                             + (2 * (tm["prologue_n"] + tm["stage_n"]) if world > 1 else 0),
             "clocks": clk.result(),
-            "host": {"gen_s": gen_s, "build_s": build_s, "nproc": os.cpu_count()},
+            "host": dict(_host_info(), gen_s=gen_s, build_s=build_s),
             "plan": {k: info[k] for k in ("n_idx_hot", "n_idx_remote", "n_slots_hot", "n_slots_remote",
                                           "n_dense_blocks", "n_sparse_blocks", "n_tiles", "rows_per_tile",
                                           "bytes_per_rhs", "bytes_pool")},

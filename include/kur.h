@@ -187,15 +187,16 @@ kur_status kur_rhs(kur_graph *g, const double *theta, const double *omega, doubl
  * for every n = 0, record_every, 2*record_every, ... <= nsteps
  * (floor(nsteps/record_every)+1 pairs, replicated on every rank).
  * A non-finite phase raises a device flag reported by kur_check.
- * Host buffers (world == 1): theta and/or omega may be HOST memory (pinned or
- * pageable).  The library then copies them into device buffers it owns, runs
+ * Host buffers: theta and/or omega may be HOST memory (pinned or pageable);
+ * with world > 1 (NCCL handle) each rank passes its own shard of n_local rows.  The library then copies them into device buffers it owns, runs
  * the same kernels, and stores theta_{n+1} back into the host theta: for
  * pinned memory, when the final stage is long enough to hide the transfer
  * (kernel bytes per RHS >= 60x the bytes of theta), the last step's final
  * stage writes it through the buffer's device mapping (the device-to-host
  * transfer overlaps that stage); otherwise one copy follows the steps.  The host result is complete when the stream is
  * synchronised; it is bitwise the device-buffer result.  Same for
- * kur_step_method.  KUR_ERR_UNSUPPORTED for host buffers with world > 1. */
+ * kur_step_method.  KUR_ERR_UNSUPPORTED for host buffers on a world > 1 handle
+ * without NCCL (the in-process kur_group_* handles take device buffers). */
 kur_status kur_step(kur_graph *g, double *theta, const double *omega, double K, double h,
                     int64_t nsteps, int32_t record_every, double *r_trace, void *stream);
 
@@ -317,9 +318,10 @@ kur_status kur_plan_sizes(const kur_plan *p, int64_t *sizes /* [16] */);
 kur_status kur_plan_export(const kur_plan *p, int32_t *perm, int32_t *D_ptr, int32_t *D_idx, int64_t *row_ptr,
                            int32_t *cols, int8_t *neg, int32_t *shard_row0);
 kur_status kur_plan_destroy(kur_plan *p);
-/* Tile and part structure of the plan (host): tiles[n_tiles][6] = {row0 (internal), nrows,
- * community, nparts, nhot, nown}: the tile's parts are its nown own-community hot windows,
- * then nhot - nown other hot windows, then at most one remote part;
+/* Tile and part structure of the plan (host): tiles[n_tiles][7] = {row0 (internal), nrows,
+ * community, nparts, nhot, nown, nloc}: the tile's parts are its nown own-community hot windows,
+ * then nhot - nown other hot windows, then at most one remote part; the first
+ * nloc <= nown of them lie inside this rank's rows (phase A of the sharded stage);
  * part_window[sum nparts] = window id of each part in that order (-1 = remote), or NULL. */
 kur_status kur_plan_tiles(const kur_plan *p, int32_t *tiles, int32_t *part_window);
 

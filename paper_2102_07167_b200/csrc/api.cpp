@@ -6,6 +6,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -361,6 +362,14 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
     if ((e = upload(&g->d_rchunks, P.rchunks)) != cudaSuccess) return bail(e, "rchunks");
     if ((e = upload(&g->d_rem_lp, P.rem_lp)) != cudaSuccess) return bail(e, "rem_lp");
   }
+  // where a remote part is summed (bitwise the same in every mode): KUR_REMOTE_MODE = 0 the k_remote
+  // pass, 1 one warp of the stage kernel with TMA gathers, 2 one warp with LDG gathers
+  dp.remote_warp = 0;
+  if (dp.has_remote) {
+    const char* rm = std::getenv("KUR_REMOTE_MODE");
+    if (rm && (rm[0] == '1' || rm[0] == '2')) dp.remote_warp = rm[0] - '0';
+  }
+  dp.n_local = g->n_local;
   dp.Wr = g->Wr;
   dp.peer_x = g->peer_on ? g->d_peer_x : nullptr;
   dp.peer_flag = g->d_peer_flag;
@@ -549,7 +558,7 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
   for (size_t r = 0; r < gs.size(); ++r) {
     kur_graph* g = gs[r];
     StageArgs& a = args[r];
-    if (g->timing && mode != PH_PROLOGUE && g->dp.has_remote) {  // time k_remote and k_stage separately
+    if (g->timing && mode != PH_PROLOGUE && g->dp.has_remote && !g->dp.remote_warp) {  // time k_remote, k_stage apart
       KUR_CUDA(g->mark(s));
       KUR_CUDA(launch_remote(g->dp, a.zin, s));
       KUR_CUDA(g->mark(s));
@@ -742,7 +751,9 @@ kur_status host_step(kur_graph* g, int method, double* theta, const double* omeg
   const int kt = mem_kind(theta), ko = mem_kind(omega);
   if (kt == 0 && ko == 0) return KUR_OK;
   *handled = true;
-  if (g->world > 1) return fail(KUR_ERR_UNSUPPORTED, "host theta/omega buffers need world == 1");
+  // world > 1 (NCCL job): every rank passes its own shard (n_local rows) in host memory; the
+  // steps are the usual collective (only handles of one process group, not kur_group_*)
+  if (g->world > 1 && !g->comm) return fail(KUR_ERR_UNSUPPORTED, "host buffers with world > 1 need an NCCL handle");
   const size_t bytes = sizeof(double) * (size_t)g->n_local;
   double* th = theta;
   if (kt != 0) {
@@ -1248,8 +1259,8 @@ kur_status kur_plan_tiles(const kur_plan* p, int32_t* tiles, int32_t* part_windo
   size_t k = 0;
   for (size_t t = 0; t < P.tiles.size(); ++t) {
     const TileDesc& T = P.tiles[t];
-    const int32_t v[6] = {T.row0, T.nrows, T.comm, T.nparts, T.nhot, T.nown};
-    std::memcpy(tiles + 6 * t, v, sizeof(v));
+    const int32_t v[7] = {T.row0, T.nrows, T.comm, T.nparts, T.nhot, T.nown, T.nloc};
+    std::memcpy(tiles + 7 * t, v, sizeof(v));
     if (part_window)
       for (int32_t q = 0; q < T.nparts; ++q) part_window[k++] = P.parts[(size_t)(T.part0 + q)].window;
   }

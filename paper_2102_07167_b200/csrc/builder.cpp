@@ -527,15 +527,19 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   int64_t total_len = 0;
 #pragma omp parallel for reduction(+ : total_len)
   for (int64_t u = 0; u < n; ++u) total_len += rlen[(size_t)u];
-  P.small = world == 1 && n <= 8192 && total_len <= (1 << 18);
+  // Every tile rule below depends on the graph (and the SM count) only, never on the world
+  // size or rank: tiles, their parts and the fixed reduction order are then the same at every
+  // world size, which makes results bitwise independent of the sharding.
+  const bool tiny = n <= 8192 && total_len <= (1 << 18);
+  P.small = world == 1 && tiny;
   // no stored entries (complete graphs: one dense block, empty complement lists) -> no shared
   // memory and nothing to balance: the largest tiles amortise the per-CTA latency (config 2:
   // 25.7 -> 21.5 us per stage with 2048- instead of 1024-row tiles, see the commit for 4096)
   // Their tile is sized so the tiles fill exactly one wave of 2 CTAs per SM (config 2: 296
   // tiles of 3552 rows instead of 256 of 4096, which left 40 SMs with one CTA).
-  int rows_per_tile = force_rows ? force_rows : P.small ? MAX_TILE_ROWS : 0;
+  int rows_per_tile = force_rows ? force_rows : tiny ? MAX_TILE_ROWS : 0;
   if (!rows_per_tile && total_len == 0) {
-    const int64_t per = (n / world + 2LL * sm_count - 1) / (2LL * sm_count);
+    const int64_t per = (n + 2LL * sm_count - 1) / (2LL * sm_count);
     rows_per_tile = (int)std::min<int64_t>(MAX_TILE_ROWS_NOPARTS, std::max<int64_t>(256, (per + 31) / 32 * 32));
   }
   for (int r = MAX_TILE_ROWS; r >= 256 && !rows_per_tile; r >>= 1) {
@@ -571,26 +575,49 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   std::vector<int64_t> cwork((size_t)C, 0);
   for (int32_t c = 0; c < C; ++c)
     for (int32_t t = P.comm_tile0[(size_t)c]; t < P.comm_tile0[(size_t)c + 1]; ++t) cwork[(size_t)c] += twork[(size_t)t];
-  std::vector<int32_t> comm_b((size_t)world + 1, 0);
+  // Shards: contiguous tile ranges balanced by work.  Whole communities per rank when that
+  // balances (then a tile's own-community windows are always local: phase A overlaps the
+  // exchange); otherwise (few large communities, e.g. one complete graph) the
+  // boundaries fall between tiles inside communities.  Every rank computes the same boundaries.
+  std::vector<int32_t> tile_b((size_t)world + 1, 0);
   {
-    const double totw = (double)std::accumulate(cwork.begin(), cwork.end(), (int64_t)0);
+    const double totw = (double)std::accumulate(twork.begin(), twork.end(), (int64_t)0);
+    auto max_shard = [&](const std::vector<int32_t>& b) {
+      int64_t m = 0;
+      for (int32_t r = 0; r < world; ++r) {
+        int64_t w = 0;
+        for (int32_t t = b[(size_t)r]; t < b[(size_t)r + 1]; ++t) w += twork[(size_t)t];
+        m = std::max(m, w);
+      }
+      return m;
+    };
+    std::vector<int32_t> cb((size_t)world + 1, 0), tb((size_t)world + 1, 0);
     int64_t acc = 0;
     int32_t c = 0;
-    for (int32_t r = 1; r < world; ++r) {
+    for (int32_t r = 1; r < world; ++r) {  // community granularity
       const double target = totw * r / world;
       while (c < C && (double)(acc + cwork[(size_t)c] / 2) < target) acc += cwork[(size_t)c++];
-      comm_b[(size_t)r] = std::max(c, comm_b[(size_t)r - 1]);
+      cb[(size_t)r] = P.comm_tile0[(size_t)std::max<int32_t>(c, 0)];
+      cb[(size_t)r] = std::max(cb[(size_t)r], cb[(size_t)r - 1]);
     }
-    comm_b[(size_t)world] = C;
+    cb[(size_t)world] = (int32_t)ntiles_all;
+    acc = 0;
+    int32_t t = 0;
+    for (int32_t r = 1; r < world; ++r) {  // tile granularity
+      const double target = totw * r / world;
+      while (t < ntiles_all && (double)(acc + twork[(size_t)t] / 2) < target) acc += twork[(size_t)t++];
+      tb[(size_t)r] = std::max(t, tb[(size_t)r - 1]);
+    }
+    tb[(size_t)world] = (int32_t)ntiles_all;
+    tile_b = (double)max_shard(cb) <= 1.1 * (double)max_shard(tb) ? cb : tb;
   }
   P.shard_row0.resize((size_t)world + 1);
   P.shard_tile0.resize((size_t)world + 1);
   for (int32_t r = 0; r <= world; ++r) {
-    P.shard_row0[(size_t)r] = P.comm_off[(size_t)comm_b[(size_t)r]];
-    P.shard_tile0[(size_t)r] = P.comm_tile0[(size_t)comm_b[(size_t)r]];
+    const int32_t tt = tile_b[(size_t)r];
+    P.shard_row0[(size_t)r] = tt < ntiles_all ? all[(size_t)tt].row0 : (int32_t)n;
+    P.shard_tile0[(size_t)r] = tt;
   }
-  P.comm_begin = comm_b[(size_t)rank];
-  P.comm_end = comm_b[(size_t)rank + 1];
   P.row_begin = P.shard_row0[(size_t)rank];
   P.row_end = P.shard_row0[(size_t)rank + 1];
   P.tile_begin = P.shard_tile0[(size_t)rank];
@@ -606,7 +633,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     std::vector<Unit> units;
     std::vector<PartDesc> parts;    // chunk0 relative to the tile
     std::vector<ChunkDesc> chunks;  // ofs relative to the tile
-    int32_t nhot = 0, nown = 0;
+    int32_t nhot = 0, nown = 0, nloc = 0;
     int64_t hot = 0, rem = 0, shot = 0, srem = 0, loads = 0;
   };
   std::vector<TileOut> outs((size_t)nt);
@@ -810,6 +837,11 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
         };
         std::stable_partition(O.parts.begin(), O.parts.end(), own);
         O.nown = (int32_t)std::count_if(O.parts.begin(), O.parts.end(), own);
+        // phase A (world > 1) sums the longest prefix of those whose columns are this rank's rows
+        O.nloc = 0;
+        while (O.nloc < O.nown && (int64_t)O.parts[(size_t)O.nloc].window * WZ >= P.row_begin &&
+               (int64_t)(O.parts[(size_t)O.nloc].window + 1) * WZ <= P.row_end)
+          ++O.nloc;
       }
       if (!remk.empty()) {
         std::sort(remk.begin(), remk.end());  // (row, sign, column)
@@ -842,6 +874,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     T.nparts = (int32_t)O.parts.size();
     T.nhot = O.nhot;
     T.nown = O.nown;
+    T.nloc = O.nloc;
     P.tiles[(size_t)lt] = T;
     uo += (int64_t)O.units.size();
     po += (int64_t)O.parts.size();

@@ -347,12 +347,12 @@ __device__ __forceinline__ void run_remote_deep(const uint4* __restrict__ q, uin
 template <bool COHERENT, bool DEEP = false>
 __device__ __forceinline__ void run_part(const DevPlan& dp, const PartDesc& P, bool hot, const double2* zs,
                                          const double2* __restrict__ z, double2* Ws, uint64_t pol, int warp,
-                                         int lane) {
+                                         int lane, uint32_t nw = NWARPS) {
     uint32_t c = warp;
     uint2 cdn = c < P.nchunks ? __ldg(dp.chunks + P.chunk0 + c) : make_uint2(0, 0);
     for (uint32_t r = 0; c < P.nchunks; ++r) {
       const uint2 cd = cdn;
-      const uint32_t cnext = (r + 1) * NWARPS + (((r + 1) & 1) ? (NWARPS - 1 - warp) : warp);
+      const uint32_t cnext = (r + 1) * nw + (((r + 1) & 1) ? (nw - 1 - warp) : warp);
       if (cnext < P.nchunks) cdn = __ldg(dp.chunks + P.chunk0 + cnext);
       const uint4* q = dp.pool + cd.x;
       const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
@@ -379,6 +379,107 @@ __device__ __forceinline__ void run_part(const DevPlan& dp, const PartDesc& P, b
       }
       c = cnext;
     }
+}
+
+// ---- the remote part of one tile summed by ONE warp of the tile's CTA (dp.remote_warp), while
+// the other warps gather the hot windows from shared memory: W_r,j = sum over the row's remote
+// entries, signed per entry (P:562-570 complement entries subtracted, P:538-542 non-zero entries
+// added), written to Wr[row] (global; the finalize adds it after a block barrier).  Per lane the
+// arithmetic is run_remote's exactly (x0 += e0, x1 += e1, x0 += e2, x1 += e3 per 4-entry group;
+// 0 + (x0 + x1)), so every remote mode gives the same bits.
+__device__ __forceinline__ void wr_store(const DevPlan& dp, const TileDesc& T, uint16_t row, int lp, int lane,
+                                         double sx, double sy) {
+  for (int o = 1; o < (1 << lp); o <<= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+  }
+  KUR_ASSERT(row == EMPTY_LANE || (int64_t)(T.row0 - dp.row_begin) + row < dp.n_local);
+  if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0)
+    __stcg(dp.Wr + (T.row0 - dp.row_begin) + row, make_double2(0.0 + sx, 0.0 + sy));
+}
+
+// remote_warp == 2: LDG gathers (one L1 wavefront per entry), 8 in flight per lane.
+__device__ __forceinline__ void remote_warp_ldg(const DevPlan& dp, const TileDesc& T, const double2* __restrict__ z,
+                                             uint64_t pol, int lane) {
+  const PartDesc P = dp.parts[T.part0 + T.nhot];
+  const int lp = P.neg >> 8;
+  for (uint32_t c = 0; c < P.nchunks; ++c) {
+    const uint2 cd = __ldg(dp.chunks + P.chunk0 + c);
+    const uint4* q = dp.pool + cd.x;
+    const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
+    double sx, sy;
+    run_remote_deep(q + HDR_UNITS + lane, cd.y, (uint32_t)dp.n, z, pol, sx, sy);
+    wr_store(dp, T, row, lp, lane, sx, sy);
+  }
+}
+
+// remote_warp == 1: the z entries are fetched by TMA bulk copies (16 bytes each, async proxy:
+// no L1 wavefront per gather) into a ring of RING_SLOTS slots in shared memory; slot s holds one
+// 4-entry group of every lane, entry e of lane l at [s][e][l] (conflict-free LDS.128 reads).
+// The groups of all the part's chunks form one sequence, RING_SLOTS - 1 issued ahead of the one
+// being summed.
+__device__ __forceinline__ void remote_warp_tma(const DevPlan& dp, const TileDesc& T, const double2* __restrict__ z,
+                                             double2* ring, uint64_t* rbar, uint64_t pol, int lane) {
+  const PartDesc P = dp.parts[T.part0 + T.nhot];
+  const int lp = P.neg >> 8;
+  const uint32_t nch = P.nchunks;
+  uint32_t ci = 0, gi = 0, qi = 0;  // issue cursor: chunk, group, sequence number
+  uint2 cdi = nch > 0 ? __ldg(dp.chunks + P.chunk0) : make_uint2(0, 0);
+  uint32_t sgn = 0;  // per slot: the 4 entries' sign bits (bit 31 of the ids)
+  auto issue = [&]() {
+    while (ci < nch && gi >= cdi.y) {  // next chunk with groups left
+      ++ci;
+      gi = 0;
+      if (ci < nch) cdi = __ldg(dp.chunks + P.chunk0 + ci);
+    }
+    if (ci >= nch) return;
+    const uint4 u = ldg_stream(dp.pool + cdi.x + HDR_UNITS + (size_t)gi * 32 + lane, pol);
+    const uint32_t s = qi % RING_SLOTS;
+    sgn = (sgn & ~(0xFu << (4 * s))) |
+          (((u.x >> 31) | ((u.y >> 31) << 1) | ((u.z >> 31) << 2) | ((u.w >> 31) << 3)) << (4 * s));
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(rbar + s)), "r"(128 * 16)
+                   : "memory");
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t ids[4] = {u.x & 0x7FFFFFFFu, u.y & 0x7FFFFFFFu, u.z & 0x7FFFFFFFu, u.w & 0x7FFFFFFFu};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      KUR_ASSERT(ids[e] < g_dbg_zlen);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+              smem_addr(ring + (size_t)s * 128 + e * 32 + lane)),
+          "l"(z + ids[e]), "r"(smem_addr(rbar + s))
+          : "memory");
+    }
+    ++gi;
+    ++qi;
+  };
+  for (int k = 0; k < RING_SLOTS - 1; ++k) issue();
+  uint32_t qc = 0, phases = 0;  // sequence number being summed; mbarrier phase bit per slot
+  for (uint32_t c = 0; c < nch; ++c) {
+    const uint2 cd = __ldg(dp.chunks + P.chunk0 + c);
+    const uint16_t row = reinterpret_cast<const uint16_t*>(dp.pool + cd.x)[lane];
+    double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
+    for (uint32_t g = 0; g < cd.y; ++g) {
+      issue();  // fills the slot summed in the previous iteration: RING_SLOTS - 1 groups stay ahead
+      const uint32_t s = qc % RING_SLOTS;
+      mbar_wait(rbar + s, (phases >> s) & 1u);
+      phases ^= 1u << s;
+      const uint32_t m = sgn >> (4 * s);
+      const double2* slot = ring + (size_t)s * 128 + lane;
+      double2 a0 = slot[0], a1 = slot[32], a2 = slot[64], a3 = slot[96];
+      if (m & 1u) a0 = make_double2(-a0.x, -a0.y);
+      if (m & 2u) a1 = make_double2(-a1.x, -a1.y);
+      if (m & 4u) a2 = make_double2(-a2.x, -a2.y);
+      if (m & 8u) a3 = make_double2(-a3.x, -a3.y);
+      x0 += a0.x; y0 += a0.y; x1 += a1.x; y1 += a1.y;
+      x0 += a2.x; y0 += a2.y; x1 += a3.x; y1 += a3.y;
+      __syncwarp();  // every lane has read slot s before the next issue() overwrites it
+      ++qc;
+    }
+    wr_store(dp, T, row, lp, lane, x0 + x1, y0 + y1);
+  }
 }
 
 // world > 1: one double of this rank's packed exchange record [phases | per tile (sum z, max
@@ -588,7 +689,7 @@ __device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs
 template <int MODE, bool SMALL>
 __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a, const TileDesc& T, double2* zs,
                                            double2* Ws, uint64_t* bar, uint32_t& phase, double& px, double& py,
-                                           double& dmax) {
+                                           double& dmax, double2* ring = nullptr, uint64_t* rbar = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool parts = dp.has_parts;
   // the remote part of the tile was summed by k_remote into Wr (added in the finalize);
@@ -597,7 +698,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   const bool addr = split && T.nparts > T.nhot && a.phase != PHASE_A;
   // world > 1: phase A sums the own-community hot parts (local z only) into Wh while the
   // previous stage's exchange is in flight; phase B continues from Wh (exact copy)
-  const bool from_wh = !SMALL && a.phase == PHASE_B && T.nown > 0;
+  const bool from_wh = !SMALL && a.phase == PHASE_B && T.nloc > 0;
   if (parts) {
     for (int r = tid; r < T.nrows; r += NTHREADS)
       Ws[r] = from_wh ? __ldcg(a.Wh + (T.row0 - dp.row_begin) + r) : make_double2(0.0, 0.0);
@@ -617,12 +718,25 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   // single remote part (inline) — or its k_remote row sum Wr added in the finalize: one
   // addition per row either way, so both modes and every world size are bitwise identical.
   const int nrem = split ? 0 : T.nparts - T.nhot;
-  const int pbeg = (!SMALL && a.phase == PHASE_B) ? T.nown : 0;
-  const int pend = (!SMALL && a.phase == PHASE_A) ? T.nown : T.nhot + nrem;
+  const int pbeg = (!SMALL && a.phase == PHASE_B) ? T.nloc : 0;
+  const int pend = (!SMALL && a.phase == PHASE_A) ? T.nloc : T.nhot + nrem;
   bool pending = false;
 #ifdef KUR_PROFILE
   if (!SMALL && g_prof && tid == 0) g_prof[(size_t)blockIdx.x * PROF_STRIDE + 29] = (unsigned long long)nrem;
 #endif
+  // remote warp: the last warp sums the tile's remote part (into Wr) while the other NWARPS - 1
+  // gather the hot parts, which then synchronise on named barrier 1 instead of the block barrier
+#ifdef KUR_NO_REMOTE_WARP
+  constexpr bool rw = false;
+#else
+  const bool rw = !SMALL && addr && dp.remote_warp;
+#endif
+  if (rw && warp == NWARPS - 1) {
+    if (dp.remote_warp == 1) remote_warp_tma(dp, T, a.zin, ring, rbar, pol, lane);
+    else remote_warp_ldg(dp, T, a.zin, pol, lane);
+    __syncthreads();  // joins the hot warps below (Wr complete, Ws complete)
+  } else {
+  const uint32_t nhw = rw ? NWARPS - 1 : NWARPS;
   if (pbeg < T.nhot && pbeg < pend) {
     loaded = dp.parts[T.part0 + pbeg].window;
     pending = true;
@@ -650,10 +764,13 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
                      "r"((uint32_t)(WZ * sizeof(double2)))
                      : "memory");
     }
-    run_part<SMALL, !SMALL>(dp, P, hot, zs, a.zin, Ws, pol, warp, lane);
+    run_part<SMALL, !SMALL>(dp, P, hot, zs, a.zin, Ws, pol, warp, lane, nhw);
     if (!SMALL) PROF_W(pi, warp);
-    __syncthreads();
+    if (rw) asm volatile("bar.sync 1, %0;" ::"r"(nhw * 32) : "memory");
+    else __syncthreads();
     if (!SMALL && pi < 8) PROF_T(3 + 3 * pi);
+  }
+  if (rw) __syncthreads();  // joins the remote warp
   }
   if (!SMALL) PROF_T(25);
   if (!SMALL && a.phase == PHASE_A) {  // hand the own-community sums to phase B
@@ -673,7 +790,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     const int li = row - dp.row_begin;
     double2 w = parts ? Ws[lr] : make_double2(0.0, 0.0);
     if (addr) {
-      const double2 r = __ldcs(dp.Wr + li);
+      const double2 r = rw ? __ldcg(dp.Wr + li) : __ldcs(dp.Wr + li);
       w.x += r.x;
       w.y += r.y;
     }
@@ -804,7 +921,7 @@ __global__ void __launch_bounds__(KREM_THREADS, KREM_CTAS_PER_SM) k_remote(const
       sy += __shfl_xor_sync(0xffffffffu, sy, o);
     }
     // 0 + s: the same single rounding-free addition the inline path does into a zeroed sum
-    KUR_ASSERT(row == EMPTY_LANE || (int)(rc.y + row) < dp.row_begin + dp.n + 1);
+    KUR_ASSERT(row == EMPTY_LANE || (int64_t)(rc.y + row) < dp.n_local);
     if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0)
       __stcs(dp.Wr + rc.y + row, make_double2(0.0 + sx, 0.0 + sy));  // streaming: keep z in L2
     if (!more) break;
@@ -826,8 +943,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* zs = reinterpret_cast<double2*>(smem_raw);  // [WZ + 8]: window + 8 zero sentinels
   double2* Ws = zs + (WZ + 8);                         // [rows_per_tile]: W_j of the tile
+  double2* ring = Ws + dp.rows_per_tile;               // [RING_SLOTS][4][32] remote warp (TMA)
   __shared__ double2 red[NWARPS];
   __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t rbar[RING_SLOTS];
   __shared__ int s_nonfinite;
   const int tid = threadIdx.x;
   // implicit midpoint: iterations after convergence are no-ops (uniform: every CTA reads the same flag)
@@ -845,16 +964,17 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   }
   const int lt = dp.order[blockIdx.x];
   const TileDesc T = dp.tiles[lt];
-  if (a.phase == PHASE_A && T.nown == 0) return;  // nothing local to pre-sum (phase B starts from 0)
+  if (a.phase == PHASE_A && T.nloc == 0) return;  // nothing local to pre-sum (phase B starts from 0)
   if (dp.has_parts && tid < 8) zs[WZ + tid] = make_double2(0.0, 0.0);
   if (tid == 0) {
     s_nonfinite = 0;
     mbar_init(&bar, 1);
   }
+  if (dp.remote_warp == 1 && tid >= 32 && tid < 32 + RING_SLOTS) mbar_init(rbar + (tid - 32), 1);
   __syncthreads();
   uint32_t phase = 0;
   double px, py, dmax;
-  const bool bad = stage_rows<MODE, false>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax);
+  const bool bad = stage_rows<MODE, false>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax, ring, rbar);
   if (MODE == MODE_RHS || a.phase == PHASE_A) return;
   constexpr bool FINAL = MODE == MODE_S4 || MODE == MODE_E1 || MODE == MODE_H2;
   if (FINAL && bad) s_nonfinite = 1;
@@ -1119,7 +1239,7 @@ __global__ void k_permute(const int32_t* __restrict__ perm, int64_t n, const dou
 template <int MODE>
 cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
   static std::atomic<uint64_t> attr_set{0};  // one bit per device (the attribute is per device context)
-  const size_t smem = stage_smem_bytes(MAX_TILE_ROWS);
+  const size_t smem = stage_smem_bytes(MAX_TILE_ROWS) + RING_BYTES;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!((attr_set.load() >> (dev & 63)) & 1)) {
@@ -1127,11 +1247,12 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(1ull << (dev & 63));
   }
-  if (dp.has_remote && !a.no_remote && a.phase != PHASE_A) {
+  if (dp.has_remote && !dp.remote_warp && !a.no_remote && a.phase != PHASE_A) {
     cudaError_t e = launch_remote(dp, a.zin, s);
     if (e != cudaSuccess) return e;
   }
-  k_stage<MODE><<<dp.ntiles, NTHREADS, dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) : 0, s>>>(dp, a);
+  const size_t dyn = dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) + (dp.remote_warp == 1 ? RING_BYTES : 0) : 0;
+  k_stage<MODE><<<dp.ntiles, NTHREADS, dyn, s>>>(dp, a);
   return cudaGetLastError();
 }
 
@@ -1146,7 +1267,7 @@ namespace kur {
 #endif
 
 cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s) {
-  if (!dp.has_remote || dp.n_rchunks <= 0) return cudaSuccess;
+  if (!dp.has_remote || dp.remote_warp || dp.n_rchunks <= 0) return cudaSuccess;
   constexpr int wpb = KREM_THREADS / 32;
   static thread_local int dev_cached = -1, sms = 0;
   int dev = 0;

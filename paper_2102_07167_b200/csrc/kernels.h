@@ -23,6 +23,7 @@ struct Ctrl {             // device-resident control block
 
 struct DevPlan {
   int64_t n;              // global N
+  int64_t n_local;        // this rank's rows
   int32_t C;
   int32_t rows_per_tile;  // <= MAX_TILE_ROWS
   int32_t ntiles;         // local tiles (one CTA each)
@@ -30,7 +31,11 @@ struct DevPlan {
   int32_t row_begin;      // internal id of local row 0
   int32_t world;
   int32_t has_parts;          // any tile has stored entries (else no shared memory is needed)
-  int32_t has_remote;         // any tile has remote parts (k_remote runs before each k_stage)
+  int32_t has_remote;         // any tile has remote parts summed out of line into Wr (see remote_warp)
+  int32_t remote_warp;        // has_remote: 0 = the k_remote pass before each k_stage; inside k_stage, one
+                              // warp of each tile sums its remote part while the others gather the hot
+                              // windows: 1 = z gathered by 16-byte TMA bulk copies into a shared-memory
+                              // ring, 2 = LDG gathers
   const TileDesc* tiles;      // [ntiles]
   const int32_t* order;       // [ntiles] launch order
   const PartDesc* parts;      // [n_parts]
@@ -127,6 +132,9 @@ cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_t
 cudaError_t launch_permute(const int32_t* perm, int64_t n, const double* in, double* out, int dir,
                            cudaStream_t s);
 size_t stage_smem_bytes(int rows_per_tile);
+// remote warp (remote_warp == 1): RING_SLOTS groups of 32 lanes x 4 entries x 16 bytes in flight
+constexpr int RING_SLOTS = 6;
+constexpr size_t RING_BYTES = (size_t)RING_SLOTS * 128 * 16;
 // variable-step RK4: tile_ss[t] = sum over tile t's rows of ((y2 - y1) / (atol + rtol |y2|))^2
 cudaError_t launch_errnorm(const DevPlan& dp, const double* y1, const double* y2, double atol, double rtol,
                            double* tile_ss, cudaStream_t s);

@@ -61,7 +61,7 @@ struct TileDesc {   // 32 bytes; device array
   int32_t nparts;   // hot parts first (by window), then remote parts
   int32_t nhot;     // number of hot parts
   int32_t nown;     // of which the first nown lie wholly inside the tile's own community
-  int32_t pad1;
+  int32_t nloc;     // of which the first nloc also lie inside this rank's rows (phase A, world > 1)
 };
 
 struct PartDesc {   // 16 bytes; device array
@@ -90,7 +90,6 @@ struct HostPlan {
   int32_t rank = 0, world = 1;
   int64_t row_begin = 0, row_end = 0;     // this rank's internal rows
   int32_t tile_begin = 0, tile_end = 0;   // this rank's tiles (global ids)
-  int32_t comm_begin = 0, comm_end = 0;   // this rank's communities
   std::vector<int32_t> perm;        // [n] internal -> user
   std::vector<int32_t> comm_off;    // [C+1] internal row offsets
   std::vector<int32_t> comm_tile0;  // [C+1] tile offsets (global tile ids)

@@ -477,7 +477,7 @@ def plan_export(inst, *, rank=0, world=1, sm_count=148, dense_threshold=-1.0, ho
         _check(_lib.kur_plan_sizes(h, _np_ptr(sz)))
         out.update(conflicts=int(sz[10]), slots_hot=int(sz[11]), idx_hot=int(sz[12]), slots_remote=int(sz[13]),
                    idx_remote=int(sz[14]), window_loads=int(sz[15]))
-        tiles = np.zeros((max(nt, 1), 6), np.int32)
+        tiles = np.zeros((max(nt, 1), 7), np.int32)
         _check(_lib.kur_plan_tiles(h, ctypes.c_void_p(tiles.ctypes.data), None))
         pw = np.zeros(max(int(tiles[:nt, 3].sum()), 1), np.int32)
         _check(_lib.kur_plan_tiles(h, ctypes.c_void_p(tiles.ctypes.data), ctypes.c_void_p(pw.ctypes.data)))

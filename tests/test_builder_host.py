@@ -31,6 +31,7 @@ def reconstruct(inst, plan):
 
 def check_plan(inst, A, **kw):
     world = kw.pop("world", 1)
+    split_ok = kw.pop("split_ok", False)
     covered = []
     for rank in range(world):
         plan = kur.plan_export(inst, rank=rank, world=world, **kw)
@@ -49,7 +50,7 @@ def check_plan(inst, A, **kw):
             assert np.array_equal(got, want), (rank, j)
         covered.append((plan["row_begin"], plan["row_begin"] + plan["n_local"]))
         sr = plan["shard_row0"]
-        if world > 1:  # shards are whole communities
+        if world > 1 and not split_ok:  # shards are whole communities
             for b in sr[1:-1]:
                 assert b == 0 or b == inst.n or lab_int[b - 1] != lab_int[b]
     covered.sort()
@@ -252,10 +253,10 @@ def test_canonical_part_order(world):
     off = np.concatenate([[0], np.cumsum(sizes)])
     k = 0
     seen_remote_first = False
-    for row0, nrows, comm, nparts, nhot, nown in out["tiles"]:
+    for row0, nrows, comm, nparts, nhot, nown, nloc in out["tiles"]:
         w = out["part_window"][k:k + nparts]
         k += nparts
-        assert 0 <= nown <= nhot <= nparts <= nhot + 1
+        assert 0 <= nloc <= nown <= nhot <= nparts <= nhot + 1
         assert np.all(w[:nhot] >= 0) and np.all(w[nhot:] == -1)
         for q in range(nhot):
             inside = w[q] * 4096 >= off[comm] and (w[q] + 1) * 4096 <= off[comm + 1]
@@ -280,3 +281,68 @@ def test_hot_chunk_lengths_every_remainder():
     plan = check_plan(inst, A, hot_min=1)
     assert plan["idx_hot"] == int(A.sum())
     assert plan["slots_hot"] >= plan["idx_hot"]
+
+
+def _tiles_all_ranks(inst, world, **kw):
+    """(tiles without nloc, part windows, shard_row0) over all ranks of a world-size plan."""
+    tiles, windows, shards = [], [], None
+    for rank in range(world):
+        out = kur.plan_export(inst, rank=rank, world=world, **kw)
+        tiles.append(out["tiles"][:, :6])
+        windows.append(out["part_window"])
+        if shards is None:
+            shards = out["shard_row0"]
+        assert np.array_equal(out["shard_row0"], shards)
+        assert out["row_begin"] == shards[rank] and out["n_local"] == shards[rank + 1] - shards[rank]
+    return np.concatenate(tiles), np.concatenate(windows), shards
+
+
+@pytest.mark.parametrize("case", ["sbm_small", "complete_small", "complete_2e20", "sbm5"])
+def test_tiles_independent_of_world(case):
+    """The tile rule depends on the graph only: tiles, their parts and windows
+    (hence the fixed reduction order and every rounding) are the same at world 1, 2 and 3;
+    shards are contiguous tile ranges covering all rows (builder.cpp tile rule)."""
+    if case == "sbm_small":
+        inst = kurgen.sbm([1000, 1000], np.array([[0.02, 0.02], [0.02, 0.02]]), 5)
+    elif case == "complete_small":
+        inst = kurgen.complete_graph(5000, 7)
+    elif case == "complete_2e20":
+        inst = kurgen.complete_graph(1 << 20, 7)
+    else:
+        inst = kurgen.sbm([5000, 4096, 700, 9000, 33], np.array(
+            [[0.97, 0.002, 0.6, 0.0, 0.1], [0.002, 0.9, 0.0, 0.001, 0.0], [0.6, 0.0, 0.98, 0.0, 0.0],
+             [0.0, 0.001, 0.0, 0.95, 0.02], [0.1, 0.0, 0.0, 0.02, 0.5]]), 31)
+    t1, w1, s1 = _tiles_all_ranks(inst, 1)
+    for world in (2, 3):
+        tw, ww, sw = _tiles_all_ranks(inst, world)
+        assert np.array_equal(tw, t1), world
+        assert np.array_equal(ww, w1), world
+        assert sw[0] == 0 and sw[-1] == inst.n and np.all(np.diff(sw) >= 0)
+        assert set(sw.tolist()) <= set(t1[:, 0].tolist()) | {inst.n}  # boundaries between tiles
+    if case == "complete_2e20":  # one community: the rows are split, every rank has tiles
+        _, _, s2 = _tiles_all_ranks(inst, 2)
+        assert 0 < s2[1] < inst.n
+
+
+def test_split_community_plan_decodes():
+    """Shards inside a community (tile granularity): every rank's layout still decodes to A and
+    nloc counts only own-community windows inside the rank's rows."""
+    rng = np.random.default_rng(3)
+    n = 9000
+    A = (rng.random((n, n)) < 0.97).astype(np.uint8)
+    np.fill_diagonal(A, 0)
+    inst = kurgen.from_dense(A, np.zeros(n, np.int64), kind="zeros")
+    check_plan(inst, A, world=2, split_ok=True, tile_rows=512)
+    for rank in range(2):
+        out = kur.plan_export(inst, rank=rank, world=2, tile_rows=512)
+        rb, re_ = out["row_begin"], out["row_begin"] + out["n_local"]
+        assert 0 < out["n_local"] < n
+        k = 0
+        for row0, nrows, comm, nparts, nhot, nown, nloc in out["tiles"]:
+            w = out["part_window"][k:k + nparts]
+            k += nparts
+            for q in range(nown):
+                inside = w[q] * 4096 >= rb and (w[q] + 1) * 4096 <= re_
+                if q < nloc:
+                    assert inside
+            assert nloc == nown or not (w[nloc] * 4096 >= rb and (w[nloc] + 1) * 4096 <= re_)

@@ -81,3 +81,87 @@ def test_group_handle_alone_is_refused():
     with pytest.raises(kur.KurError) as e:
         kur.step(gs[0], th, th.clone(), 1.0, 0.01, 1)
     assert e.value.status == 10
+
+
+def _group_vs_single(inst, world, steps=4, method="rk4", **kw):
+    """world-rank group (one device) against world 1: RHS, `steps` steps and r(t), bitwise."""
+    g1 = kur.graph_build(inst, **kw)
+    dev = "cuda:0"
+    th_full = g1.to_internal(torch.from_numpy(inst.theta0).to(dev))
+    om_full = g1.to_internal(torch.from_numpy(inst.omega).to(dev))
+    f1 = kur.rhs(g1, th_full, om_full, inst.K)
+    th1 = th_full.clone()
+    rt1 = kur.step_method(g1, method, th1, om_full, inst.K, inst.h, steps, 1)
+    gs = kur.group_build(inst, world, **kw)
+    ths = [th_full[g.row_begin:g.row_end].clone() for g in gs]
+    oms = [om_full[g.row_begin:g.row_end].clone() for g in gs]
+    fs = kur.group_rhs(gs, ths, oms, inst.K)
+    rts = kur.group_step_method(gs, method, ths, oms, inst.K, inst.h, steps, 1)
+    torch.cuda.synchronize()
+    ok = (torch.equal(torch.cat(fs), f1), torch.equal(torch.cat(ths), th1), all(torch.equal(r, rt1) for r in rts))
+    bounds = [(g.row_begin, g.row_end) for g in gs]
+    for g in gs:
+        g.close()
+    g1.close()
+    return ok, bounds
+
+
+@pytest.mark.parametrize("case", ["sbm_2x1000", "complete_20000", "one_community_9000"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_group_bitwise_world_independent_tiles(case, world):
+    """The world-independent tile rule (builder.cpp) makes ANY world size bitwise equal to world 1,
+    including graphs the round-1 rule tiled differently per world (a small SBM: tiny-graph tiles;
+    a complete graph: entry-free tiles sized by n / world) and a single community split between
+    ranks at tile boundaries (phase A then only sums the windows inside the rank's rows)."""
+    if case == "sbm_2x1000":
+        inst = kurgen.sbm([1000, 1000], np.array([[0.02, 0.02], [0.02, 0.02]]), 5, K=2.0, h=0.01)
+    elif case == "complete_20000":
+        inst = kurgen.complete_graph(20000, 9, K=3.0, h=0.01)
+    else:
+        rng = np.random.default_rng(3)
+        n = 9000
+        A = (rng.random((n, n)) < 0.97).astype(np.uint8)
+        A = np.triu(A, 1)
+        A = A + A.T
+        inst = kurgen.from_dense(A, np.zeros(n, np.int64), kind="zeros", seed=4, K=2.0, h=0.01)
+    for method in ("rk4", "heun"):
+        ok, bounds = _group_vs_single(inst, world, method=method)
+        assert all(ok), (case, world, method, ok)
+    if case != "sbm_2x1000":  # one community: every rank holds rows
+        assert all(b > a for a, b in bounds), bounds
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_remote_modes_bitwise(world, monkeypatch):
+    """The remote part summed by the k_remote pass (KUR_REMOTE_MODE=0), by one warp of the stage kernel
+    with TMA gathers (1) or with LDG gathers (2): the same bits (world 2: phase B with the remote warp)."""
+    inst = kurgen.sbm([4000, 3000, 2500, 2600], np.array(
+        [[0.97, 0.01, 0.002, 0.0], [0.01, 0.9, 0.0, 0.01], [0.002, 0.0, 0.98, 0.003], [0.0, 0.01, 0.003, 0.95]]),
+        41, K=3.0, h=0.01)
+    res = []
+    for mode in ("0", "1", "2"):
+        monkeypatch.setenv("KUR_REMOTE_MODE", mode)
+        if world == 1:
+            g = kur.graph_build(inst, remote_pass=True, tile_rows=512)
+            assert g.info["remote_pass"] == 1
+            th = g.to_internal(torch.from_numpy(inst.theta0).cuda())
+            om = g.to_internal(torch.from_numpy(inst.omega).cuda())
+            f = kur.rhs(g, th, om, inst.K)
+            rt = kur.step(g, th, om, inst.K, inst.h, 5, 1)
+            res.append((f, th, rt))
+            g.close()
+        else:
+            ok, _ = _group_vs_single(inst, world, steps=5, remote_pass=True, tile_rows=512)
+            assert all(ok), (mode, ok)
+    if world == 1:
+        for f, th, rt in res[1:]:
+            assert torch.equal(f, res[0][0]) and torch.equal(th, res[0][1]) and torch.equal(rt, res[0][2])
+
+
+def test_config5_world8_bitwise():
+    """Config 5 (the scaling workload) split over 8 rank handles on one device, as bench.py --gpus 8
+    shards it (32 whole communities per rank): RHS, 2 RK4 steps and r(t) bitwise equal to world 1."""
+    inst = kurgen.config(5)
+    ok, bounds = _group_vs_single(inst, 8, steps=2)
+    assert all(ok), ok
+    assert len(bounds) == 8 and all(b - a == inst.n // 8 for a, b in bounds), bounds

@@ -228,19 +228,29 @@ def test_o8_relabelling_equivariance():
 
 
 # ---------------------------------------------------------------- O9 naive == matvec
-@pytest.mark.parametrize("which", ["cfg1", "cfg3", "sbm"])
+@pytest.mark.parametrize("which", ["cfg1", "cfg3", "sbm", "cfg4_rows", "cfg5_rows"])
 def test_o9_naive_equals_matvec(which):
+    """O9: the P:388 definition (per-edge sines) and the P:443 componentwise form agree,
+    on whole configs 1 and 3 and on sampled rows (1024 + a whole community) of the full configs 4 and 5."""
+    rows = None
     if which == "cfg1":
         inst = kurgen.config(1)
     elif which == "cfg3":
         inst = kurgen.config(3)
+    elif which in ("cfg4_rows", "cfg5_rows"):
+        c = 4 if which == "cfg4_rows" else 5
+        inst = kurgen.config(c)
+        rnd = (kurgen.raw_bits(c, 11, 1024) % np.uint64(inst.n)).astype(np.int64)
+        rows = np.concatenate([rnd, np.flatnonzero(inst.community == 1)[:2048].astype(np.int64)])
     else:
         inst = kurgen.sbm([500, 300, 10], [[0.95, 0.2, 0.6], [0.2, 0.05, 0.0], [0.6, 0.0, 1.0]], 31)
     g = oracle.Graph(inst)
-    fn = oracle.rhs(g, inst.theta0, inst.omega, inst.K, mode="naive")
-    fm = oracle.rhs(g, inst.theta0, inst.omega, inst.K, mode="matvec")
-    scale = np.abs(fn - inst.omega) + np.abs(inst.omega)
+    fn = oracle.rhs(g, inst.theta0, inst.omega, inst.K, mode="naive", rows=rows)
+    fm = oracle.rhs(g, inst.theta0, inst.omega, inst.K, mode="matvec", rows=rows)
+    om = inst.omega if rows is None else inst.omega[rows]
+    scale = np.abs(fn - om) + np.abs(om)
     assert np.all(np.abs(fn - fm) <= 1e-12 * scale + 1e-13)
+    assert np.median(np.abs(fn - om)) > 1e-6  # the coupling term is not vacuous on these rows
 
 
 def test_sampled_rows_match_full():
@@ -264,3 +274,56 @@ def test_thread_count_invariance():
     finally:
         oracle.set_num_threads(t0)
     assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- r(t) recording schedule (R10)
+def _adler_rpsi(t, K, w, th0):
+    """r e^{i psi} = (e^{i th1} + e^{i th2}) / 2 of the closed-form two-oscillator solution."""
+    a, b = _adler_exact(t, K, w, *th0)
+    return (complex(math.cos(a), math.sin(a)) + complex(math.cos(b), math.sin(b))) / 2.0
+
+
+@pytest.mark.parametrize("mode", ["naive", "matvec", "op"])
+def test_rk4_records_r_on_schedule_adler(mode):
+    """orc_rk4 records r e^{i psi} of theta_n at n = 0, k, 2k, ... (reading R10, before stepping) and
+    captures theta after 10 steps: both against the Adler closed form at t = n h (RK4 error ~1e-11 at
+    h = 0.01); a schedule shifted by one step would be off by ~|dr/dt| h ~ 4e-3."""
+    K, w, h, k, nsteps = 1.0, 0.3, 0.01, 5, 200
+    th0 = np.array([0.1, 2.1])
+    inst = _complete(2, th0, np.array([w, w]))
+    g = oracle.Graph(inst)
+    _, th10, rt = oracle.rk4(g, th0, inst.omega, K, h, nsteps, k, mode=mode)
+    assert rt.shape == (nsteps // k + 1, 2)
+    got = rt[:, 0] * np.exp(1j * rt[:, 1])
+    t = np.arange(rt.shape[0]) * k * h
+    exact = np.array([_adler_rpsi(ti, K, w, th0) for ti in t])
+    assert np.max(np.abs(got - exact)) <= 1e-9
+    shifted = np.array([_adler_rpsi(ti + h, K, w, th0) for ti in t])
+    assert np.max(np.abs(got - shifted)) > 1e-4  # non-vacuity of the bound above
+    assert np.max(np.abs(th10 - np.array(_adler_exact(10 * h, K, w, *th0)))) <= 1e-11
+    # a trajectory shorter than 10 steps: theta10 is not captured past nsteps, the final state is
+    th, _, rt3 = oracle.rk4(g, th0, inst.omega, K, h, 3, 1, mode=mode)
+    assert rt3.shape == (4, 2)
+    assert np.max(np.abs(th - np.array(_adler_exact(3 * h, K, w, *th0)))) <= 1e-12
+
+
+@pytest.mark.parametrize("method,order", [("euler", 1), ("heun", 2), ("implicit_midpoint", 2)])
+def test_step_method_records_r_on_schedule(method, order):
+    """orc_step_method's r(t) samples: rt[i] is the order parameter of theta after i*k steps (the
+    same method run for exactly i*k steps, then the plain definition), and for the
+    second-order methods within C h^2 of the Adler closed form (a one-step shift costs ~4e-3)."""
+    K, w, h, k, nsteps = 1.0, 0.3, 0.01, 4, 100
+    th0 = np.array([0.1, 2.1])
+    inst = _complete(2, th0, np.array([w, w]))
+    g = oracle.Graph(inst)
+    _, rt = oracle.step_method(g, method, th0, inst.omega, K, h, nsteps, k)
+    assert rt.shape == (nsteps // k + 1, 2)
+    for i in (0, 1, 7, nsteps // k):
+        thi, _ = oracle.step_method(g, method, th0, inst.omega, K, h, i * k, 0)
+        z = np.exp(1j * thi).mean()
+        assert abs(rt[i, 0] * np.exp(1j * rt[i, 1]) - z) <= 1e-15, (method, i)
+    got = rt[:, 0] * np.exp(1j * rt[:, 1])
+    t = np.arange(rt.shape[0]) * k * h
+    exact = np.array([_adler_rpsi(ti, K, w, th0) for ti in t])
+    err = np.max(np.abs(got - exact))
+    assert err <= (5e-4 if order == 2 else 1e-2), err
