@@ -136,17 +136,72 @@ def _dist():
     return world, rank, local
 
 
-def cpu_oracle_rhs_rate(inst, rows_sample, mode="matvec"):
-    """Oracle RHS evaluations/s extrapolated from a bounded row sample (test infrastructure)."""
+def cpu_oracle_rhs_rate(inst, rows_sample, mode="matvec", threads=None, reps=1):
+    """Oracle RHS evaluations/s extrapolated from a bounded row sample (rows_sample None: the whole
+    graph), median of `reps` timings, on `threads` host threads (None: all).  Test infrastructure:
+    bench.py's cpu_baseline leg only."""
     import oracle
     og = oracle.Graph(inst)
-    rows = np.ascontiguousarray(rows_sample, np.int64)
-    oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode=mode, rows=rows[: min(64, rows.size)])  # warm
-    t0 = time.perf_counter()
-    oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode=mode, rows=rows)
-    dt = time.perf_counter() - t0
-    full = dt * inst.n / rows.size
-    return 1.0 / full, dt, oracle.num_threads()
+    all_threads = oracle.num_threads()
+    oracle.set_num_threads(threads or all_threads)
+    try:
+        rows = None if rows_sample is None else np.ascontiguousarray(rows_sample, np.int64)
+        nrow = inst.n if rows is None else rows.size
+        oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode=mode, rows=None if rows is None else rows[:64])  # warm
+        dts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode=mode, rows=rows)
+            dts.append(time.perf_counter() - t0)
+        dt = float(np.median(dts))
+        return 1.0 / (dt * inst.n / nrow), dt, oracle.num_threads()
+    finally:
+        oracle.set_num_threads(all_threads)
+
+
+# SURVEY 8(d) / BASELINE.md §3 oracle protocol per config: (mode, rows sampled at all cores, rows at 1 core).
+# None = the whole graph.  cfg2's naive mode costs N per row (1.1e12 sines per RHS): timed per row on 256
+# sampled rows and reported "per row", not extrapolated into the headline; its headline is the O(N) op form.
+def _cpu_protocol_plan(inst, cfg):
+    comm_rows = lambda k: np.flatnonzero(np.isin(inst.community, np.arange(0, inst.n_comm,
+                                                                           max(1, inst.n_comm // k))[:k]))
+    if cfg == 1:
+        return [("naive", None, None), ("op", None, None)]
+    if cfg == 2:
+        return [("op", None, None), ("naive", np.arange(0, inst.n, inst.n // 256)[:256], "per_row")]
+    if cfg == 3:
+        return [("matvec", None, None), ("naive", comm_rows(2), None)]
+    if cfg == 4:
+        return [("matvec", comm_rows(16), None)]
+    return [("matvec", comm_rows(128), comm_rows(1))]
+
+
+def cpu_protocol(inst, cfg):
+    """The oracle timed on this host at all cores and at 1 core (bounded samples), per mode."""
+    out, head = [], None
+    for mode, rows, extra in _cpu_protocol_plan(inst, cfg):
+        r_all, dt_all, cores = cpu_oracle_rhs_rate(inst, rows, mode, reps=3 if (rows is None and inst.n <= 70000) else 1)
+        rows1 = rows
+        if extra is not None and not isinstance(extra, str):
+            rows1 = extra
+        r_one, dt_one, _ = cpu_oracle_rhs_rate(inst, rows1, mode, threads=1)
+        nrow = inst.n if rows is None else rows.size
+        rec = {"mode": mode, "rows": nrow, "rhs_per_s_all_cores": r_all, "rhs_per_s_1_core": r_one,
+               "steps_per_s_all_cores": r_all / 4.0, "steps_per_s_1_core": r_one / 4.0, "cores": cores,
+               "seconds": dt_all + dt_one}
+        if extra == "per_row":
+            rec = {"mode": mode, "rows": nrow, "unit": "rows/s (not extrapolated)",
+                   "rows_per_s_all_cores": r_all * inst.n, "rows_per_s_1_core": r_one * inst.n, "cores": cores,
+                   "seconds": dt_all + dt_one}
+        elif head is None:
+            head = (rec, nrow)
+        out.append(rec)
+    rec, nrow = head
+    return {"value": rec["rhs_per_s_all_cores"], "unit": UNIT, "cores": rec["cores"], "kind": "oracle",
+            "sample": f"oracle {rec['mode']} RHS on {nrow} of {inst.n} rows" +
+                      ("" if nrow == inst.n else f", extrapolated x{inst.n / nrow:.1f}") +
+                      "; steps/s = RHS/s / 4 (an RK4 step is 4 RHS evaluations plus O(N) updates)",
+            "protocol": out, "host": _host_info()}
 
 
 def _sample_rows(inst, cfg):
@@ -372,11 +427,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rows = _sample_rows(inst, args.config)
-        rate, dt, cores = cpu_oracle_rhs_rate(inst, rows)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"oracle matvec RHS (P:443, O(nnz), no block sums) on {rows.size} of {inst.n} rows "
-                         f"({dt:.1f} s), extrapolated x{inst.n / rows.size:.1f}"}
+        cpu = cpu_protocol(inst, args.config)
 
     ws = info["bytes_pool"] + 56 * inst.n
     l2_note = (f"inputs larger than L2 (index pool {info['bytes_pool'] / 1e9:.2f} GB + vectors vs 126 MB L2)"

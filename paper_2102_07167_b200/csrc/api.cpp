@@ -1,5 +1,7 @@
 // api.cpp — the C ABI of libkur.so (include/kur.h): handle ownership, device
 // memory, launch orchestration, error conventions.  Product code.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <omp.h>
@@ -11,6 +13,8 @@
 #include <new>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "kernels.h"
 #include "kur.h"
@@ -74,6 +78,7 @@ struct kur_graph {
   double *d_rowscale = nullptr, *d_potc = nullptr;
   double *xsend = nullptr, *xrecv = nullptr;  // world > 1: packed exchange buffers
   double2* Wh = nullptr;                      // world > 1: phase-A row sums
+  CUtensorMap tmaps[2];                       // remote warp 3: z viewed as [n_pad][2] fp64 (gather4)
   cudaStream_t comm_stream = nullptr;         // NCCL: exchange + unpack + finish, overlapping phase A
   cudaEvent_t ev_b = nullptr, ev_exch = nullptr;
   bool exch_pending = false;                  // comm_stream holds an exchange the next phase B waits for
@@ -90,6 +95,10 @@ struct kur_graph {
   std::vector<cudaEvent_t> ev;        // pool, reused
   std::vector<std::pair<int, int>> ev_kind;  // per recorded pair: (0 prologue | 1 k_stage | 2 k_remote, RHS evals)
   bool small = false;                 // whole kur_step in one single-CTA launch
+  bool persist = false;               // entry-free plan: whole RK4 kur_step in one cooperative launch
+  double2* pbuf = nullptr;            // persist: [2][ntiles] tile partials
+  unsigned int* gbar = nullptr;       // persist: grid-barrier words
+  int32_t* d_big = nullptr;           // communities of > 64 tiles
   size_t ev_used = 0;
   cudaError_t mark(cudaStream_t s) {  // records the next event of the pool on s
     if (!timing) return cudaSuccess;
@@ -107,7 +116,7 @@ struct kur_graph {
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
                     xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh, d_rchunks, d_rem_lp, d_flag, d_xticket,
-                    d_peer_x, d_peer_flag, theta_ws, omega_ws};
+                    d_peer_x, d_peer_flag, theta_ws, omega_ws, pbuf, gbar, d_big};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -367,7 +376,27 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   dp.remote_warp = 0;
   if (dp.has_remote) {
     const char* rm = std::getenv("KUR_REMOTE_MODE");
-    if (rm && (rm[0] == '1' || rm[0] == '2')) dp.remote_warp = rm[0] - '0';
+    if (rm && (rm[0] == '1' || rm[0] == '2' || rm[0] == '3')) dp.remote_warp = rm[0] - '0';
+  }
+  dp.tmaps = nullptr;
+  dp.zbuf[0] = g->zA;
+  dp.zbuf[1] = g->zB;
+  if (dp.remote_warp == 3) {  // tensor maps for tile::gather4: 16-byte rows of z, box of one row
+    PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess || !enc)
+      return bail(cudaErrorNotSupported, "cuTensorMapEncodeTiled");
+    const double2* bufs[2] = {g->zA, g->zB};
+    for (int i = 0; i < 2; ++i) {
+      cuuint64_t gdim[2] = {2, (cuuint64_t)g->n_pad};
+      cuuint64_t gstr[1] = {sizeof(double2)};
+      cuuint32_t box[2] = {2, 1}, es[2] = {1, 1};
+      if (enc(&g->tmaps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)bufs[i], gdim, gstr, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return bail(cudaErrorInvalidValue, "cuTensorMapEncodeTiled (z)");
+    }
+    dp.tmaps = g->tmaps;
   }
   dp.n_local = g->n_local;
   dp.Wr = g->Wr;
@@ -379,6 +408,14 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   dp.n_rchunks = (int32_t)(P.rem_lp.size());
   // tiny graphs run a whole trajectory in one CTA (launch latency dominates otherwise)
   g->small = P.small;
+  {
+    std::vector<int32_t> big;
+    for (int32_t c = 0; c < P.C; ++c)
+      if (P.comm_tile0[(size_t)c + 1] - P.comm_tile0[(size_t)c] > 64) big.push_back(c);
+    if ((e = upload(&g->d_big, big)) != cudaSuccess) return bail(e, "big communities");
+    dp.big_comm = g->d_big;
+    dp.n_big = (int32_t)big.size();
+  }
   dp.shard_row0 = g->d_shard_row0;
   dp.shard_tile0 = g->d_shard_tile0;
   dp.xrows = xrows;
@@ -397,6 +434,14 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   dp.pmax = g->pmax;
   dp.S = g->S;
   dp.ctrl = g->ctrl;
+  // entry-free plans (world 1, beyond the single-CTA size): RK4 trajectories in one cooperative launch
+  if (!g->small && persist_fits(dp)) {
+    if ((e = cudaMalloc((void**)&g->pbuf, sizeof(double2) * 2 * (size_t)dp.ntiles)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&g->gbar, 2 * sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMemset(g->gbar, 0, 2 * sizeof(unsigned int))) != cudaSuccess)
+      return bail(e, "persistent trajectory buffers");
+    g->persist = std::getenv("KUR_NO_PERSIST") == nullptr;  // (A/B switch)
+  }
 
   kur_graph_info_t& I = g->info;
   I.n = P.n;
@@ -500,8 +545,20 @@ enum { PH_PROLOGUE = -1 };
 
 // mode: PH_PROLOGUE or a StageMode.  zin/zout/Tin/Tout select the ping-pong buffers.
 // commit (prologue only): theta = acc first (implicit midpoint step completion).
+// NVTX range per phase (a stage = one RHS evaluation), visible in nsys/ncu timelines; free without a tool
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+const char* phase_name(int mode) {
+  static const char* names[] = {"kur rhs", "kur RK4 S1", "kur RK4 S2", "kur RK4 S3", "kur RK4 S4", "kur potential",
+                                "kur Euler", "kur Heun H1", "kur Heun H2", "kur midpoint M0", "kur midpoint MI"};
+  return mode < 0 ? "kur prologue" : (mode < 11 ? names[mode] : "kur stage");
+}
+
 kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vector<RankIO>& io, double K,
                      double h, int record, bool z_from_A, cudaStream_t s, bool commit = false) {
+  NvtxRange nvtx_(phase_name(mode));
   const int world = gs[0]->world;
   std::vector<StageArgs> args(gs.size());
   for (size_t r = 0; r < gs.size(); ++r) {
@@ -689,6 +746,23 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
     KUR_CUDA(launch_small(g->dp, a, g->zA, g->zB, g->TA, g->TB, (long long)nsteps, s));
     KUR_CUDA(g->mark(s));
     if (g->timing) g->ev_kind.push_back({1, (int)std::min<int64_t>(4 * nsteps, INT32_MAX)});
+    return KUR_OK;
+  }
+  NvtxRange nvtx_("kur_step");
+  if (gs.size() == 1 && gs[0]->persist && method == KUR_RK4) {  // entry-free plan: one cooperative launch
+    kur_graph* g = gs[0];
+    StageArgs a{};
+    a.theta = io[0].theta;
+    a.omega = io[0].omega;
+    a.KN = K / (double)g->n;
+    a.K = K;
+    a.h = h;
+    KUR_CUDA(g->mark(s));
+    KUR_CUDA(launch_persist_rk4(g->dp, a, g->pbuf, g->gbar, (long long)nsteps, s));
+    KUR_CUDA(g->mark(s));
+    if (g->timing) g->ev_kind.push_back({1, (int)std::min<int64_t>(4 * nsteps, INT32_MAX)});
+    if (host_out) KUR_CUDA(cudaMemcpyAsync(host_out, io[0].theta, sizeof(double) * (size_t)g->n_local,
+                                           cudaMemcpyDefault, s));
     return KUR_OK;
   }
   kur_status st = run_phase(gs, PH_PROLOGUE, io, K, h, REC_START, true, s);

@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstring>
 
 #include "kernels.h"
 
@@ -156,6 +157,13 @@ __device__ __forceinline__ double block_max(double d, double* red) {
     for (int o = NWARPS / 2; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
   }
   return d;
+}
+
+// a4: k_j = omega_j + (K/M_j)(cos th_j Im W_j - sin th_j Re W_j), with explicit roundings:
+// every kernel evaluates it through this one expression, so the per-row arithmetic is bitwise the
+// same in all of them whatever the compiler would contract.
+__device__ __forceinline__ double rhs_k(double om, double kn, double zx, double zy, double wx, double wy) {
+  return __fma_rn(kn, __fma_rn(zx, wy, -__dmul_rn(zy, wx)), om);
 }
 
 // Sum of the 9 window-local z entries named by one 16-byte unit of 13-bit slots
@@ -482,6 +490,75 @@ __device__ __forceinline__ void remote_warp_tma(const DevPlan& dp, const TileDes
   }
 }
 
+// remote_warp == 3: as remote_warp_tma, but each lane fetches its 4 entries with ONE TMA
+// tile::gather4 (4 rows of z viewed as a [n_pad][2] fp64 tensor) into its own 128-byte cell of the
+// slot; lane l rotates its coordinates by l & 3 so a quarter-warp's reads of entry e spread over 4
+// bank groups (2-way conflicts: 1/4 wavefront per entry, against 1 for an LDG gather).
+__device__ __forceinline__ void remote_warp_g4(const DevPlan& dp, const TileDesc& T, const CUtensorMap* tmz,
+                                               double2* ring, uint64_t* rbar, uint64_t pol, int lane) {
+  const PartDesc P = dp.parts[T.part0 + T.nhot];
+  const int lp = P.neg >> 8;
+  const uint32_t nch = P.nchunks;
+  const uint32_t rot = lane & 3;
+  uint32_t ci = 0, gi = 0, qi = 0;
+  uint2 cdi = nch > 0 ? __ldg(dp.chunks + P.chunk0) : make_uint2(0, 0);
+  uint32_t sgn = 0;
+  auto issue = [&]() {
+    while (ci < nch && gi >= cdi.y) {
+      ++ci;
+      gi = 0;
+      if (ci < nch) cdi = __ldg(dp.chunks + P.chunk0 + ci);
+    }
+    if (ci >= nch) return;
+    const uint4 u = ldg_stream(dp.pool + cdi.x + HDR_UNITS + (size_t)gi * 32 + lane, pol);
+    const uint32_t s = qi % RING_SLOTS_G4;
+    sgn = (sgn & ~(0xFu << (4 * s))) |
+          (((u.x >> 31) | ((u.y >> 31) << 1) | ((u.z >> 31) << 2) | ((u.w >> 31) << 3)) << (4 * s));
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(rbar + s)), "r"(32 * 64)
+                   : "memory");
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    auto sel = [&](uint32_t k) {  // entry k of the unit (selects, no local-memory array)
+      const uint32_t v = k == 0 ? u.x : k == 1 ? u.y : k == 2 ? u.z : u.w;
+      return v & 0x7FFFFFFFu;
+    };
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_addr(ring + (size_t)s * 256 + lane * 8)),
+        "l"(tmz), "r"(0), "r"(sel(rot)), "r"(sel((rot + 1) & 3)), "r"(sel((rot + 2) & 3)), "r"(sel((rot + 3) & 3)),
+        "r"(smem_addr(rbar + s))
+        : "memory");
+    ++gi;
+    ++qi;
+  };
+  for (int k = 0; k < RING_SLOTS_G4 - 1; ++k) issue();
+  uint32_t qc = 0, phases = 0;
+  for (uint32_t c = 0; c < nch; ++c) {
+    const uint2 cd = __ldg(dp.chunks + P.chunk0 + c);
+    const uint16_t row = reinterpret_cast<const uint16_t*>(dp.pool + cd.x)[lane];
+    double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
+    for (uint32_t g = 0; g < cd.y; ++g) {
+      issue();
+      const uint32_t s = qc % RING_SLOTS_G4;
+      mbar_wait(rbar + s, (phases >> s) & 1u);
+      phases ^= 1u << s;
+      const uint32_t m = sgn >> (4 * s);
+      const double2* cell = ring + (size_t)s * 256 + lane * 8;  // position p holds entry (p + rot) & 3
+      double2 a0 = cell[(0 - rot) & 3], a1 = cell[(1 - rot) & 3], a2 = cell[(2 - rot) & 3], a3 = cell[(3 - rot) & 3];
+      if (m & 1u) a0 = make_double2(-a0.x, -a0.y);
+      if (m & 2u) a1 = make_double2(-a1.x, -a1.y);
+      if (m & 4u) a2 = make_double2(-a2.x, -a2.y);
+      if (m & 8u) a3 = make_double2(-a3.x, -a3.y);
+      x0 += a0.x; y0 += a0.y; x1 += a1.x; y1 += a1.y;
+      x0 += a2.x; y0 += a2.y; x1 += a3.x; y1 += a3.y;
+      __syncwarp();
+      ++qc;
+    }
+    wr_store(dp, T, row, lp, lane, x0 + x1, y0 + y1);
+  }
+}
+
 // world > 1: one double of this rank's packed exchange record [phases | per tile (sum z, max
 // |update|)] at offset off — into the send buffer (all-gather), or, with the fused peer-store
 // exchange, straight into every rank's receive buffer over NVLink (slot `rank` of each).
@@ -550,9 +627,9 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
     }
     dp.S[c] = make_double2(x, y);
   }
-  for (int c = 0; c < dp.C; ++c) {  // large communities (uniform branch): fixed-shape block reduction
+  for (int i = 0; i < dp.n_big; ++i) {  // communities of > BIG tiles (uniform): fixed-shape block reduction
+    const int c = dp.big_comm[i];
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
-    if (t1 - t0 <= BIG) continue;
     double x = 0.0, y = 0.0;
     for (int t = t0 + tid; t < t1; t += NTHREADS) {
       const double2 v = __ldcg(dp.partial + t);
@@ -686,10 +763,11 @@ __device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs
 // zs: [WZ + 8] window + zero sentinels, Ws: [rows_per_tile] row sums (both
 // unused when the plan has no parts).  Returns the thread's partial sums of
 // the next stage's z in (px, py) and whether a phase became non-finite.
-template <int MODE, bool SMALL>
+template <int MODE, bool SMALL, bool RW = false>
 __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a, const TileDesc& T, double2* zs,
                                            double2* Ws, uint64_t* bar, uint32_t& phase, double& px, double& py,
-                                           double& dmax, double2* ring = nullptr, uint64_t* rbar = nullptr) {
+                                           double& dmax, double2* ring = nullptr, uint64_t* rbar = nullptr,
+                                           const CUtensorMap* tmz = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool parts = dp.has_parts;
   // the remote part of the tile was summed by k_remote into Wr (added in the finalize);
@@ -726,13 +804,11 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
 #endif
   // remote warp: the last warp sums the tile's remote part (into Wr) while the other NWARPS - 1
   // gather the hot parts, which then synchronise on named barrier 1 instead of the block barrier
-#ifdef KUR_NO_REMOTE_WARP
-  constexpr bool rw = false;
-#else
-  const bool rw = !SMALL && addr && dp.remote_warp;
-#endif
+  // (a compile-time variant: the branch alone costs the default kernel ~4 % even when not taken)
+  const bool rw = RW && !SMALL && addr;
   if (rw && warp == NWARPS - 1) {
-    if (dp.remote_warp == 1) remote_warp_tma(dp, T, a.zin, ring, rbar, pol, lane);
+    if (dp.remote_warp == 3) remote_warp_g4(dp, T, tmz, ring, rbar, pol, lane);
+    else if (dp.remote_warp == 1) remote_warp_tma(dp, T, a.zin, ring, rbar, pol, lane);
     else remote_warp_ldg(dp, T, a.zin, pol, lane);
     __syncthreads();  // joins the hot warps below (Wr complete, Ws complete)
   } else {
@@ -803,7 +879,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       px += -a.omega[li] * a.theta[li] + 0.5 * a.K * sm * (dp.potc[li] - (zj.x * wx + zj.y * wy));
       continue;
     }
-    const double k = a.omega[li] + kn * (zj.x * wy - zj.y * wx);
+    const double k = rhs_k(a.omega[li], kn, zj.x, zj.y, wx, wy);
     if (MODE == MODE_RHS) {
       a.out[li] = k;
     } else {
@@ -938,8 +1014,9 @@ __global__ void __launch_bounds__(KREM_THREADS, KREM_CTAS_PER_SM) k_remote(const
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const StageArgs a) {
+template <int MODE, bool RW>
+__global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const StageArgs a,
+                                                       const __grid_constant__ CUtensorMap tmz) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* zs = reinterpret_cast<double2*>(smem_raw);  // [WZ + 8]: window + 8 zero sentinels
   double2* Ws = zs + (WZ + 8);                         // [rows_per_tile]: W_j of the tile
@@ -970,11 +1047,12 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
     s_nonfinite = 0;
     mbar_init(&bar, 1);
   }
-  if (dp.remote_warp == 1 && tid >= 32 && tid < 32 + RING_SLOTS) mbar_init(rbar + (tid - 32), 1);
+  if (RW && (dp.remote_warp == 1 || dp.remote_warp == 3) && tid >= 32 && tid < 32 + RING_SLOTS)
+    mbar_init(rbar + (tid - 32), 1);
   __syncthreads();
   uint32_t phase = 0;
   double px, py, dmax;
-  const bool bad = stage_rows<MODE, false>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax, ring, rbar);
+  const bool bad = stage_rows<MODE, false, RW>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax, ring, rbar, &tmz);
   if (MODE == MODE_RHS || a.phase == PHASE_A) return;
   constexpr bool FINAL = MODE == MODE_S4 || MODE == MODE_E1 || MODE == MODE_H2;
   if (FINAL && bad) s_nonfinite = 1;
@@ -1120,7 +1198,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_small_dense(const DevPlan dp, S
       for (int k = 0; k < R; ++k) {
         const int lr = tid + k * NTHREADS;
         if (lr >= T.nrows) break;
-        const double kk = om[k] + kn[k] * (zc[k] * wy - zsn[k] * wx);
+        const double kk = rhs_k(om[k], kn[k], zc[k], zsn[k], wx, wy);
         double ts;
         if (st == 1) {
           acc[k] = kk;
@@ -1150,6 +1228,199 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_small_dense(const DevPlan dp, S
   }
   if (bad) ct->nonfinite = 1;
   if (tid == 0) ct->step = nsteps;
+}
+
+// ---- persistent grid-synchronous RK4 for entry-free plans (no stored entries: complete graphs and
+// graphs whose blocks are all full or empty; world 1, every tile's CTA co-resident -- cooperative
+// launch).  W_j = T_{c(j)} (P:557-561 with empty lists; P:240-255 for one community), so a stage
+// needs nothing but the block sums of the previous one: each CTA keeps its tile's z and omega in
+// shared memory and theta_n, acc in registers for the whole trajectory, publishes its tile partial
+// of z, and after ONE grid barrier per stage every CTA reduces all partials itself in finish_reduce's
+// exact summation shapes -- the same bits as the general path (k_prologue + k_stage<S1..S4>), without
+// a kernel boundary or a last-CTA tail per stage.
+__device__ __forceinline__ void grid_barrier(unsigned int* gbar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int gen = *(volatile unsigned int*)(gbar + 1);  // read before arriving
+    __threadfence();
+    if (atomicAdd(gbar, 1u) == gridDim.x - 1) {
+      atomicExch(gbar, 0u);
+      __threadfence();
+      atomicAdd(gbar + 1, 1u);
+    } else {
+      unsigned int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar + 1) : "memory");
+      } while (v == gen);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// S_b of every community from tile partials src (finish_reduce's shapes: one thread per community
+// summing its tiles in order, or a fixed-shape block reduction for communities of > 64 tiles), into
+// shared S_sh; then T of community c and (r, psi) = (1/N) sum_b S_b.  Ends with a block barrier.
+__device__ __forceinline__ void local_reduce(const DevPlan& dp, const double2* src, double2* S_sh, double2* red,
+                                             int c_own, double2* sT, double* s_rpsi) {
+  const int tid = threadIdx.x;
+  constexpr int BIG = 64;
+  for (int c = tid; c < dp.C; c += NTHREADS) {
+    const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
+    if (t1 - t0 > BIG) continue;
+    double x = 0.0, y = 0.0;
+    for (int t = t0; t < t1; ++t) {
+      const double2 v = __ldcg(src + t);
+      x += v.x;
+      y += v.y;
+    }
+    S_sh[c] = make_double2(x, y);
+  }
+  for (int i = 0; i < dp.n_big; ++i) {
+    const int c = dp.big_comm[i];
+    const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
+    double x = 0.0, y = 0.0;
+    for (int t = t0 + tid; t < t1; t += NTHREADS) {
+      const double2 v = __ldcg(src + t);
+      x += v.x;
+      y += v.y;
+    }
+    block_sum2(x, y, red);
+    if (tid == 0) S_sh[c] = make_double2(x, y);
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0) {  // T of this tile's community = sum over its dense column communities
+    double x = 0.0, y = 0.0;
+    for (int i = dp.D_ptr[c_own]; i < dp.D_ptr[c_own + 1]; ++i) {
+      const double2 v = S_sh[dp.D_idx[i]];
+      x += v.x;
+      y += v.y;
+    }
+    *sT = make_double2(x, y);
+  }
+  double x = 0.0, y = 0.0;  // r e^{i psi} = (1/N) sum_b S_b
+  for (int c = tid; c < dp.C; c += NTHREADS) {
+    const double2 v = S_sh[c];
+    x += v.x;
+    y += v.y;
+  }
+  block_sum2(x, y, red);
+  if (tid == 0) {
+    const double cm = x / (double)dp.n, sm = y / (double)dp.n;
+    const double r = sqrt(cm * cm + sm * sm);
+    s_rpsi[0] = r;
+    s_rpsi[1] = r == 0.0 ? 0.0 : atan2(sm, cm);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void record_rpsi(const DevPlan& dp, const double* rp, long long step) {
+  Ctrl* ct = dp.ctrl;
+  ct->rpsi[0] = rp[0];
+  ct->rpsi[1] = rp[1];
+  if (ct->record_every > 0 && ct->r_trace && step % ct->record_every == 0) {
+    const long long i = step / ct->record_every;
+    if (i < ct->nrec_cap) {
+      ct->r_trace[2 * i] = rp[0];
+      ct->r_trace[2 * i + 1] = rp[1];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS, 2) k_persist_rk4(const DevPlan dp, const StageArgs a, double2* pbuf,
+                                                             unsigned int* gbar, long long nsteps) {
+  constexpr int R = MAX_TILE_ROWS_NOPARTS / NTHREADS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* zc = reinterpret_cast<double*>(smem_raw);  // [rows_per_tile] z of the stage state
+  double* zsn = zc + dp.rows_per_tile;
+  double* om = zsn + dp.rows_per_tile;                // [rows_per_tile] omega
+  double2* S_sh = reinterpret_cast<double2*>(om + dp.rows_per_tile);  // [C]
+  __shared__ double2 red[NWARPS];
+  __shared__ double2 sT;
+  __shared__ double s_rpsi[2];
+  const int tid = threadIdx.x, lt = blockIdx.x;
+  const TileDesc T = dp.tiles[lt];
+  const int nt = gridDim.x;
+  double thn[R], acc[R];
+  // prologue: z(theta_n), the tile partial, S_b, T, (r, psi) of theta_0 (recorded as n = 0)
+  double x = 0.0, y = 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int lr = tid + k * NTHREADS;
+    thn[k] = lr < T.nrows ? a.theta[T.row0 + lr - dp.row_begin] : 0.0;
+    acc[k] = 0.0;
+    if (lr < T.nrows) om[lr] = a.omega[T.row0 + lr - dp.row_begin];
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int lr = tid + k * NTHREADS;
+    if (lr >= T.nrows) break;
+    double s, c;
+    sincos(thn[k], &s, &c);
+    zc[lr] = c;
+    zsn[lr] = s;
+    x += c;
+    y += s;
+  }
+  block_sum2(x, y, red);
+  if (tid == 0) pbuf[lt] = make_double2(x, y);
+  grid_barrier(gbar);
+  local_reduce(dp, pbuf, S_sh, red, T.comm, &sT, s_rpsi);
+  if (lt == 0 && tid == 0) record_rpsi(dp, s_rpsi, 0);
+  bool bad = false;
+  int par = 1;  // partial buffer half of the next publication
+  for (long long n = 0; n < nsteps; ++n) {
+#pragma unroll 1
+    for (int st = 1; st <= 4; ++st) {
+      const double2 Tc = sT;
+      const double wx = Tc.x + 0.0, wy = Tc.y + 0.0;  // W_j = T_c + (empty lists)
+      double px = 0.0, py = 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int lr = tid + k * NTHREADS;
+        if (lr >= T.nrows) break;
+        const int li = T.row0 + lr - dp.row_begin;
+        const double kn = dp.rowscale ? a.K * dp.rowscale[li] : a.KN;
+        const double kk = rhs_k(om[lr], kn, zc[lr], zsn[lr], wx, wy);
+        double ts;
+        if (st == 1) {
+          acc[k] = kk;
+          ts = __dadd_rn(thn[k], __dmul_rn(a.h / 2.0, kk));
+        } else if (st == 2) {
+          acc[k] = __dadd_rn(acc[k], __dmul_rn(2.0, kk));
+          ts = __dadd_rn(thn[k], __dmul_rn(a.h / 2.0, kk));
+        } else if (st == 3) {
+          acc[k] = __dadd_rn(acc[k], __dmul_rn(2.0, kk));
+          ts = __dadd_rn(thn[k], __dmul_rn(a.h, kk));
+        } else {  // theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
+          ts = __dadd_rn(thn[k], __dmul_rn(a.h / 6.0, __dadd_rn(acc[k], kk)));
+          thn[k] = ts;
+          bad |= !isfinite(ts);
+        }
+        double s, c;
+        sincos(ts, &s, &c);
+        zc[lr] = c;
+        zsn[lr] = s;
+        px += c;
+        py += s;
+      }
+      block_sum2(px, py, red);
+      double2* dst = pbuf + (size_t)par * nt;
+      if (tid == 0) dst[lt] = make_double2(px, py);
+      grid_barrier(gbar);
+      local_reduce(dp, dst, S_sh, red, T.comm, &sT, s_rpsi);
+      if (st == 4 && lt == 0 && tid == 0) record_rpsi(dp, s_rpsi, n + 1);
+      par ^= 1;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int lr = tid + k * NTHREADS;
+    if (lr < T.nrows) a.theta[T.row0 + lr - dp.row_begin] = thn[k];
+  }
+  if (bad) dp.ctrl->nonfinite = 1;
+  if (lt == 0 && tid == 0) dp.ctrl->step = nsteps;
 }
 
 // world > 1: z of the non-local rows from the exchanged stage phases (the same
@@ -1236,14 +1507,14 @@ __global__ void k_permute(const int32_t* __restrict__ perm, int64_t n, const dou
   else out[perm[i]] = in[i];
 }
 
-template <int MODE>
+template <int MODE, bool RW>
 cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
   static std::atomic<uint64_t> attr_set{0};  // one bit per device (the attribute is per device context)
-  const size_t smem = stage_smem_bytes(MAX_TILE_ROWS) + RING_BYTES;
+  const size_t smem = stage_smem_bytes(MAX_TILE_ROWS) + (RW ? RING_BYTES : 0);
   int dev = 0;
   cudaGetDevice(&dev);
   if (!((attr_set.load() >> (dev & 63)) & 1)) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_stage<MODE, RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(1ull << (dev & 63));
   }
@@ -1251,9 +1522,18 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
     cudaError_t e = launch_remote(dp, a.zin, s);
     if (e != cudaSuccess) return e;
   }
-  const size_t dyn = dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) + (dp.remote_warp == 1 ? RING_BYTES : 0) : 0;
-  k_stage<MODE><<<dp.ntiles, NTHREADS, dyn, s>>>(dp, a);
+  const size_t dyn = dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) +
+                                         ((dp.remote_warp == 1 || dp.remote_warp == 3) ? RING_BYTES : 0) : 0;
+  CUtensorMap tm;  // remote_warp 3: the tensor map of the stage's input z (zA or zB)
+  if (dp.tmaps) tm = dp.tmaps[a.zin == dp.zbuf[0] ? 0 : 1];
+  else memset(&tm, 0, sizeof(tm));
+  k_stage<MODE, RW><<<dp.ntiles, NTHREADS, dyn, s>>>(dp, a, tm);
   return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
+  return dp.remote_warp ? launch_stage_m<MODE, true>(dp, a, s) : launch_stage_m<MODE, false>(dp, a, s);
 }
 
 }  // namespace
@@ -1338,6 +1618,37 @@ cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, dou
   }
   k_small<<<1, NTHREADS, dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) : 0, s>>>(dp, a, zA, zB, TA, TB, nsteps);
   return cudaGetLastError();
+}
+
+size_t persist_smem_bytes(const DevPlan& dp) {
+  return sizeof(double) * 3 * (size_t)dp.rows_per_tile + sizeof(double2) * (size_t)std::max(dp.C, 1);
+}
+
+bool persist_fits(const DevPlan& dp) {
+  if (dp.world != 1 || dp.has_parts || dp.ntiles <= 0 || dp.rows_per_tile > MAX_TILE_ROWS_NOPARTS) return false;
+  const size_t smem = persist_smem_bytes(dp);
+  if (smem > 200 * 1024) return false;
+  int dev = 0, sms = 0, nb = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaFuncSetAttribute(k_persist_rk4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persist_rk4, NTHREADS, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (long long)nb * sms >= dp.ntiles;
+}
+
+cudaError_t launch_persist_rk4(const DevPlan& dp, const StageArgs& a, double2* pbuf, unsigned int* gbar,
+                               long long nsteps, cudaStream_t s) {
+  const size_t smem = persist_smem_bytes(dp);
+  cudaError_t e = cudaFuncSetAttribute(k_persist_rk4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  DevPlan d = dp;
+  StageArgs aa = a;
+  void* args[] = {(void*)&d, (void*)&aa, (void*)&pbuf, (void*)&gbar, (void*)&nsteps};
+  return cudaLaunchCooperativeKernel((const void*)k_persist_rk4, dim3((unsigned)dp.ntiles), dim3(NTHREADS), args,
+                                     smem, s);
 }
 
 cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, unsigned int expect,

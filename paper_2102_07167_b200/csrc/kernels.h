@@ -1,5 +1,6 @@
 // kernels.h — device-side plan + launchers (product code; used by api.cpp).
 #pragma once
+#include <cuda.h>  // CUtensorMap (type only; the encoder is fetched through the runtime)
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -35,13 +36,17 @@ struct DevPlan {
   int32_t remote_warp;        // has_remote: 0 = the k_remote pass before each k_stage; inside k_stage, one
                               // warp of each tile sums its remote part while the others gather the hot
                               // windows: 1 = z gathered by 16-byte TMA bulk copies into a shared-memory
-                              // ring, 2 = LDG gathers
+                              // ring, 2 = LDG gathers, 3 = TMA tile::gather4 (4 entries per request)
+  const CUtensorMap* tmaps;   // remote_warp 3: HOST array [2] = tensor maps of zbuf[0], zbuf[1] (launcher only)
+  const double2* zbuf[2];     // zA, zB (device)
   const TileDesc* tiles;      // [ntiles]
   const int32_t* order;       // [ntiles] launch order
   const PartDesc* parts;      // [n_parts]
   const uint2* chunks;        // [n_chunks] {header offset, groups}
   const uint4* pool;          // index units
   const int32_t* comm_tile0;  // [C+1] global tile ids
+  const int32_t* big_comm;    // [n_big] communities of more than 64 tiles (block-reduced block sums)
+  int32_t n_big;
   const int32_t* D_ptr;       // [C+1]
   const int32_t* D_idx;
   const int32_t* comm_size;   // [C]
@@ -124,6 +129,11 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
 cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, double2* zB, double2* TA, double2* TB,
                          long long nsteps, cudaStream_t s);
 // expect: with the fused peer-store exchange, the arrival count that completes this exchange
+// entry-free plans, world 1: the whole RK4 trajectory in one cooperative launch (one CTA per tile,
+// all co-resident; pbuf [2 * ntiles] partial halves, gbar [2] zeroed grid-barrier words)
+bool persist_fits(const DevPlan& dp);
+cudaError_t launch_persist_rk4(const DevPlan& dp, const StageArgs& a, double2* pbuf, unsigned int* gbar,
+                               long long nsteps, cudaStream_t s);
 cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, unsigned int expect,
                           cudaStream_t s);
 cudaError_t launch_finish(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
@@ -135,6 +145,9 @@ size_t stage_smem_bytes(int rows_per_tile);
 // remote warp (remote_warp == 1): RING_SLOTS groups of 32 lanes x 4 entries x 16 bytes in flight
 constexpr int RING_SLOTS = 6;
 constexpr size_t RING_BYTES = (size_t)RING_SLOTS * 128 * 16;
+// remote warp 3 (gather4): a slot is 32 lanes x one 128-byte cell (64 bytes used)
+constexpr int RING_SLOTS_G4 = 3;
+static_assert((size_t)RING_SLOTS_G4 * 32 * 128 <= RING_BYTES, "gather4 ring");
 // variable-step RK4: tile_ss[t] = sum over tile t's rows of ((y2 - y1) / (atol + rtol |y2|))^2
 cudaError_t launch_errnorm(const DevPlan& dp, const double* y1, const double* y2, double atol, double rtol,
                            double* tile_ss, cudaStream_t s);

@@ -90,3 +90,30 @@ def test_adaptive_group_bitwise(peer):
     torch.cuda.synchronize()
     assert rej3 == rej1 and np.array_equal(t3, t1) and np.array_equal(h3, h1) and np.array_equal(rp3, rp1)
     assert torch.equal(torch.cat(ths), th1)
+
+
+def _paper_fig2_instance(M, K):
+    """P:137-140 and P:361-362: omega_m = 1 + omega_0 (2m - M - 1)/(M - 1) with omega_0 = 2,
+    theta_m(0) = 2 pi m / M, complete graph (the classical model), coupling K."""
+    m = np.arange(1, M + 1)
+    A = np.ones((M, M), np.uint8) - np.eye(M, dtype=np.uint8)
+    return kurgen.from_dense(A, np.zeros(M, np.int64), kind="zeros", omega=1.0 + 2.0 * (2 * m - M - 1) / (M - 1),
+                             theta0=2 * np.pi * m / M, K=K)
+
+
+@pytest.mark.parametrize("K", [1.0, 5.0])
+def test_paper_synchronisation_claim_k5(K):
+    """P:361-375 (Figs. 2-5): M = 10^2, T = 200, variable-step RK4: "the modulus of the complex order
+    parameter is close to one for K = 5" (qualitative, not a parity number the paper prints); K = 1 stays
+    far from synchrony.  GPU and oracle take the same accepted steps and agree on r e^{i psi}."""
+    inst = _paper_fig2_instance(100, K)
+    run, th, t, h, rp, rej, (th_r, t_r, h_r, rp_r, rej_r) = _both(inst, 200.0, 0.01, mode="naive", atol=1e-8,
+                                                                  rtol=1e-8)
+    assert len(t) == len(t_r) and rej == rej_r and t[-1] == 200.0
+    assert np.max(np.abs(complex_rpsi(rp) - complex_rpsi(rp_r))) <= R_TOL
+    r_end = rp[-1, 0]
+    if K == 5.0:
+        assert r_end >= 0.9, r_end
+        assert np.all(rp[len(rp) // 2:, 0] >= 0.9)  # locked for the second half of [0, T]
+    else:
+        assert r_end <= 0.5, r_end

@@ -134,12 +134,13 @@ def test_group_bitwise_world_independent_tiles(case, world):
 @pytest.mark.parametrize("world", [1, 2])
 def test_remote_modes_bitwise(world, monkeypatch):
     """The remote part summed by the k_remote pass (KUR_REMOTE_MODE=0), by one warp of the stage kernel
-    with TMA gathers (1) or with LDG gathers (2): the same bits (world 2: phase B with the remote warp)."""
+    with TMA 16-byte gathers (1), LDG gathers (2) or TMA tile::gather4 (3): the same bits (world 2:
+    phase B with the remote warp)."""
     inst = kurgen.sbm([4000, 3000, 2500, 2600], np.array(
         [[0.97, 0.01, 0.002, 0.0], [0.01, 0.9, 0.0, 0.01], [0.002, 0.0, 0.98, 0.003], [0.0, 0.01, 0.003, 0.95]]),
         41, K=3.0, h=0.01)
     res = []
-    for mode in ("0", "1", "2"):
+    for mode in ("0", "1", "2", "3"):
         monkeypatch.setenv("KUR_REMOTE_MODE", mode)
         if world == 1:
             g = kur.graph_build(inst, remote_pass=True, tile_rows=512)

@@ -269,3 +269,28 @@ def test_adaptive_rk4_preserves_linear_invariant_and_potential_decreases():
         assert v <= v_prev + 1e-12
         v_prev, prev_t = v, tk
     assert np.max(np.abs(cur - th2)) <= 1e-12
+
+
+@pytest.mark.parametrize("K,expect_sync", [(1.0, False), (3.0, True), (5.0, True)])
+def test_paper_fig2_synchronisation_strength(K, expect_sync):
+    """P:361-375: M = 10^2, T = 200, omega_m = 1 + omega_0 (2m-M-1)/(M-1) with omega_0 = 2 and
+    theta_m(0) = 2 pi m/M, variable-step RK4: "the modulus of the complex order parameter
+    is close to one for K = 5".  The frequencies are uniform on [-1, 3] (half-width 2), so the mean-field
+    locking threshold is K_L = 4*2/pi ~ 2.55 (textbook, not from the paper): K = 3 and 5 lock, K = 1 does
+    not."""
+    M = 100
+    m = np.arange(1, M + 1)
+    A = np.ones((M, M), np.uint8) - np.eye(M, dtype=np.uint8)
+    inst = kurgen.from_dense(A, np.zeros(M, np.int64), kind="zeros", omega=1.0 + 2.0 * (2 * m - M - 1) / (M - 1),
+                             theta0=2 * np.pi * m / M, K=K)
+    _, t, h, rp, rej = oracle.integrate_adaptive(oracle.Graph(inst), inst.theta0, inst.omega, K, 200.0, 0.01,
+                                                 mode="op", atol=1e-8, rtol=1e-8)
+    assert t[-1] == 200.0
+    r_tail = rp[len(rp) // 2:, 0]
+    if expect_sync:
+        assert r_tail.min() >= (0.9 if K == 5.0 else 0.6), r_tail.min()
+        assert np.ptp(r_tail) <= 1e-3  # locked: r constant along the second half
+    else:
+        assert rp[-1, 0] <= 0.5
+    if K == 5.0:  # the paper's sentence
+        assert rp[-1, 0] >= 0.95
