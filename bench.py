@@ -358,6 +358,11 @@ def main():
                 "kernel_bytes_gbs": kernel_bytes / (stage_ms / 1e3) / 1e9,
                 "kernel_bytes_frac": kernel_bytes / (stage_ms / 1e3) / 1e9 / peak,
                 "traffic_gbs": None if traffic is None else traffic / (stage_ms / 1e3) / 1e9}
+    if int(info["n_idx"]) == 0:  # entry-free plan (complete graph): no index stream at all
+        roofline["note"] = ("entry-free plan: the SURVEY bytes are nominal -- the persistent trajectory kernel keeps "
+                            "theta_n, acc, z and omega on chip for the whole kur_step, so per stage it moves only "
+                            "its tile partials; it is bound by fp64 issue (sincos) and the per-stage grid "
+                            "synchronisation, see profiles/r02/cfg2_k_persist_*")
     # the bound k_stage actually meets: the L1/shared-memory data pipe: one 16-byte z
     # read per hot entry from the staged window; nominal 128 B/clk/SM (B300_MICROARCH smem crossbar),
     # of which tools/mb_lds.cu reaches 99 % with slot ids in registers
@@ -451,8 +456,10 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "rhs_calls": rhs_calls,
-            "gpu_launches": 1 + tm["prologue_n"] + tm["stage_n"] + tm["remote_n"]
-                            + (2 * (tm["prologue_n"] + tm["stage_n"]) if world > 1 else 0),
+            # k_set_ctrl + every timed launch (prologue, k_remote, k_stage -- phase A and B at world > 1 --
+            # or the one trajectory kernel) + k_unpack and k_finish per exchanged phase at world > 1
+            "gpu_launches": 1 + tm["launches"] + ((2 + int(info["peer_exchange"])) * (tm["prologue_n"] + tm["stage_n"])
+                                                  if world > 1 else 0),
             "clocks": clk.result(),
             "host": dict(_host_info(), gen_s=gen_s, build_s=build_s),
             "plan": {k: info[k] for k in ("n_idx_hot", "n_idx_remote", "n_slots_hot", "n_slots_remote",

@@ -97,7 +97,8 @@ struct kur_graph {
   bool small = false;                 // whole kur_step in one single-CTA launch
   bool persist = false;               // entry-free plan: whole RK4 kur_step in one cooperative launch
   double2* pbuf = nullptr;            // persist: [2][ntiles] tile partials
-  unsigned int* gbar = nullptr;       // persist: grid-barrier words
+  unsigned long long* gbar = nullptr; // persist: monotonic arrival counter
+  unsigned long long persist_q = 0;   // persist: publications so far
   int32_t* d_big = nullptr;           // communities of > 64 tiles
   size_t ev_used = 0;
   cudaError_t mark(cudaStream_t s) {  // records the next event of the pool on s
@@ -437,8 +438,8 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   // entry-free plans (world 1, beyond the single-CTA size): RK4 trajectories in one cooperative launch
   if (!g->small && persist_fits(dp)) {
     if ((e = cudaMalloc((void**)&g->pbuf, sizeof(double2) * 2 * (size_t)dp.ntiles)) != cudaSuccess ||
-        (e = cudaMalloc((void**)&g->gbar, 2 * sizeof(unsigned int))) != cudaSuccess ||
-        (e = cudaMemset(g->gbar, 0, 2 * sizeof(unsigned int))) != cudaSuccess)
+        (e = cudaMalloc((void**)&g->gbar, sizeof(unsigned long long))) != cudaSuccess ||
+        (e = cudaMemset(g->gbar, 0, sizeof(unsigned long long))) != cudaSuccess)
       return bail(e, "persistent trajectory buffers");
     g->persist = std::getenv("KUR_NO_PERSIST") == nullptr;  // (A/B switch)
   }
@@ -758,7 +759,8 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
     a.K = K;
     a.h = h;
     KUR_CUDA(g->mark(s));
-    KUR_CUDA(launch_persist_rk4(g->dp, a, g->pbuf, g->gbar, (long long)nsteps, s));
+    KUR_CUDA(launch_persist_rk4(g->dp, a, g->pbuf, g->gbar, (long long)nsteps, g->persist_q, s));
+    g->persist_q += (unsigned long long)(1 + 4 * nsteps);
     KUR_CUDA(g->mark(s));
     if (g->timing) g->ev_kind.push_back({1, (int)std::min<int64_t>(4 * nsteps, INT32_MAX)});
     if (host_out) KUR_CUDA(cudaMemcpyAsync(host_out, io[0].theta, sizeof(double) * (size_t)g->n_local,
@@ -1150,6 +1152,7 @@ kur_status kur_timing_read(kur_graph* g, double* out) {
   out[3] = (double)cnt[1];
   out[4] = ms[2];
   out[5] = (double)cnt[2];
+  out[6] = (double)g->ev_kind.size();
   g->ev_used = 0;
   g->ev_kind.clear();
   return KUR_OK;

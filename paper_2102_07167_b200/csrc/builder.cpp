@@ -114,13 +114,20 @@ void enumerate_row(const Src& S, const std::vector<int32_t>& D_ptr, const std::v
 // the two bounds drops; quarters are sorted by their bound and grouped 4 per
 // chunk.  (Config-5-like SBM: hot padding 13.7 % -> 6.2 %, with the 4-slot
 // half-group tail of plan.h.)
+//
+// Rows split into w = 2^lp pieces (row pieces, w <= 8) are packed as items of w adjacent, aligned
+// lanes: a quarter then holds 8 / w rows, an item's lane length is its longest piece (cnt), its
+// residue counts are the whole row's; `ord` entries are item ids and the returned lanes hold
+// item ids at the first lane of each item (the caller expands them to pieces).
 template <class CountFn>
 void plan_pools(const std::vector<int32_t>& ord, const std::vector<int32_t>& cnt,
-                std::vector<std::array<int32_t, 32>>& lanes, CountFn count) {
+                std::vector<std::array<int32_t, 32>>& lanes, CountFn count, int w = 1) {
   constexpr int POOL = 256, NQ = POOL / 8;
-  for (size_t p0 = 0; p0 < ord.size(); p0 += POOL) {
-    const int np = (int)std::min<size_t>(POOL, ord.size() - p0);
-    const int nq = (np + 7) / 8;
+  const int per_q = 8 / w;            // items per quarter
+  const int pool_items = NQ * per_q;  // items per pool (256 lanes)
+  for (size_t p0 = 0; p0 < ord.size(); p0 += (size_t)pool_items) {
+    const int np = (int)std::min<size_t>((size_t)pool_items, ord.size() - p0);
+    const int nq = (np + per_q - 1) / per_q;
     int cv[POOL][8];
     std::memset(cv, 0, sizeof(cv));
     for (int i = 0; i < np; ++i) count(ord[p0 + (size_t)i], cv[i]);
@@ -132,7 +139,7 @@ void plan_pools(const std::vector<int32_t>& ord, const std::vector<int32_t>& cnt
       int bq = -1;
       long bmx = 0, bss = 0;
       for (int q = 0; q < nq; ++q) {
-        if (qf[q] == 8) continue;
+        if (qf[q] == per_q) continue;
         long mx = std::max(qlen[q], cnt[(size_t)ord[p0 + (size_t)i]]), ss = 0;
         for (int r = 0; r < 8; ++r) {
           const long v = qt[q][r] + cv[i][r];
@@ -214,7 +221,7 @@ void plan_pools(const std::vector<int32_t>& ord, const std::vector<int32_t>& cnt
       a.fill(-1);
       for (int k = 0; k < 4 && c * 4 + k < nq; ++k) {
         const int q = qord[c * 4 + k];
-        for (int m = 0; m < qf[q]; ++m) a[(size_t)(k * 8 + m)] = qm[q][m];
+        for (int m = 0; m < qf[q]; ++m) a[(size_t)(k * 8 + m * w)] = qm[q][m];
       }
       lanes.push_back(a);
     }
@@ -685,6 +692,27 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
           const size_t nr = rows.size(), ne = k1 - k0;
           while (lp < 5 && nr * ((size_t)2 << lp) <= (size_t)NTHREADS && ne / (nr * ((size_t)2 << lp)) >= 16) ++lp;
         }
+        // hot parts with pieces of <= 8 lanes: pack whole rows (items of 2^lp aligned lanes) into
+        // residue-balanced quarters first, in the row-level numbering (ord / cnt / rb / rl by row)
+        std::vector<std::array<int32_t, 32>> lanes;
+        const bool pooled = hot && lp <= 3;
+        if (pooled) {
+          const int w = 1 << lp;
+          std::vector<int32_t> lane_len(cnt.size());
+          for (size_t i = 0; i < cnt.size(); ++i) lane_len[i] = (cnt[i] + w - 1) / w;  // longest piece
+          std::vector<int32_t> pos_of(cnt.size());
+          for (size_t p = 0; p < ord.size(); ++p) pos_of[(size_t)ord[p]] = (int32_t)p;  // row -> ord position
+          plan_pools(ord, lane_len, lanes, [&](int32_t ri, int* cv) {
+            for (int e = 0; e < cnt[(size_t)ri]; ++e) cv[(src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) & 7]++;
+          }, w);
+          if (lp > 0)  // expand items to pieces: the pieces of the row at ord position p are p*w .. p*w+w-1
+            for (auto& a : lanes)
+              for (int l = 0; l < 32; l += w)
+                if (a[(size_t)l] >= 0) {
+                  const int32_t p = pos_of[(size_t)a[(size_t)l]];
+                  for (int i = 0; i < w; ++i) a[(size_t)(l + i)] = p * w + i;
+                }
+        }
         if (lp > 0) {
           const int pcs = 1 << lp;
           std::vector<int32_t> vrb, vcnt, vrl;
@@ -706,13 +734,8 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
         auto slot_of = [&](int32_t ri, int e) -> uint32_t {
           return (uint32_t)((src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) - (uint64_t)window * WZ);
         };
-        // chunks (lane -> row); hot parts: residue-balanced quarter-warps from 128-row pools
-        std::vector<std::array<int32_t, 32>> lanes;
-        if (hot && lp == 0) {
-          plan_pools(ord, cnt, lanes, [&](int32_t ri, int* cv) {
-            for (int e = 0; e < cnt[(size_t)ri]; ++e) cv[slot_of(ri, e) & 7]++;
-          });
-        } else {
+        // chunks (lane -> row or piece); hot parts: residue-balanced quarter-warps (above)
+        if (!pooled) {
           for (size_t c0 = 0; c0 < ord.size(); c0 += 32) {
             std::array<int32_t, 32> a;
             for (int l = 0; l < 32; ++l) a[(size_t)l] = c0 + (size_t)l < ord.size() ? ord[c0 + (size_t)l] : -1;

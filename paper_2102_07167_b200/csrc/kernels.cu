@@ -1235,34 +1235,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_small_dense(const DevPlan dp, S
 // launch).  W_j = T_{c(j)} (P:557-561 with empty lists; P:240-255 for one community), so a stage
 // needs nothing but the block sums of the previous one: each CTA keeps its tile's z and omega in
 // shared memory and theta_n, acc in registers for the whole trajectory, publishes its tile partial
-// of z, and after ONE grid barrier per stage every CTA reduces all partials itself in finish_reduce's
-// exact summation shapes -- the same bits as the general path (k_prologue + k_stage<S1..S4>), without
-// a kernel boundary or a last-CTA tail per stage.
-__device__ __forceinline__ void grid_barrier(unsigned int* gbar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int gen = *(volatile unsigned int*)(gbar + 1);  // read before arriving
+// of z, and every CTA reduces all partials itself in finish_reduce's exact summation shapes -- the
+// same bits as the general path (k_prologue + k_stage<S1..S4>), without a kernel boundary or a
+// last-CTA tail per stage.  Grid synchronisation: a monotonic 64-bit arrival counter -- publication q
+// is complete when it reaches q * (number of CTAs); one atomic and one spinning thread per CTA (one
+// spinning thread per partial measured 16.8 against 10.3 us per stage: the acquire polls load the
+// L2).  Partials are double-buffered by the parity of q: a CTA can publish q + 2 (same half) only
+// after publication q + 1 completed, i.e. after every CTA finished reading publication q.
+__device__ __forceinline__ void publish_and_wait(double2* pbuf, unsigned long long* cnt, int nt, int lt,
+                                                 unsigned long long q, double x, double y) {
+  if (threadIdx.x == 0) {  // (block_sum2's result is in thread 0)
+    pbuf[(size_t)(q & 1ull) * nt + lt] = make_double2(x, y);
     __threadfence();
-    if (atomicAdd(gbar, 1u) == gridDim.x - 1) {
-      atomicExch(gbar, 0u);
-      __threadfence();
-      atomicAdd(gbar + 1, 1u);
-    } else {
-      unsigned int v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar + 1) : "memory");
-      } while (v == gen);
-    }
-    __threadfence();
+    atomicAdd(cnt, 1ull);
+    const unsigned long long target = q * (unsigned long long)nt;
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+    } while ((long long)(v - target) < 0);
   }
   __syncthreads();
 }
 
-// S_b of every community from tile partials src (finish_reduce's shapes: one thread per community
-// summing its tiles in order, or a fixed-shape block reduction for communities of > 64 tiles), into
-// shared S_sh; then T of community c and (r, psi) = (1/N) sum_b S_b.  Ends with a block barrier.
-__device__ __forceinline__ void local_reduce(const DevPlan& dp, const double2* src, double2* S_sh, double2* red,
-                                             int c_own, double2* sT, double* s_rpsi) {
+// S_b of every community from the tile partials of publication q (finish_reduce's shapes: one thread
+// per community summing its tiles in order, or a fixed-shape block reduction for communities of
+// > 64 tiles), into shared S_sh; then T of community c_own; (r, psi) = (1/N) sum_b S_b only if
+// want_rpsi.  Ends with a block barrier.
+__device__ __forceinline__ void local_reduce(const DevPlan& dp, const double2* pbuf, int nt, unsigned long long q,
+                                             double2* S_sh, double2* red, int c_own, double2* sT, double* s_rpsi,
+                                             bool want_rpsi) {
+  const double2* src = pbuf + (size_t)(q & 1ull) * nt;
   const int tid = threadIdx.x;
   constexpr int BIG = 64;
   for (int c = tid; c < dp.C; c += NTHREADS) {
@@ -1299,18 +1301,20 @@ __device__ __forceinline__ void local_reduce(const DevPlan& dp, const double2* s
     }
     *sT = make_double2(x, y);
   }
-  double x = 0.0, y = 0.0;  // r e^{i psi} = (1/N) sum_b S_b
-  for (int c = tid; c < dp.C; c += NTHREADS) {
-    const double2 v = S_sh[c];
-    x += v.x;
-    y += v.y;
-  }
-  block_sum2(x, y, red);
-  if (tid == 0) {
-    const double cm = x / (double)dp.n, sm = y / (double)dp.n;
-    const double r = sqrt(cm * cm + sm * sm);
-    s_rpsi[0] = r;
-    s_rpsi[1] = r == 0.0 ? 0.0 : atan2(sm, cm);
+  if (want_rpsi) {  // uniform branch
+    double x = 0.0, y = 0.0;  // r e^{i psi} = (1/N) sum_b S_b
+    for (int c = tid; c < dp.C; c += NTHREADS) {
+      const double2 v = S_sh[c];
+      x += v.x;
+      y += v.y;
+    }
+    block_sum2(x, y, red);
+    if (tid == 0) {
+      const double cm = x / (double)dp.n, sm = y / (double)dp.n;
+      const double r = sqrt(cm * cm + sm * sm);
+      s_rpsi[0] = r;
+      s_rpsi[1] = r == 0.0 ? 0.0 : atan2(sm, cm);
+    }
   }
   __syncthreads();
 }
@@ -1329,7 +1333,8 @@ __device__ __forceinline__ void record_rpsi(const DevPlan& dp, const double* rp,
 }
 
 __global__ void __launch_bounds__(NTHREADS, 2) k_persist_rk4(const DevPlan dp, const StageArgs a, double2* pbuf,
-                                                             unsigned int* gbar, long long nsteps) {
+                                                             unsigned long long* cnt, long long nsteps,
+                                                             unsigned long long q0) {
   constexpr int R = MAX_TILE_ROWS_NOPARTS / NTHREADS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* zc = reinterpret_cast<double*>(smem_raw);  // [rows_per_tile] z of the stage state
@@ -1342,7 +1347,12 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_persist_rk4(const DevPlan dp, c
   const int tid = threadIdx.x, lt = blockIdx.x;
   const TileDesc T = dp.tiles[lt];
   const int nt = gridDim.x;
+  const bool rec = lt == 0 && dp.ctrl->record_every > 0;  // CTA 0 keeps (r, psi) and the record
+  const int re = rec ? dp.ctrl->record_every : 0;
+  const double KN = a.KN, K = a.K, h = a.h;
+  const double* __restrict__ rs = dp.rowscale;
   double thn[R], acc[R];
+  unsigned long long q = q0;  // publication counter (the arrival counter is monotonic across launches)
   // prologue: z(theta_n), the tile partial, S_b, T, (r, psi) of theta_0 (recorded as n = 0)
   double x = 0.0, y = 0.0;
 #pragma unroll
@@ -1364,37 +1374,32 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_persist_rk4(const DevPlan dp, c
     y += s;
   }
   block_sum2(x, y, red);
-  if (tid == 0) pbuf[lt] = make_double2(x, y);
-  grid_barrier(gbar);
-  local_reduce(dp, pbuf, S_sh, red, T.comm, &sT, s_rpsi);
+  publish_and_wait(pbuf, cnt, nt, lt, ++q, x, y);
+  local_reduce(dp, pbuf, nt, q, S_sh, red, T.comm, &sT, s_rpsi, lt == 0);
   if (lt == 0 && tid == 0) record_rpsi(dp, s_rpsi, 0);
   bool bad = false;
-  int par = 1;  // partial buffer half of the next publication
   for (long long n = 0; n < nsteps; ++n) {
 #pragma unroll 1
     for (int st = 1; st <= 4; ++st) {
       const double2 Tc = sT;
       const double wx = Tc.x + 0.0, wy = Tc.y + 0.0;  // W_j = T_c + (empty lists)
+      const double hs = st == 4 ? h / 6.0 : (st == 3 ? h : h / 2.0);
       double px = 0.0, py = 0.0;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const int lr = tid + k * NTHREADS;
         if (lr >= T.nrows) break;
-        const int li = T.row0 + lr - dp.row_begin;
-        const double kn = dp.rowscale ? a.K * dp.rowscale[li] : a.KN;
+        const double kn = rs ? K * rs[T.row0 + lr - dp.row_begin] : KN;
         const double kk = rhs_k(om[lr], kn, zc[lr], zsn[lr], wx, wy);
         double ts;
         if (st == 1) {
           acc[k] = kk;
-          ts = __dadd_rn(thn[k], __dmul_rn(a.h / 2.0, kk));
-        } else if (st == 2) {
+          ts = __dadd_rn(thn[k], __dmul_rn(hs, kk));
+        } else if (st < 4) {
           acc[k] = __dadd_rn(acc[k], __dmul_rn(2.0, kk));
-          ts = __dadd_rn(thn[k], __dmul_rn(a.h / 2.0, kk));
-        } else if (st == 3) {
-          acc[k] = __dadd_rn(acc[k], __dmul_rn(2.0, kk));
-          ts = __dadd_rn(thn[k], __dmul_rn(a.h, kk));
+          ts = __dadd_rn(thn[k], __dmul_rn(hs, kk));
         } else {  // theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
-          ts = __dadd_rn(thn[k], __dmul_rn(a.h / 6.0, __dadd_rn(acc[k], kk)));
+          ts = __dadd_rn(thn[k], __dmul_rn(hs, __dadd_rn(acc[k], kk)));
           thn[k] = ts;
           bad |= !isfinite(ts);
         }
@@ -1406,12 +1411,11 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_persist_rk4(const DevPlan dp, c
         py += s;
       }
       block_sum2(px, py, red);
-      double2* dst = pbuf + (size_t)par * nt;
-      if (tid == 0) dst[lt] = make_double2(px, py);
-      grid_barrier(gbar);
-      local_reduce(dp, dst, S_sh, red, T.comm, &sT, s_rpsi);
-      if (st == 4 && lt == 0 && tid == 0) record_rpsi(dp, s_rpsi, n + 1);
-      par ^= 1;
+      publish_and_wait(pbuf, cnt, nt, lt, ++q, px, py);
+      // (r, psi) only where it is recorded, or of the final state (ctrl->rpsi)
+      const bool want = lt == 0 && st == 4 && ((re > 0 && (n + 1) % re == 0) || n + 1 == nsteps);
+      local_reduce(dp, pbuf, nt, q, S_sh, red, T.comm, &sT, s_rpsi, want);
+      if (want && tid == 0) record_rpsi(dp, s_rpsi, n + 1);
     }
   }
 #pragma unroll
@@ -1425,26 +1429,26 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_persist_rk4(const DevPlan dp, c
 
 // world > 1: z of the non-local rows from the exchanged stage phases (the same
 // sincos the owner evaluated -> bitwise identical), and every tile partial.
-__global__ void k_unpack(const DevPlan dp, const double* __restrict__ xrecv, double2* __restrict__ zout,
-                         unsigned int expect) {
-  if (dp.peer_x) {  // fused exchange: every rank's record of this stage has landed in xrecv
-    if (threadIdx.x == 0) {
-      unsigned int v;
-      uint64_t t0, t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      for (;;) {
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(dp.peer_flag[dp.rank]) : "memory");
-        if ((int)(v - expect) >= 0) break;
-        __nanosleep(64);
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 20000000000ull) {  // 20 s: a rank is gone; fail loudly instead of hanging
-          dp.ctrl->xtimeout = 1;
-          break;
-        }
-      }
+// Fused exchange: ONE thread waits until every rank's record of this stage has landed in xrecv
+// (arrival counter, acquire at system scope); k_unpack is stream-ordered after it, so its blocks
+// start on complete data instead of each spinning on the flag.
+__global__ void k_wait_peers(const DevPlan dp, unsigned int expect) {
+  unsigned int v;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(dp.peer_flag[dp.rank]) : "memory");
+    if ((int)(v - expect) >= 0) break;
+    __nanosleep(64);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) {  // 20 s: a rank is gone; fail loudly instead of hanging
+      dp.ctrl->xtimeout = 1;
+      break;
     }
-    __syncthreads();
   }
+}
+
+__global__ void k_unpack(const DevPlan dp, const double* __restrict__ xrecv, double2* __restrict__ zout) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < dp.n) {
     int r = 0;
@@ -1639,14 +1643,14 @@ bool persist_fits(const DevPlan& dp) {
   return (long long)nb * sms >= dp.ntiles;
 }
 
-cudaError_t launch_persist_rk4(const DevPlan& dp, const StageArgs& a, double2* pbuf, unsigned int* gbar,
-                               long long nsteps, cudaStream_t s) {
+cudaError_t launch_persist_rk4(const DevPlan& dp, const StageArgs& a, double2* pbuf, unsigned long long* cnt,
+                               long long nsteps, unsigned long long q0, cudaStream_t s) {
   const size_t smem = persist_smem_bytes(dp);
   cudaError_t e = cudaFuncSetAttribute(k_persist_rk4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   DevPlan d = dp;
   StageArgs aa = a;
-  void* args[] = {(void*)&d, (void*)&aa, (void*)&pbuf, (void*)&gbar, (void*)&nsteps};
+  void* args[] = {(void*)&d, (void*)&aa, (void*)&pbuf, (void*)&cnt, (void*)&nsteps, (void*)&q0};
   return cudaLaunchCooperativeKernel((const void*)k_persist_rk4, dim3((unsigned)dp.ntiles), dim3(NTHREADS), args,
                                      smem, s);
 }
@@ -1655,7 +1659,8 @@ cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout,
                           cudaStream_t s) {
   const int64_t m = std::max<int64_t>(dp.n, (int64_t)1);
   const int bs = 256;
-  k_unpack<<<(unsigned)((m + bs - 1) / bs), bs, 0, s>>>(dp, xrecv, zout, expect);
+  if (dp.peer_x) k_wait_peers<<<1, 1, 0, s>>>(dp, expect);
+  k_unpack<<<(unsigned)((m + bs - 1) / bs), bs, 0, s>>>(dp, xrecv, zout);
   return cudaGetLastError();
 }
 

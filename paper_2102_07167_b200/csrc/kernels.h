@@ -130,10 +130,11 @@ cudaError_t launch_small(const DevPlan& dp, const StageArgs& a, double2* zA, dou
                          long long nsteps, cudaStream_t s);
 // expect: with the fused peer-store exchange, the arrival count that completes this exchange
 // entry-free plans, world 1: the whole RK4 trajectory in one cooperative launch (one CTA per tile,
-// all co-resident; pbuf [2 * ntiles] partial halves, gbar [2] zeroed grid-barrier words)
+// all co-resident; pbuf [2 * ntiles] partial halves, cnt a zeroed, monotonic 64-bit arrival counter:
+// q0 = publications of the previous launches, each launch publishes 1 + 4 nsteps)
 bool persist_fits(const DevPlan& dp);
-cudaError_t launch_persist_rk4(const DevPlan& dp, const StageArgs& a, double2* pbuf, unsigned int* gbar,
-                               long long nsteps, cudaStream_t s);
+cudaError_t launch_persist_rk4(const DevPlan& dp, const StageArgs& a, double2* pbuf, unsigned long long* cnt,
+                               long long nsteps, unsigned long long q0, cudaStream_t s);
 cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, unsigned int expect,
                           cudaStream_t s);
 cudaError_t launch_finish(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
