@@ -189,7 +189,7 @@ def cpu_protocol(inst, cfg):
         rec = {"mode": mode, "rows": nrow, "rhs_per_s_all_cores": r_all, "rhs_per_s_1_core": r_one,
                "steps_per_s_all_cores": r_all / 4.0, "steps_per_s_1_core": r_one / 4.0, "cores": cores,
                "seconds": dt_all + dt_one}
-        if extra == "per_row":
+        if isinstance(extra, str) and extra == "per_row":
             rec = {"mode": mode, "rows": nrow, "unit": "rows/s (not extrapolated)",
                    "rows_per_s_all_cores": r_all * inst.n, "rows_per_s_1_core": r_one * inst.n, "cores": cores,
                    "seconds": dt_all + dt_one}

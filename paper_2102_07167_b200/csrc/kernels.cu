@@ -1245,14 +1245,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_small_dense(const DevPlan dp, S
 __device__ __forceinline__ void publish_and_wait(double2* pbuf, unsigned long long* cnt, int nt, int lt,
                                                  unsigned long long q, double x, double y) {
   if (threadIdx.x == 0) {  // (block_sum2's result is in thread 0)
-    pbuf[(size_t)(q & 1ull) * nt + lt] = make_double2(x, y);
-    __threadfence();
-    atomicAdd(cnt, 1ull);
+    __stcg(pbuf + (size_t)(q & 1ull) * nt + lt, make_double2(x, y));
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");  // orders the partial before
     const unsigned long long target = q * (unsigned long long)nt;
     unsigned long long v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+    do {  // relaxed polls (an acquire poll, like a sequentially consistent fence, invalidates L1 each time)
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
     } while ((long long)(v - target) < 0);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the partials are then read through L2 (ld.global.cg)
   }
   __syncthreads();
 }
