@@ -53,6 +53,10 @@ def main():
             (hot if p < nhot[t] else rem)[t] += pe - we  # the inline remote part runs last
             imb[t] += pe - wf.mean()
     fin = t26 - t25
+    q = np.percentile(tot, [50, 90, 99, 100])
+    print(f"tile cycles p50 {q[0]:.0f} p90 {q[1]:.0f} p99 {q[2]:.0f} max {q[3]:.0f}; "
+          f"remote part p50 {np.percentile(rem, 50):.0f} max {rem.max():.0f}; hot p50 {np.percentile(hot, 50):.0f} "
+          f"max {hot.max():.0f}")
     print(f"cfg{args.config}: {nt} tiles, rows/tile {g.info['rows_per_tile']}, parts/tile {nparts.mean():.2f} "
           f"(hot {nhot.mean():.2f})")
     print(f"mean cycles per tile: total {tot.mean():.0f}")
