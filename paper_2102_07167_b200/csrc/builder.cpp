@@ -976,9 +976,10 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   // launch order: decreasing work (longest-processing-time first)
   P.tile_order.resize((size_t)nt);
   std::iota(P.tile_order.begin(), P.tile_order.end(), 0);
-  std::stable_sort(P.tile_order.begin(), P.tile_order.end(), [&](int32_t x, int32_t y) {
-    return twork[(size_t)(P.tile_begin + x)] > twork[(size_t)(P.tile_begin + y)];
-  });
+  if (!std::getenv("KUR_TILE_ORDER_PLAIN"))  // (A/B switch: tiles in community order)
+    std::stable_sort(P.tile_order.begin(), P.tile_order.end(), [&](int32_t x, int32_t y) {
+      return twork[(size_t)(P.tile_begin + x)] > twork[(size_t)(P.tile_begin + y)];
+    });
   return KUR_OK;
 }
 

@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <utility>
 
 #include "kernels.h"
 
@@ -103,19 +104,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 // One thread: TMA bulk copy of `bytes` from global to shared memory, completion on `bar`.
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                            int win_policy = 0) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
-  // evict-first: a window is dead once its community's tiles have staged it; z_out (stored
-  // by this kernel, gathered by the next k_remote) keeps the L2
+  // evict-first (0): a window is dead once its community's tiles have staged it; z_out (stored
+  // by this kernel, gathered by the next k_remote) keeps the L2.  1: evict-normal, 2: evict-last
   uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  if (win_policy == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else if (win_policy == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
       : "memory");
+}
+
+// Programmatic dependent launch (world 1 stage sequence): the next kernel of the stream is launched
+// while this one runs; its CTAs wait here until the previous grid has completed and flushed, so the
+// launch latency and the previous grid's tail overlap.  No-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 __device__ __forceinline__ void warp_sum2(double& x, double& y) {
@@ -590,6 +602,30 @@ __device__ __forceinline__ void peer_arrive(const DevPlan& dp) {
   }
 }
 
+// Sequential sum (x, y) = 0 + v[t0] + v[t0+1] + ... + v[t1-1] of tile partials in global memory,
+// with the loads issued 8 at a time (the additions stay in order: the same bits as a plain loop,
+// without one L2 round trip per term on the critical path of the last CTA).
+__device__ __forceinline__ double2 seq_sum_partials(const double2* v, int t0, int t1) {
+  double x = 0.0, y = 0.0;
+  int t = t0;
+  for (; t + 8 <= t1; t += 8) {
+    double2 b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b[i] = __ldcg(v + t + i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      x += b[i].x;
+      y += b[i].y;
+    }
+  }
+  for (; t < t1; ++t) {
+    const double2 b = __ldcg(v + t);
+    x += b.x;
+    y += b.y;
+  }
+  return make_double2(x, y);
+}
+
 // Executed by every thread of the LAST CTA of a grid: S_b from the per-tile
 // partials, T_a, the order parameter and its recording.
 __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
@@ -619,13 +655,7 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
   for (int c = tid; c < dp.C; c += NTHREADS) {
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
     if (t1 - t0 > BIG) continue;
-    double x = 0.0, y = 0.0;
-    for (int t = t0; t < t1; ++t) {
-      const double2 v = __ldcg(dp.partial + t);
-      x += v.x;
-      y += v.y;
-    }
-    dp.S[c] = make_double2(x, y);
+    dp.S[c] = seq_sum_partials(dp.partial, t0, t1);
   }
   for (int i = 0; i < dp.n_big; ++i) {  // communities of > BIG tiles (uniform): fixed-shape block reduction
     const int c = dp.big_comm[i];
@@ -816,7 +846,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   if (pbeg < T.nhot && pbeg < pend) {
     loaded = dp.parts[T.part0 + pbeg].window;
     pending = true;
-    if (tid == 0) tma_load_1d(zs, a.zin + (size_t)loaded * WZ, WZ * sizeof(double2), bar);
+    if (tid == 0) tma_load_1d(zs, a.zin + (size_t)loaded * WZ, WZ * sizeof(double2), bar, dp.win_policy);
   }
   for (int pi = pbeg; pi < pend; ++pi) {
     const int p = T.part0 + pi;
@@ -824,7 +854,8 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     const bool hot = P.window >= 0;
     if (!SMALL && pi < 8) PROF_T(1 + 3 * pi);
     if (hot && (P.window != loaded || pending)) {  // all reads of the previous window ended at the last barrier
-      if (P.window != loaded && tid == 0) tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), bar);
+      if (P.window != loaded && tid == 0)
+        tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), bar, dp.win_policy);
       mbar_wait(bar, phase);
       phase ^= 1u;
       loaded = P.window;
@@ -932,6 +963,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
 
 __global__ void __launch_bounds__(NTHREADS) k_prologue(const DevPlan dp, const StageArgs a) {
   __shared__ double2 red[NWARPS];
+  pdl_wait_and_release();
   const int lt = dp.order[blockIdx.x];
   const TileDesc T = dp.tiles[lt];
   double x, y;
@@ -955,6 +987,7 @@ __global__ void __launch_bounds__(KREM_THREADS, KREM_CTAS_PER_SM) k_remote(const
   // index units are requested before the current chunk's gathers (and its list entry /
   // descriptor two and one chunks ahead), so a warp never waits on an index load between
   // chunks; only the drain of the current gathers before its row sums remains.
+  pdl_wait_and_release();
   const int lane = threadIdx.x & 31;
   const int nw = (int)gridDim.x * (KREM_THREADS / 32);
   int w = (int)blockIdx.x * (KREM_THREADS / 32) + (threadIdx.x >> 5);
@@ -1026,6 +1059,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __shared__ __align__(8) uint64_t rbar[RING_SLOTS];
   __shared__ int s_nonfinite;
   const int tid = threadIdx.x;
+  pdl_wait_and_release();
   // implicit midpoint: iterations after convergence are no-ops (uniform: every CTA reads the same flag)
   // (phase A never skips: it may run before the finish that sets or clears the flag, and
   // phase B, which does check it, then reads Wh)
@@ -1270,13 +1304,7 @@ __device__ __forceinline__ void local_reduce(const DevPlan& dp, const double2* p
   for (int c = tid; c < dp.C; c += NTHREADS) {
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
     if (t1 - t0 > BIG) continue;
-    double x = 0.0, y = 0.0;
-    for (int t = t0; t < t1; ++t) {
-      const double2 v = __ldcg(src + t);
-      x += v.x;
-      y += v.y;
-    }
-    S_sh[c] = make_double2(x, y);
+    S_sh[c] = seq_sum_partials(src, t0, t1);
   }
   for (int i = 0; i < dp.n_big; ++i) {
     const int c = dp.big_comm[i];
@@ -1336,7 +1364,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_persist_rk4(const DevPlan dp, c
                                                              unsigned long long* cnt, long long nsteps,
                                                              unsigned long long q0) {
   constexpr int R = MAX_TILE_ROWS_NOPARTS / NTHREADS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   double* zc = reinterpret_cast<double*>(smem_raw);  // [rows_per_tile] z of the stage state
   double* zsn = zc + dp.rows_per_tile;
   double* om = zsn + dp.rows_per_tile;                // [rows_per_tile] omega
@@ -1511,6 +1539,24 @@ __global__ void k_permute(const int32_t* __restrict__ perm, int64_t n, const dou
   else out[perm[i]] = in[i];
 }
 
+// Launch with the programmatic-stream-serialization attribute (PDL) when dp.pdl (world 1, the
+// kernels call pdl_wait_and_release first), else a plain launch.
+template <class... P, class... A>
+cudaError_t launch_maybe_pdl(bool pdl, void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
 template <int MODE, bool RW>
 cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
   static std::atomic<uint64_t> attr_set{0};  // one bit per device (the attribute is per device context)
@@ -1531,8 +1577,7 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
   CUtensorMap tm;  // remote_warp 3: the tensor map of the stage's input z (zA or zB)
   if (dp.tmaps) tm = dp.tmaps[a.zin == dp.zbuf[0] ? 0 : 1];
   else memset(&tm, 0, sizeof(tm));
-  k_stage<MODE, RW><<<dp.ntiles, NTHREADS, dyn, s>>>(dp, a, tm);
-  return cudaGetLastError();
+  return launch_maybe_pdl(dp.pdl != 0, k_stage<MODE, RW>, dim3(dp.ntiles), dim3(NTHREADS), dyn, s, dp, a, tm);
 }
 
 template <int MODE>
@@ -1563,8 +1608,8 @@ cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s)
     dev_cached = dev;
   }
   const long long need = (dp.n_rchunks + wpb - 1) / wpb, full = (long long)KREM_CTAS_PER_SM * sms;
-  k_remote<<<(unsigned)(need < full ? need : full), KREM_THREADS, 0, s>>>(dp, zin);
-  return cudaGetLastError();
+  return launch_maybe_pdl(dp.pdl != 0, k_remote, dim3((unsigned)(need < full ? need : full)), dim3(KREM_THREADS), 0, s,
+                          dp, zin);
 }
 
 size_t stage_smem_bytes(int rows_per_tile) { return sizeof(double2) * (size_t)(WZ + 8 + rows_per_tile); }
@@ -1574,8 +1619,7 @@ cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t 
     if (dp.peer_x && a.xsend) k_arrive<<<1, 1, 0, s>>>(dp);
     return cudaGetLastError();
   }
-  k_prologue<<<dp.ntiles, NTHREADS, 0, s>>>(dp, a);
-  return cudaGetLastError();
+  return launch_maybe_pdl(dp.pdl != 0, k_prologue, dim3(dp.ntiles), dim3(NTHREADS), 0, s, dp, a);
 }
 
 cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
