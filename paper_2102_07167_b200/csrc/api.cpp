@@ -404,8 +404,6 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   // (profiles/r02/notes/pdl_ab.log): no gain on configs 3/4, config 5 4.41 -> 5.17 ms per RK4 step
   // (the early-resident k_remote / k_stage CTAs of the next stage only wait), so off by default.
   dp.pdl = (world == 1 && std::getenv("KUR_PDL") != nullptr) ? 1 : 0;
-  dp.win_policy = 0;
-  if (const char* wp = std::getenv("KUR_WIN_POLICY")) dp.win_policy = (wp[0] == '1') ? 1 : (wp[0] == '2') ? 2 : 0;
   dp.Wr = g->Wr;
   dp.peer_x = g->peer_on ? g->d_peer_x : nullptr;
   dp.peer_flag = g->d_peer_flag;

@@ -52,9 +52,18 @@ constexpr int PROF_STRIDE = 192;  // [0] start, [1+3p..] window wait begin/end +
   do { if (g_prof && threadIdx.x == 0) g_prof[(size_t)blockIdx.x * PROF_STRIDE + (i)] = clock64(); } while (0)
 #define PROF_W(p, w) \
   do { if (g_prof && (threadIdx.x & 31) == 0 && (p) < 8) g_prof[(size_t)blockIdx.x * PROF_STRIDE + 32 + 16 * (p) + (w)] = clock64(); } while (0)
+// global-timer stamps (ns, comparable across SMs): [160] CTA start, [161] tile done, [162] last CTA: finish done
+__device__ __forceinline__ unsigned long long prof_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROF_G(i) \
+  do { if (g_prof && threadIdx.x == 0) g_prof[(size_t)blockIdx.x * PROF_STRIDE + (i)] = prof_gtime(); } while (0)
 #else
 #define PROF_T(i) do {} while (0)
 #define PROF_W(p, w) do {} while (0)
+#define PROF_G(i) do {} while (0)
 #endif
 namespace {
 
@@ -104,17 +113,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 // One thread: TMA bulk copy of `bytes` from global to shared memory, completion on `bar`.
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                            int win_policy = 0) {
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
-  // evict-first (0): a window is dead once its community's tiles have staged it; z_out (stored
-  // by this kernel, gathered by the next k_remote) keeps the L2.  1: evict-normal, 2: evict-last
+  // evict-normal: the tiles of one community run together (the builder's launch order) and re-read
+  // its windows from L2 (config 5: k_stage DRAM reads 3.31 -> 2.90 GB per launch against evict-first,
+  // profiles/r02/notes/window_policy_ab.log).  A compile-time choice: a runtime switch between
+  // policies here cost k_stage 2 % (profiles/r02/notes/window_policy_branch_cost.log).
   uint64_t pol;
-  if (win_policy == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  else if (win_policy == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           smem_addr(dst)),
@@ -628,8 +636,11 @@ __device__ __forceinline__ double2 seq_sum_partials(const double2* v, int t0, in
 
 // Executed by every thread of the LAST CTA of a grid: S_b from the per-tile
 // partials, T_a, the order parameter and its recording.
-__device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
+// S_sh: shared scratch of >= C entries for the block sums (k_stage's free window buffer), or NULL:
+// then dp.S in global memory (one more L2 round trip for T_a and for (r, psi) each).
+__device__ void finish_reduce(const DevPlan& dp, const StageArgs& a, double2* S_sh = nullptr) {
   __shared__ double2 fred[NWARPS];
+  double2* const Sd = S_sh ? S_sh : dp.S;
   const int tid = threadIdx.x;
   constexpr int BIG = 64;  // communities with more tiles are reduced by the whole CTA
   if (a.v_out) {  // kur_potential: V = sum of the tile partials in tile order (fixed shape)
@@ -655,7 +666,7 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
   for (int c = tid; c < dp.C; c += NTHREADS) {
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
     if (t1 - t0 > BIG) continue;
-    dp.S[c] = seq_sum_partials(dp.partial, t0, t1);
+    Sd[c] = seq_sum_partials(dp.partial, t0, t1);
   }
   for (int i = 0; i < dp.n_big; ++i) {  // communities of > BIG tiles (uniform): fixed-shape block reduction
     const int c = dp.big_comm[i];
@@ -667,21 +678,22 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
       y += v.y;
     }
     block_sum2(x, y, fred);
-    if (tid == 0) dp.S[c] = make_double2(x, y);
+    if (tid == 0) Sd[c] = make_double2(x, y);
     __syncthreads();
   }
   __threadfence_block();
   __syncthreads();
+  auto ldS = [&](int c) { return S_sh ? S_sh[c] : __ldcg(dp.S + c); };
   for (int c = tid; c < dp.C; c += NTHREADS) {  // T_a = sum over dense column communities
     double x = 0.0, y = 0.0;
     for (int i = dp.D_ptr[c]; i < dp.D_ptr[c + 1]; ++i) {
-      const double2 v = __ldcg(dp.S + dp.D_idx[i]);
+      const double2 v = ldS(dp.D_idx[i]);
       x += v.x;
       y += v.y;
     }
     a.Tout[c] = make_double2(x, y);
     if (a.op_local) {  // localised order parameters S_b / n_b
-      const double2 v = __ldcg(dp.S + c);
+      const double2 v = ldS(c);
       const double nb = (double)dp.comm_size[c];
       const double cx = nb > 0 ? v.x / nb : 0.0, cy = nb > 0 ? v.y / nb : 0.0;
       const double r = sqrt(cx * cx + cy * cy);
@@ -692,7 +704,7 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
   {  // r e^{i psi} = (1/N) sum_b S_b, fixed-shape block reduction
     double x = 0.0, y = 0.0;
     for (int c = tid; c < dp.C; c += NTHREADS) {
-      const double2 v = __ldcg(dp.S + c);
+      const double2 v = ldS(c);
       x += v.x;
       y += v.y;
     }
@@ -727,7 +739,8 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a) {
 // Writes the tile partial, then lets the last CTA of the grid finish.
 // dmax: this thread's max |fixed-point update| (implicit midpoint iterations, else 0).
 __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const StageArgs& a, int lt,
-                                                        double x, double y, double2* red, double dmax = 0.0) {
+                                                        double x, double y, double2* red, double dmax = 0.0,
+                                                        double2* S_sh = nullptr) {
   __shared__ bool s_last;
   if (a.fp_check) {
     dmax = block_max(dmax, reinterpret_cast<double*>(red));
@@ -752,8 +765,9 @@ __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  finish_reduce(dp, a);
+  finish_reduce(dp, a, S_sh);
   if (threadIdx.x == 0) dp.ctrl->ticket = 0;
+  PROF_G(162);
 }
 
 // a1 for one tile: z = e^{i theta} of its rows; returns this thread's partial sums.
@@ -846,7 +860,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   if (pbeg < T.nhot && pbeg < pend) {
     loaded = dp.parts[T.part0 + pbeg].window;
     pending = true;
-    if (tid == 0) tma_load_1d(zs, a.zin + (size_t)loaded * WZ, WZ * sizeof(double2), bar, dp.win_policy);
+    if (tid == 0) tma_load_1d(zs, a.zin + (size_t)loaded * WZ, WZ * sizeof(double2), bar);
   }
   for (int pi = pbeg; pi < pend; ++pi) {
     const int p = T.part0 + pi;
@@ -854,8 +868,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     const bool hot = P.window >= 0;
     if (!SMALL && pi < 8) PROF_T(1 + 3 * pi);
     if (hot && (P.window != loaded || pending)) {  // all reads of the previous window ended at the last barrier
-      if (P.window != loaded && tid == 0)
-        tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), bar, dp.win_policy);
+      if (P.window != loaded && tid == 0) tma_load_1d(zs, a.zin + (size_t)P.window * WZ, WZ * sizeof(double2), bar);
       mbar_wait(bar, phase);
       phase ^= 1u;
       loaded = P.window;
@@ -1060,6 +1073,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __shared__ int s_nonfinite;
   const int tid = threadIdx.x;
   pdl_wait_and_release();
+  PROF_G(160);
   // implicit midpoint: iterations after convergence are no-ops (uniform: every CTA reads the same flag)
   // (phase A never skips: it may run before the finish that sets or clears the flag, and
   // phase B, which does check it, then reads Wh)
@@ -1093,7 +1107,9 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __syncthreads();
   if (FINAL && tid == 0 && s_nonfinite) dp.ctrl->nonfinite = 1;
   PROF_T(26);
-  tile_partial_and_finish(dp, a, lt, px, py, red, dmax);
+  PROF_G(161);
+  // the window buffer is free now: the last CTA keeps the block sums in it (WZ >= C)
+  tile_partial_and_finish(dp, a, lt, px, py, red, dmax, (dp.has_parts && dp.C <= WZ) ? zs : nullptr);
   if (dp.peer_x && a.xsend) peer_arrive(dp);
 }
 

@@ -33,7 +33,6 @@ struct DevPlan {
   int32_t world;
   int32_t has_parts;          // any tile has stored entries (else no shared memory is needed)
   int32_t pdl;                // world 1: k_prologue / k_remote / k_stage launched as programmatic dependents
-  int32_t win_policy;         // L2 policy of the window TMA loads: 0 evict-first, 1 normal, 2 evict-last
   int32_t has_remote;         // any tile has remote parts summed out of line into Wr (see remote_warp)
   int32_t remote_warp;        // has_remote: 0 = the k_remote pass before each k_stage; inside k_stage, one
                               // warp of each tile sums its remote part while the others gather the hot

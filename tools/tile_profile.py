@@ -53,6 +53,12 @@ def main():
             (hot if p < nhot[t] else rem)[t] += pe - we  # the inline remote part runs last
             imb[t] += pe - wf.mean()
     fin = t26 - t25
+    g0, g1, g2 = P[:, 160], P[:, 161], P[:, 162]
+    t_first = g0.min()
+    fin_end = g2[g2 > 0].max() if np.any(g2 > 0) else float("nan")
+    print(f"global timeline (us from the first CTA start): last CTA start {(g0.max() - t_first) / 1e3:.2f}, "
+          f"median tile done {(np.median(g1) - t_first) / 1e3:.2f}, last tile done {(g1.max() - t_first) / 1e3:.2f}, "
+          f"finish done {(fin_end - t_first) / 1e3:.2f}")
     q = np.percentile(tot, [50, 90, 99, 100])
     print(f"tile cycles p50 {q[0]:.0f} p90 {q[1]:.0f} p99 {q[2]:.0f} max {q[3]:.0f}; "
           f"remote part p50 {np.percentile(rem, 50):.0f} max {rem.max():.0f}; hot p50 {np.percentile(hot, 50):.0f} "
