@@ -379,6 +379,15 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
     const char* rm = std::getenv("KUR_REMOTE_MODE");
     if (rm && (rm[0] == '1' || rm[0] == '2' || rm[0] == '3')) dp.remote_warp = rm[0] - '0';
   }
+  // inline remote parts that are a large share of the tile's LSU work (one L1 wavefront per random
+  // gather against 1/8 per staged hot entry; config 3: 4.3 M remote slots against 14.3 M hot ones)
+  // run concurrently with the hot windows on half the warps; small tiles only (shared Wc)
+  dp.cr_hot_warps = 0;
+  if (!dp.has_remote && P.n_slots_remote > 0 && P.rows_per_tile <= 512 &&
+      2 * P.n_slots_remote * 8 >= P.n_slots_hot)
+    dp.cr_hot_warps = NWARPS / 2;
+  if (const char* cr = std::getenv("KUR_CONC_REMOTE")) dp.cr_hot_warps = std::atoi(cr);  // (A/B: 0 off, k hot warps)
+  if (dp.cr_hot_warps < 0 || dp.cr_hot_warps >= NWARPS || P.rows_per_tile > MAX_TILE_ROWS) dp.cr_hot_warps = 0;
   dp.tmaps = nullptr;
   dp.zbuf[0] = g->zA;
   dp.zbuf[1] = g->zB;

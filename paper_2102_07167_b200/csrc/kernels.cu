@@ -807,7 +807,7 @@ __device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs
 // zs: [WZ + 8] window + zero sentinels, Ws: [rows_per_tile] row sums (both
 // unused when the plan has no parts).  Returns the thread's partial sums of
 // the next stage's z in (px, py) and whether a phase became non-finite.
-template <int MODE, bool SMALL, bool RW = false>
+template <int MODE, bool SMALL, bool RW = false, bool CR = false>
 __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a, const TileDesc& T, double2* zs,
                                            double2* Ws, uint64_t* bar, uint32_t& phase, double& px, double& py,
                                            double& dmax, double2* ring = nullptr, uint64_t* rbar = nullptr,
@@ -821,9 +821,17 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   // world > 1: phase A sums the own-community hot parts (local z only) into Wh while the
   // previous stage's exchange is in flight; phase B continues from Wh (exact copy)
   const bool from_wh = !SMALL && a.phase == PHASE_B && T.nloc > 0;
+  // concurrent inline remote part (compile-time variant CR, plans whose inline remote part is a large
+  // share of the LSU work, e.g. config 3): warps [cr_hot_warps, NWARPS) sum the tile's remote part
+  // into Wc (shared) while the others gather the hot windows; the finalize adds Wc once per row --
+  // the k_remote pass's arithmetic (Ws + (0 + remote sum)), so every mode gives the same bits
+  const bool cr = CR && !SMALL && !split && T.nparts > T.nhot && a.phase != PHASE_A;
+  double2* Wc = Ws + dp.rows_per_tile;
   if (parts) {
-    for (int r = tid; r < T.nrows; r += NTHREADS)
+    for (int r = tid; r < T.nrows; r += NTHREADS) {
       Ws[r] = from_wh ? __ldcg(a.Wh + (T.row0 - dp.row_begin) + r) : make_double2(0.0, 0.0);
+      if (cr) Wc[r] = make_double2(0.0, 0.0);
+    }
     __syncthreads();
   }
   // ---- parts: hot ones gather from the staged window, remote ones from global memory
@@ -855,14 +863,20 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     else if (dp.remote_warp == 1) remote_warp_tma(dp, T, a.zin, ring, rbar, pol, lane);
     else remote_warp_ldg(dp, T, a.zin, pol, lane);
     __syncthreads();  // joins the hot warps below (Wr complete, Ws complete)
+  } else if (cr && warp >= dp.cr_hot_warps) {
+    run_part<false, true>(dp, dp.parts[T.part0 + T.nhot], false, zs, a.zin, Wc, pol, warp - dp.cr_hot_warps, lane,
+                          NWARPS - dp.cr_hot_warps);
+    __syncthreads();  // joins the hot warps below
   } else {
-  const uint32_t nhw = rw ? NWARPS - 1 : NWARPS;
-  if (pbeg < T.nhot && pbeg < pend) {
+  const uint32_t nhw = rw ? NWARPS - 1 : (cr ? dp.cr_hot_warps : NWARPS);
+  const bool named = rw || cr;  // the hot group synchronises on named barrier 1
+  const int pend_h = cr ? min(pend, T.nhot) : pend;
+  if (pbeg < T.nhot && pbeg < pend_h) {
     loaded = dp.parts[T.part0 + pbeg].window;
     pending = true;
     if (tid == 0) tma_load_1d(zs, a.zin + (size_t)loaded * WZ, WZ * sizeof(double2), bar);
   }
-  for (int pi = pbeg; pi < pend; ++pi) {
+  for (int pi = pbeg; pi < pend_h; ++pi) {
     const int p = T.part0 + pi;
     const PartDesc P = dp.parts[p];
     const bool hot = P.window >= 0;
@@ -877,7 +891,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     if (!SMALL && pi < 8) PROF_T(2 + 3 * pi);
     // large tiles: warm L2 with the next hot window while this part is gathered, so its TMA
     // copy hits L2 (cfg5 1.190 -> 1.183 ms; small tiles lose slightly, cfg4 0.321 -> 0.323)
-    if (dp.rows_per_tile >= MAX_TILE_ROWS && tid == 0 && pi + 1 < pend && pi + 1 < T.nhot) {
+    if (dp.rows_per_tile >= MAX_TILE_ROWS && tid == 0 && pi + 1 < pend_h && pi + 1 < T.nhot) {
       const int wn = dp.parts[T.part0 + pi + 1].window;
       if (wn != loaded)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.zin + (size_t)wn * WZ),
@@ -886,11 +900,11 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     }
     run_part<SMALL, !SMALL>(dp, P, hot, zs, a.zin, Ws, pol, warp, lane, nhw);
     if (!SMALL) PROF_W(pi, warp);
-    if (rw) asm volatile("bar.sync 1, %0;" ::"r"(nhw * 32) : "memory");
+    if (named) asm volatile("bar.sync 1, %0;" ::"r"(nhw * 32) : "memory");
     else __syncthreads();
     if (!SMALL && pi < 8) PROF_T(3 + 3 * pi);
   }
-  if (rw) __syncthreads();  // joins the remote warp
+  if (named) __syncthreads();  // joins the remote warp(s)
   }
   if (!SMALL) PROF_T(25);
   if (!SMALL && a.phase == PHASE_A) {  // hand the own-community sums to phase B
@@ -911,6 +925,11 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     double2 w = parts ? Ws[lr] : make_double2(0.0, 0.0);
     if (addr) {
       const double2 r = rw ? __ldcg(dp.Wr + li) : __ldcs(dp.Wr + li);
+      w.x += r.x;
+      w.y += r.y;
+    }
+    if (cr) {
+      const double2 r = Wc[lr];
       w.x += r.x;
       w.y += r.y;
     }
@@ -1060,7 +1079,7 @@ __global__ void __launch_bounds__(KREM_THREADS, KREM_CTAS_PER_SM) k_remote(const
   }
 }
 
-template <int MODE, bool RW>
+template <int MODE, bool RW, bool CR>
 __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const StageArgs a,
                                                        const __grid_constant__ CUtensorMap tmz) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1100,7 +1119,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __syncthreads();
   uint32_t phase = 0;
   double px, py, dmax;
-  const bool bad = stage_rows<MODE, false, RW>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax, ring, rbar, &tmz);
+  const bool bad = stage_rows<MODE, false, RW, CR>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax, ring, rbar, &tmz);
   if (MODE == MODE_RHS || a.phase == PHASE_A) return;
   constexpr bool FINAL = MODE == MODE_S4 || MODE == MODE_E1 || MODE == MODE_H2;
   if (FINAL && bad) s_nonfinite = 1;
@@ -1573,14 +1592,15 @@ cudaError_t launch_maybe_pdl(bool pdl, void (*k)(P...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
 }
 
-template <int MODE, bool RW>
+template <int MODE, bool RW, bool CR>
 cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
   static std::atomic<uint64_t> attr_set{0};  // one bit per device (the attribute is per device context)
-  const size_t smem = stage_smem_bytes(MAX_TILE_ROWS) + (RW ? RING_BYTES : 0);
+  const size_t smem = stage_smem_bytes(MAX_TILE_ROWS) + (RW ? RING_BYTES : 0) +
+                      (CR ? sizeof(double2) * (size_t)MAX_TILE_ROWS : 0);
   int dev = 0;
   cudaGetDevice(&dev);
   if (!((attr_set.load() >> (dev & 63)) & 1)) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage<MODE, RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_stage<MODE, RW, CR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(1ull << (dev & 63));
   }
@@ -1589,16 +1609,19 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
     if (e != cudaSuccess) return e;
   }
   const size_t dyn = dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) +
-                                         ((dp.remote_warp == 1 || dp.remote_warp == 3) ? RING_BYTES : 0) : 0;
+                                         ((dp.remote_warp == 1 || dp.remote_warp == 3) ? RING_BYTES : 0) +
+                                         (CR ? sizeof(double2) * (size_t)dp.rows_per_tile : 0) : 0;
   CUtensorMap tm;  // remote_warp 3: the tensor map of the stage's input z (zA or zB)
   if (dp.tmaps) tm = dp.tmaps[a.zin == dp.zbuf[0] ? 0 : 1];
   else memset(&tm, 0, sizeof(tm));
-  return launch_maybe_pdl(dp.pdl != 0, k_stage<MODE, RW>, dim3(dp.ntiles), dim3(NTHREADS), dyn, s, dp, a, tm);
+  return launch_maybe_pdl(dp.pdl != 0, k_stage<MODE, RW, CR>, dim3(dp.ntiles), dim3(NTHREADS), dyn, s, dp, a, tm);
 }
 
 template <int MODE>
 cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
-  return dp.remote_warp ? launch_stage_m<MODE, true>(dp, a, s) : launch_stage_m<MODE, false>(dp, a, s);
+  if (dp.remote_warp) return launch_stage_m<MODE, true, false>(dp, a, s);
+  if (dp.cr_hot_warps > 0) return launch_stage_m<MODE, false, true>(dp, a, s);
+  return launch_stage_m<MODE, false, false>(dp, a, s);
 }
 
 }  // namespace

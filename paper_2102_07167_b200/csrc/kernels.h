@@ -38,6 +38,8 @@ struct DevPlan {
                               // warp of each tile sums its remote part while the others gather the hot
                               // windows: 1 = z gathered by 16-byte TMA bulk copies into a shared-memory
                               // ring, 2 = LDG gathers, 3 = TMA tile::gather4 (4 entries per request)
+  int32_t cr_hot_warps;       // > 0: inline remote parts run concurrently on warps [cr_hot_warps, NWARPS)
+                              // while the hot windows are gathered by the others (k_stage<..., CR = true>)
   const CUtensorMap* tmaps;   // remote_warp 3: HOST array [2] = tensor maps of zbuf[0], zbuf[1] (launcher only)
   const double2* zbuf[2];     // zA, zB (device)
   const TileDesc* tiles;      // [ntiles]

@@ -166,3 +166,30 @@ def test_config5_world8_bitwise():
     ok, bounds = _group_vs_single(inst, 8, steps=2)
     assert all(ok), ok
     assert len(bounds) == 8 and all(b - a == inst.n // 8 for a, b in bounds), bounds
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_concurrent_inline_remote_bitwise(world, monkeypatch):
+    """The inline remote part run concurrently with the hot windows on warps [k, 16) (KUR_CONC_REMOTE=k,
+    k_stage<..., CR>) gives the bits of the sequential inline part and of the k_remote pass."""
+    inst = kurgen.sbm([3000, 2000, 2500, 1200], np.array(
+        [[0.95, 0.004, 0.003, 0.002], [0.004, 0.97, 0.003, 0.005], [0.003, 0.003, 0.9, 0.004],
+         [0.002, 0.005, 0.004, 0.96]]), 43, K=3.0, h=0.01)
+    ref = None
+    for mode, rp in (("0", False), ("8", False), ("4", False), ("12", False), ("0", True)):
+        monkeypatch.setenv("KUR_CONC_REMOTE", mode)
+        if world == 1:
+            g = kur.graph_build(inst, remote_pass=rp, tile_rows=256)
+            th = g.to_internal(torch.from_numpy(inst.theta0).cuda())
+            om = g.to_internal(torch.from_numpy(inst.omega).cuda())
+            f = kur.rhs(g, th, om, inst.K)
+            rt = kur.step(g, th, om, inst.K, inst.h, 5, 1)
+            out = (f, th, rt)
+            g.close()
+            if ref is None:
+                ref = out
+            else:
+                assert all(torch.equal(x, y) for x, y in zip(out, ref)), (mode, rp)
+        else:
+            ok, _ = _group_vs_single(inst, world, steps=4, remote_pass=rp, tile_rows=256)
+            assert all(ok), (mode, rp, ok)
