@@ -117,12 +117,14 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
-  // evict-normal: the tiles of one community run together (the builder's launch order) and re-read
-  // its windows from L2 (config 5: k_stage DRAM reads 3.31 -> 2.90 GB per launch against evict-first,
-  // profiles/r02/notes/window_policy_ab.log).  A compile-time choice: a runtime switch between
-  // policies here cost k_stage 2 % (profiles/r02/notes/window_policy_branch_cost.log).
+  // evict-first: a window is dead once its community's tiles have staged it; z_out (stored by this
+  // kernel, gathered by the next k_remote) keeps the L2.  Measured alternative (config 5,
+  // profiles/r02/notes/window_policy_ab.log, r2k_ab.log): evict-normal with the tiles of a community
+  // launched together re-reads windows from L2 -- k_stage DRAM reads 3.31 -> 2.90 GB per launch --
+  // but the stage got 0.5 % slower (k_stage is bound by the L1/LSU pipe, not DRAM).  Compile-time:
+  // a runtime switch between policies here cost k_stage 2 % (notes/window_policy_branch_cost.log).
   uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           smem_addr(dst)),
