@@ -1397,10 +1397,12 @@ __device__ __forceinline__ void record_rpsi(const DevPlan& dp, const double* rp,
   }
 }
 
+// R = rows per thread (ceil(rows_per_tile / NTHREADS)): config 2's 3552-row tiles need 7, and every
+// row slot held in registers costs two live doubles (theta_n, acc) across the whole trajectory
+template <int R>
 __global__ void __launch_bounds__(NTHREADS, 2) k_persist_rk4(const DevPlan dp, const StageArgs a, double2* pbuf,
                                                              unsigned long long* cnt, long long nsteps,
                                                              unsigned long long q0) {
-  constexpr int R = MAX_TILE_ROWS_NOPARTS / NTHREADS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* zc = reinterpret_cast<double*>(smem_raw);  // [rows_per_tile] z of the stage state
   double* zsn = zc + dp.rows_per_tile;
@@ -1713,15 +1715,31 @@ size_t persist_smem_bytes(const DevPlan& dp) {
   return sizeof(double) * 3 * (size_t)dp.rows_per_tile + sizeof(double2) * (size_t)std::max(dp.C, 1);
 }
 
+using PersistKernel = void (*)(const DevPlan, const StageArgs, double2*, unsigned long long*, long long,
+                               unsigned long long);
+PersistKernel persist_kernel(const DevPlan& dp) {
+  switch ((dp.rows_per_tile + NTHREADS - 1) / NTHREADS) {
+    case 1: return k_persist_rk4<1>;
+    case 2: return k_persist_rk4<2>;
+    case 3: return k_persist_rk4<3>;
+    case 4: return k_persist_rk4<4>;
+    case 5: return k_persist_rk4<5>;
+    case 6: return k_persist_rk4<6>;
+    case 7: return k_persist_rk4<7>;
+    default: return k_persist_rk4<8>;
+  }
+}
+
 bool persist_fits(const DevPlan& dp) {
   if (dp.world != 1 || dp.has_parts || dp.ntiles <= 0 || dp.rows_per_tile > MAX_TILE_ROWS_NOPARTS) return false;
   const size_t smem = persist_smem_bytes(dp);
   if (smem > 200 * 1024) return false;
   int dev = 0, sms = 0, nb = 0;
+  const PersistKernel k = persist_kernel(dp);
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-      cudaFuncSetAttribute(k_persist_rk4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persist_rk4, NTHREADS, smem) != cudaSuccess) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, NTHREADS, smem) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -1731,13 +1749,13 @@ bool persist_fits(const DevPlan& dp) {
 cudaError_t launch_persist_rk4(const DevPlan& dp, const StageArgs& a, double2* pbuf, unsigned long long* cnt,
                                long long nsteps, unsigned long long q0, cudaStream_t s) {
   const size_t smem = persist_smem_bytes(dp);
-  cudaError_t e = cudaFuncSetAttribute(k_persist_rk4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const PersistKernel k = persist_kernel(dp);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   DevPlan d = dp;
   StageArgs aa = a;
   void* args[] = {(void*)&d, (void*)&aa, (void*)&pbuf, (void*)&cnt, (void*)&nsteps, (void*)&q0};
-  return cudaLaunchCooperativeKernel((const void*)k_persist_rk4, dim3((unsigned)dp.ntiles), dim3(NTHREADS), args,
-                                     smem, s);
+  return cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)dp.ntiles), dim3(NTHREADS), args, smem, s);
 }
 
 cudaError_t launch_unpack(const DevPlan& dp, const double* xrecv, double2* zout, unsigned int expect,
