@@ -471,8 +471,7 @@ def main():
                                                   if world > 1 else 0),
             "clocks": clk.result(),
             "host": dict(_host_info(), gen_s=gen_s, build_s=build_s),
-            "plan": {k: info[k] for k in ("n_idx_hot", "n_idx_remote", "n_idx_cold", "n_slots_hot", "n_slots_remote",
-                                          "n_slots_cold", "n_cold_parts",
+            "plan": {k: info[k] for k in ("n_idx_hot", "n_idx_remote", "n_slots_hot", "n_slots_remote",
                                           "n_dense_blocks", "n_sparse_blocks", "n_tiles", "rows_per_tile",
                                           "bytes_per_rhs", "bytes_pool")},
             "csr_bytes_per_rhs": 4 * int(info["nnz"]),

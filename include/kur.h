@@ -156,10 +156,6 @@ typedef struct {
   int32_t remote_pass;         /* 1: remote entries summed by the separate k_remote pass before each
                                   stage kernel (2 launches per RHS), 0: inline */
   int32_t peer_exchange;       /* world > 1: 1 = fused peer-store exchange active, 0 = all-gather */
-  int64_t n_idx_cold;          /* stored entries summed by the cold-window pass k_cold (windows holding
-                                  256..hot_min-1 of a tile's entries; 13-bit slots; in n_idx too) */
-  int64_t n_slots_cold;        /* cold slots incl. padding */
-  int64_t n_cold_parts;        /* cold parts (one per-row partial buffer each) */
 } kur_graph_info_t;
 
 typedef struct kur_graph kur_graph; /* opaque; owns all device data and workspace */
@@ -308,8 +304,7 @@ kur_status kur_check(kur_graph *g, void *stream);
  *   rows_per_tile, nnz, world, bank conflicts found by the last export (hot
  *   quarter-warp positions whose slots share a residue mod 8; 0 by
  *   construction), hot slots, hot entries, remote slots, remote entries,
- *   window loads per RHS, cold entries, cold slots, cold parts, k_cold groups
- *   (sizes[16..19]);
+ *   window loads per RHS;
  *   perm[n]: user id of internal node i; D_ptr[n_comm+1], D_idx: dense column
  *   communities of each row community (their block sums are added);
  *   row_ptr[n_local+1], cols[n_entries] (internal column ids), neg[n_entries]
@@ -319,7 +314,7 @@ kur_status kur_check(kur_graph *g, void *stream);
 typedef struct kur_plan kur_plan;
 kur_status kur_plan_build(const kur_graph_desc *desc, int32_t rank, int32_t world, int32_t sm_count,
                           kur_plan **out);
-kur_status kur_plan_sizes(const kur_plan *p, int64_t *sizes /* [20] */);
+kur_status kur_plan_sizes(const kur_plan *p, int64_t *sizes /* [16] */);
 kur_status kur_plan_export(const kur_plan *p, int32_t *perm, int32_t *D_ptr, int32_t *D_idx, int64_t *row_ptr,
                            int32_t *cols, int8_t *neg, int32_t *shard_row0);
 kur_status kur_plan_destroy(kur_plan *p);

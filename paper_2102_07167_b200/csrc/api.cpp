@@ -70,10 +70,6 @@ struct kur_graph {
   double* pmax = nullptr;
   double2* Wr = nullptr;
   uint32_t* d_rchunks = nullptr;
-  PartDesc* d_cparts = nullptr;
-  ColdGroup* d_cgroups = nullptr;
-  int32_t* d_cgroup_parts = nullptr;
-  double2* Pc = nullptr;
   uint8_t* d_rem_lp = nullptr;
   Ctrl* ctrl = nullptr;
   ncclComm_t comm = nullptr;
@@ -121,8 +117,7 @@ struct kur_graph {
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
                     xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh, d_rchunks, d_rem_lp, d_flag, d_xticket,
-                    d_peer_x, d_peer_flag, theta_ws, omega_ws, pbuf, gbar, d_big, d_cparts, d_cgroups,
-                    d_cgroup_parts, Pc};
+                    d_peer_x, d_peer_flag, theta_ws, omega_ws, pbuf, gbar, d_big};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -419,22 +414,6 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   // (the early-resident k_remote / k_stage CTAs of the next stage only wait), so off by default.
   dp.pdl = (world == 1 && std::getenv("KUR_PDL") != nullptr) ? 1 : 0;
   dp.Wr = g->Wr;
-  dp.n_cgroups = (int32_t)P.cgroups.size();
-  dp.cparts = nullptr;
-  dp.cgroups = nullptr;
-  dp.cgroup_parts = nullptr;
-  dp.Pc = nullptr;
-  if (!P.cparts.empty()) {  // cold parts: k_cold writes signed per-row partials, zero where a row has none
-    const size_t pcb = sizeof(double2) * P.cparts.size() * (size_t)P.rows_per_tile;
-    if ((e = upload(&g->d_cparts, P.cparts)) != cudaSuccess || (e = upload(&g->d_cgroups, P.cgroups)) != cudaSuccess ||
-        (e = upload(&g->d_cgroup_parts, P.cgroup_parts)) != cudaSuccess ||
-        (e = cudaMalloc((void**)&g->Pc, pcb)) != cudaSuccess || (e = cudaMemset(g->Pc, 0, pcb)) != cudaSuccess)
-      return bail(e, "cold parts");
-    dp.cparts = g->d_cparts;
-    dp.cgroups = g->d_cgroups;
-    dp.cgroup_parts = g->d_cgroup_parts;
-    dp.Pc = g->Pc;
-  }
   dp.peer_x = g->peer_on ? g->d_peer_x : nullptr;
   dp.peer_flag = g->d_peer_flag;
   dp.xticket = g->d_xticket;
@@ -491,6 +470,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   I.nnz = P.nnz;
   I.n_idx_hot = P.n_idx_hot;
   I.n_idx_remote = P.n_idx_remote;
+  I.n_idx = P.n_idx_hot + P.n_idx_remote;
   I.n_slots_hot = P.n_slots_hot;
   I.n_slots_remote = P.n_slots_remote;
   I.n_dense_blocks = P.n_dense_blocks;
@@ -501,13 +481,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   // algorithmic bytes of one fused RK stage (= one RHS evaluation), DESIGN.md §5:
   // index stream (13 bits per hot entry, 4 B per remote entry, no padding) plus per
   // local row z_in 16 + z_out 16 + omega 8 + theta_n 8 + acc 16 = 64 B.
-  I.n_idx_cold = P.n_idx_cold;
-  I.n_slots_cold = P.n_slots_cold;
-  I.n_cold_parts = (int64_t)P.cparts.size();
-  I.n_idx = P.n_idx_hot + P.n_idx_remote + P.n_idx_cold;
-  // + cold entries at 13 bits and their per-row partials (16 B written + 16 B read per part row)
-  I.bytes_per_rhs = (13 * (P.n_idx_hot + P.n_idx_cold) + 7) / 8 + 4 * P.n_idx_remote + 64 * g->n_local +
-                    32 * (int64_t)P.cparts.size() * P.rows_per_tile;
+  I.bytes_per_rhs = (13 * P.n_idx_hot + 7) / 8 + 4 * P.n_idx_remote + 64 * g->n_local;
   I.bytes_pool = pool_bytes;
   I.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   I.remote_pass = dp.has_remote;
@@ -655,11 +629,9 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
   for (size_t r = 0; r < gs.size(); ++r) {
     kur_graph* g = gs[r];
     StageArgs& a = args[r];
-    const bool side = (g->dp.has_remote && !g->dp.remote_warp) || g->dp.n_cgroups > 0;
-    if (g->timing && mode != PH_PROLOGUE && side && !(world > 1 && a.phase == PHASE_A)) {  // time k_remote/k_cold apart
+    if (g->timing && mode != PH_PROLOGUE && g->dp.has_remote && !g->dp.remote_warp) {  // time k_remote, k_stage apart
       KUR_CUDA(g->mark(s));
       KUR_CUDA(launch_remote(g->dp, a.zin, s));
-      KUR_CUDA(launch_cold(g->dp, a.zin, s));
       KUR_CUDA(g->mark(s));
       g->ev_kind.push_back({2, 1});
       a.no_remote = 1;
@@ -1255,7 +1227,7 @@ kur_status kur_plan_sizes(const kur_plan* p, int64_t* sizes) {
   sizes[1] = P.C;
   sizes[2] = P.row_end - P.row_begin;
   sizes[3] = P.row_begin;
-  sizes[4] = P.n_idx_hot + P.n_idx_remote + P.n_idx_cold;
+  sizes[4] = P.n_idx_hot + P.n_idx_remote;
   sizes[5] = (int64_t)P.D_idx.size();
   sizes[6] = (int64_t)P.tiles.size();
   sizes[7] = P.rows_per_tile;
@@ -1267,10 +1239,6 @@ kur_status kur_plan_sizes(const kur_plan* p, int64_t* sizes) {
   sizes[13] = P.n_slots_remote;
   sizes[14] = P.n_idx_remote;
   sizes[15] = P.n_window_loads;
-  sizes[16] = P.n_idx_cold;
-  sizes[17] = P.n_slots_cold;
-  sizes[18] = (int64_t)P.cparts.size();
-  sizes[19] = (int64_t)P.cgroups.size();
   return KUR_OK;
 }
 
@@ -1309,12 +1277,10 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
     return t16[(size_t)l * 4 + (pos - 9 * G)];
   };
   for (const TileDesc& T : P.tiles) {
-    // the tile's parts, then its cold parts (window-local slots like hot parts, summed by k_cold)
-    for (int pi = T.part0; pi < T.part0 + T.nparts + T.ncold; ++pi) {
-      const bool is_cold = pi >= T.part0 + T.nparts;
-      const PartDesc& pd = is_cold ? P.cparts[(size_t)(T.cold0 + (pi - T.part0 - T.nparts))] : P.parts[(size_t)pi];
+    for (int pi = T.part0; pi < T.part0 + T.nparts; ++pi) {
+      const PartDesc& pd = P.parts[(size_t)pi];
       const bool hot = pd.window >= 0;
-      if (is_cold ? !hot : hot != (pi < T.part0 + T.nhot)) return fail(KUR_ERR_INVALID_ARG, "plan: part order");
+      if (hot != (pi < T.part0 + T.nhot)) return fail(KUR_ERR_INVALID_ARG, "plan: part order");
       std::vector<uint8_t> seen((size_t)T.nrows, 0);
       const int pcs = 1 << (pd.neg >> 8);  // row pieces per row (aligned lane groups)
       for (uint32_t c = 0; c < pd.nchunks; ++c) {

@@ -639,19 +639,10 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   struct TileOut {
     std::vector<Unit> units;
     std::vector<PartDesc> parts;    // chunk0 relative to the tile
-    std::vector<PartDesc> cparts;   // cold parts (window order), chunk0 relative to the tile
     std::vector<ChunkDesc> chunks;  // ofs relative to the tile
     int32_t nhot = 0, nown = 0, nloc = 0;
-    int64_t hot = 0, rem = 0, shot = 0, srem = 0, loads = 0, cold = 0, scold = 0;
+    int64_t hot = 0, rem = 0, shot = 0, srem = 0, loads = 0;
   };
-  // Cold parts (k_cold): a window holding cold_min .. hot_min-1 of a tile's entries is
-  // summed by a separate pass in which one staged copy of the window serves that window's parts of
-  // many tiles (config 3: ~1 K entries per (tile, other-community window)), instead of one random
-  // L1-wavefront gather per entry.  Off for tiny plans (single-CTA trajectories) and when the
-  // per-row partial buffer (<= MAX_COLD_PER_TILE x 16 B per row) would exceed 512 MB.
-  const bool cold_ok = !P.small && std::getenv("KUR_NO_COLD") == nullptr &&
-                       (P.row_end - P.row_begin) * (int64_t)MAX_COLD_PER_TILE * 16 <= (512LL << 20) &&
-                       COLD_MIN < hot_min;
   std::vector<TileOut> outs((size_t)nt);
 #pragma omp parallel
   {
@@ -673,8 +664,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
       }
       std::sort(keys.begin(), keys.end());
       // one part = entries src[k0..k1) of one (window|remote, sign), sorted by (row, column)
-      auto emit_part = [&](int32_t window, int32_t neg, const uint64_t* src, size_t k0, size_t k1,
-                           bool cold = false) {
+      auto emit_part = [&](int32_t window, int32_t neg, const uint64_t* src, size_t k0, size_t k1) {
         const bool hot = window >= 0;
         PartDesc pd{window, neg, (uint32_t)O.chunks.size(), 0};
         // rows with entries, longest first
@@ -813,7 +803,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
               for (int lane = 0; lane < 32; ++lane)
                 for (int e = 0; e < 4; ++e) t16[(size_t)lane * 4 + (size_t)e] = (uint16_t)slot_at(lane, (size_t)G * 9 + (size_t)e);
             }
-            (cold ? O.scold : O.shot) += (int64_t)(9 * G + 4 * tail) * 32;
+            O.shot += (int64_t)(9 * G + 4 * tail) * 32;
           } else {
             int mx = 0;
             for (int l = 0; l < 32; ++l)
@@ -838,11 +828,6 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
           O.chunks.push_back(cd);
           pd.nchunks++;
         }
-        if (cold) {
-          O.cparts.push_back(pd);
-          O.cold += (int64_t)(k1 - k0);
-          return;
-        }
         O.parts.push_back(pd);
         if (hot) O.hot += (int64_t)(k1 - k0); else O.rem += (int64_t)(k1 - k0);
       };
@@ -859,11 +844,6 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
           if (m > i) { emit_part((int32_t)w, 0, keys.data(), i, m); O.nhot++; }
           if (j > m) { emit_part((int32_t)w, 1, keys.data(), m, j); O.nhot++; }
           if ((int32_t)w != last_w) { O.loads++; last_w = (int32_t)w; }
-        } else if (cold_ok && (int64_t)(j - i) >= COLD_MIN && (int)O.cparts.size() + 2 <= MAX_COLD_PER_TILE) {
-          size_t m = i;  // cold part(s): window-local slots like a hot part, summed by k_cold
-          while (m < j && !((keys[m] >> 43) & 1)) ++m;
-          if (m > i) emit_part((int32_t)w, 0, keys.data(), i, m, true);
-          if (j > m) emit_part((int32_t)w, 1, keys.data(), m, j, true);
         } else {  // remote: (row, sign in bit 31, column) -> one part per tile with per-entry signs
           for (size_t k = i; k < j; ++k)
             remk.push_back((keys[k] & (0x7FFULL << 32)) | (((keys[k] >> 43) & 1) << 31) | (keys[k] & COLM));
@@ -894,27 +874,23 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   }
   // ------------------------------------------------------------ 6. concatenate
   P.tiles.resize((size_t)nt);
-  int64_t units = 0, nparts = 0, nchunks = 0, ncparts = 0;
+  int64_t units = 0, nparts = 0, nchunks = 0;
   for (int32_t lt = 0; lt < nt; ++lt) {
     units += (int64_t)outs[(size_t)lt].units.size();
     nparts += (int64_t)outs[(size_t)lt].parts.size();
-    ncparts += (int64_t)outs[(size_t)lt].cparts.size();
     nchunks += (int64_t)outs[(size_t)lt].chunks.size();
   }
-  P.cparts.assign((size_t)ncparts, PartDesc{-1, 0, 0, 0});
   if (units >= (int64_t)UINT32_MAX) { err = "index pool exceeds 64 GB"; return KUR_ERR_UNSUPPORTED; }
   P.pool.resize((size_t)std::max<int64_t>(units, 1));
   P.parts.assign((size_t)std::max<int64_t>(nparts, 1), PartDesc{-1, 0, 0, 0});
   P.chunks.assign((size_t)std::max<int64_t>(nchunks, 1), ChunkDesc{0, 0});
-  int64_t uo = 0, po = 0, co = 0, cpo = 0;
+  int64_t uo = 0, po = 0, co = 0;
   P.n_idx_hot = P.n_idx_remote = P.n_slots_hot = P.n_slots_remote = P.n_hot_parts = P.n_window_loads = 0;
-  P.n_idx_cold = P.n_slots_cold = 0;
-  std::vector<int64_t> uofs((size_t)nt), pofs((size_t)nt), cofs((size_t)nt), cpofs((size_t)nt);
+  std::vector<int64_t> uofs((size_t)nt), pofs((size_t)nt), cofs((size_t)nt);
   for (int32_t lt = 0; lt < nt; ++lt) {
     uofs[(size_t)lt] = uo;
     pofs[(size_t)lt] = po;
     cofs[(size_t)lt] = co;
-    cpofs[(size_t)lt] = cpo;
     const TileOut& O = outs[(size_t)lt];
     TileDesc T = all[(size_t)(P.tile_begin + lt)];
     T.part0 = (int32_t)po;
@@ -922,15 +898,10 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     T.nhot = O.nhot;
     T.nown = O.nown;
     T.nloc = O.nloc;
-    T.cold0 = (int32_t)cpo;
-    T.ncold = (int32_t)O.cparts.size();
     P.tiles[(size_t)lt] = T;
     uo += (int64_t)O.units.size();
     po += (int64_t)O.parts.size();
-    cpo += (int64_t)O.cparts.size();
     co += (int64_t)O.chunks.size();
-    P.n_idx_cold += O.cold;
-    P.n_slots_cold += O.scold;
     P.n_idx_hot += O.hot;
     P.n_idx_remote += O.rem;
     P.n_slots_hot += O.shot;
@@ -956,43 +927,12 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
       pd.chunk0 += (uint32_t)cofs[(size_t)lt];
       P.parts[(size_t)pofs[(size_t)lt] + p] = pd;
     }
-    for (size_t p = 0; p < O.cparts.size(); ++p) {
-      PartDesc pd = O.cparts[p];
-      pd.chunk0 += (uint32_t)cofs[(size_t)lt];
-      P.cparts[(size_t)cpofs[(size_t)lt] + p] = pd;
-    }
     for (size_t c = 0; c < O.chunks.size(); ++c) {
       ChunkDesc cd = O.chunks[c];
       cd.ofs += (uint32_t)uofs[(size_t)lt];
       P.chunks[(size_t)cofs[(size_t)lt] + c] = cd;
     }
     std::vector<Unit>().swap(O.units);
-  }
-  // k_cold CTAs: the cold parts of one window (over all tiles of this rank), cut into groups of about
-  // COLD_GROUP_ENTRIES slots; a group's parts are listed in the order of P.cgroup_parts
-  P.cgroups.clear();
-  P.cgroup_parts.clear();
-  if (!P.cparts.empty()) {
-    std::vector<std::pair<int32_t, int32_t>> wp;  // (window, cold part id)
-    wp.reserve(P.cparts.size());
-    for (size_t q = 0; q < P.cparts.size(); ++q) wp.push_back({P.cparts[q].window, (int32_t)q});
-    std::stable_sort(wp.begin(), wp.end());
-    size_t a = 0;
-    while (a < wp.size()) {
-      ColdGroup G{wp[a].first, (int32_t)P.cgroup_parts.size(), 0, 0};
-      int64_t acc = 0;
-      while (a < wp.size() && wp[a].first == G.window && (G.nparts == 0 || acc < COLD_GROUP_ENTRIES)) {
-        const PartDesc& pd = P.cparts[(size_t)wp[a].second];
-        for (uint32_t c = 0; c < pd.nchunks; ++c) {
-          const uint32_t ng = P.chunks[(size_t)(pd.chunk0 + c)].ng;
-          acc += (int64_t)(9 * (ng >> 1) + 4 * (ng & 1)) * 32;
-        }
-        P.cgroup_parts.push_back(wp[a].second);
-        G.nparts++;
-        ++a;
-      }
-      P.cgroups.push_back(G);
-    }
   }
   if (P.split_remote) {  // flat list of every remote chunk (one warp each in k_remote), longest first
     std::vector<std::array<uint32_t, 4>> rc;

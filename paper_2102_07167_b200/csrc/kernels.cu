@@ -935,25 +935,6 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       w.x += r.x;
       w.y += r.y;
     }
-    if (!SMALL && T.ncold > 0 && a.phase != PHASE_A) {  // cold parts (k_cold), in window order
-      const double2* pc = dp.Pc + (size_t)T.cold0 * dp.rows_per_tile + lr;
-      int c = 0;
-      for (; c + 4 <= T.ncold; c += 4) {
-        double2 b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) b[i] = __ldcg(pc + (size_t)(c + i) * dp.rows_per_tile);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          w.x += b[i].x;
-          w.y += b[i].y;
-        }
-      }
-      for (; c < T.ncold; ++c) {
-        const double2 r = __ldcg(pc + (size_t)c * dp.rows_per_tile);
-        w.x += r.x;
-        w.y += r.y;
-      }
-    }
     const double wx = Tc.x + w.x, wy = Tc.y + w.y;
     const double2 zj = SMALL ? __ldcg(a.zin + row) : a.zin[row];
     // K/M_m: uniform K/N, or K/deg_m for the degree scaling
@@ -1097,50 +1078,6 @@ __global__ void __launch_bounds__(KREM_THREADS, KREM_CTAS_PER_SM) k_remote(const
     b1 = b1n;
     rc1 = rc2;
     cd1 = cd2;
-  }
-}
-
-// Cold parts: one CTA stages one window (TMA bulk copy) and sums that window's cold parts of many
-// tiles from shared memory (1/8 L1 wavefront per entry, conflict-free like a hot part); each row's
-// signed sum 0 + s (non-zero entries) or 0 - s (complement entries) goes to
-// Pc[part][row], added by the tile's finalize in window order.  Chunks of a group's parts are dealt
-// round-robin over the 16 warps; every row lies in exactly one chunk of a part, so Pc is written, not
-// accumulated (rows without entries keep the zeros Pc was initialised with).
-__global__ void __launch_bounds__(NTHREADS, 2) k_cold(const DevPlan dp, const double2* __restrict__ zin) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* zs = reinterpret_cast<double2*>(smem_raw);  // [WZ + 8]
-  __shared__ __align__(8) uint64_t bar;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const ColdGroup G = dp.cgroups[blockIdx.x];
-  if (tid < 8) zs[WZ + tid] = make_double2(0.0, 0.0);
-  if (tid == 0) mbar_init(&bar, 1);
-  __syncthreads();
-  if (tid == 0) tma_load_1d(zs, zin + (size_t)G.window * WZ, WZ * sizeof(double2), &bar);
-  mbar_wait(&bar, 0);
-  const uint64_t pol = evict_first_policy();
-  int base = 0;
-  for (int i = 0; i < G.nparts; ++i) {
-    const int pid = dp.cgroup_parts[G.part0 + i];
-    const PartDesc P = dp.cparts[pid];
-    KUR_ASSERT(P.window == G.window);
-    double2* out = dp.Pc + (size_t)pid * dp.rows_per_tile;
-    const int lp = P.neg >> 8;
-    for (int c = ((warp - base) % NWARPS + NWARPS) % NWARPS; c < (int)P.nchunks; c += NWARPS) {
-      const uint2 cd = __ldg(dp.chunks + P.chunk0 + c);
-      const uint4* q = dp.pool + cd.x;
-      const uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
-      double sx, sy;
-      run_hot(q + HDR_UNITS, cd.y, lane, zs, pol, sx, sy);
-      for (int o = 1; o < (1 << lp); o <<= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        sy += __shfl_xor_sync(0xffffffffu, sy, o);
-      }
-      if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) {
-        KUR_ASSERT(row < dp.rows_per_tile);
-        __stcg(out + row, (P.neg & 1) ? make_double2(0.0 - sx, 0.0 - sy) : make_double2(0.0 + sx, 0.0 + sy));
-      }
-    }
-    base += (int)P.nchunks;
   }
 }
 
@@ -1675,10 +1612,6 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
     cudaError_t e = launch_remote(dp, a.zin, s);
     if (e != cudaSuccess) return e;
   }
-  if (dp.n_cgroups > 0 && !a.no_remote && a.phase != PHASE_A) {
-    cudaError_t e = launch_cold(dp, a.zin, s);
-    if (e != cudaSuccess) return e;
-  }
   const size_t dyn = dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) +
                                          ((dp.remote_warp == 1 || dp.remote_warp == 3) ? RING_BYTES : 0) +
                                          (CR ? sizeof(double2) * (size_t)dp.rows_per_tile : 0) : 0;
@@ -1723,21 +1656,6 @@ cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s)
 }
 
 size_t stage_smem_bytes(int rows_per_tile) { return sizeof(double2) * (size_t)(WZ + 8 + rows_per_tile); }
-
-cudaError_t launch_cold(const DevPlan& dp, const double2* zin, cudaStream_t s) {
-  if (dp.n_cgroups <= 0) return cudaSuccess;
-  static std::atomic<uint64_t> attr_set{0};  // one bit per device
-  const size_t smem = sizeof(double2) * (size_t)(WZ + 8);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!((attr_set.load() >> (dev & 63)) & 1)) {
-    cudaError_t e = cudaFuncSetAttribute(k_cold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set.fetch_or(1ull << (dev & 63));
-  }
-  k_cold<<<dp.n_cgroups, NTHREADS, smem, s>>>(dp, zin);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
   if (dp.ntiles <= 0) {

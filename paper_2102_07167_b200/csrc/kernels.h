@@ -70,11 +70,6 @@ struct DevPlan {
   const uint32_t* rchunks;    // [n_rchunks][2] remote pass: {chunk id, local row of the tile's row 0}
   const uint8_t* rem_lp;      // [n_rchunks] row-piece shift of each chunk's part
   int32_t n_rchunks;
-  const PartDesc* cparts;     // [n cold parts] cold parts (window-local slots; chunk table shared)
-  const ColdGroup* cgroups;   // [n_cgroups] k_cold CTAs
-  const int32_t* cgroup_parts;  // cold part ids of the groups
-  int32_t n_cgroups;
-  double2* Pc;                // [n cold parts][rows_per_tile] signed partial row sums of the cold parts
   double2* S;                 // [C] block sums S_b of the last reduction
   Ctrl* ctrl;
 };
@@ -130,8 +125,6 @@ cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t 
 // k_remote (plans with the remote pass); launch_stage runs it first unless a.no_remote
 cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s);
 cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaStream_t s);
-// k_cold (plans with cold parts); launch_stage runs it first unless a.no_remote
-cudaError_t launch_cold(const DevPlan& dp, const double2* zin, cudaStream_t s);
 // world > 1: after the all-gather of the packed buffers (xrecv = world x xstride doubles),
 // z of every non-local row from its exchanged phase, all tile partials; then the
 // fixed-order block-sum reduction by one CTA.

@@ -53,7 +53,7 @@ constexpr int MAX_TILE_ROWS_NOPARTS = 4096;  // plans without stored entries kee
 constexpr int HDR_UNITS = 4;         // 64-byte chunk header
 constexpr uint16_t EMPTY_LANE = 0xFFFF;
 
-struct TileDesc {   // 48 bytes; device array
+struct TileDesc {   // 32 bytes; device array
   int32_t row0;     // first internal row (global numbering)
   int32_t nrows;    // rows in this tile (<= rows_per_tile)
   int32_t comm;     // community of every row of the tile
@@ -62,22 +62,7 @@ struct TileDesc {   // 48 bytes; device array
   int32_t nhot;     // number of hot parts
   int32_t nown;     // of which the first nown lie wholly inside the tile's own community
   int32_t nloc;     // of which the first nloc also lie inside this rank's rows (phase A, world > 1)
-  int32_t cold0;    // first cold part of the tile (this rank's cold part list)
-  int32_t ncold;    // cold parts: windows holding cold_min..hot_min-1 of the tile's entries, summed by
-                    // k_cold (one staged window serves every tile's part of it) into Pc
-  int32_t pad2[2];
 };
-
-struct ColdGroup {  // 16 bytes; one k_cold CTA: cold parts [part0, part0 + nparts) of one window
-  int32_t window;
-  int32_t part0;
-  int32_t nparts;
-  int32_t pad;
-};
-
-constexpr int COLD_MIN = 256;            // entries of a (tile, window) below hot_min that make a cold part
-constexpr int MAX_COLD_PER_TILE = 32;    // bounds Pc to 32 x 16 B per row
-constexpr int COLD_GROUP_ENTRIES = 16384;  // entries per k_cold CTA (one staged window)
 
 struct PartDesc {   // 16 bytes; device array
   int32_t window;   // window id (hot) or -1 (remote)
@@ -119,14 +104,10 @@ struct HostPlan {
   std::vector<uint8_t> rem_lp;      // remote pass: row-piece shift (PartDesc.neg >> 8) per listed chunk
   std::vector<double> rowscale;     // [local rows] 1/M_m (degree scaling only; empty = uniform K/N)
   std::vector<double> potc;         // [local rows] off-diagonal ones + [z_m inside W_m] (kur_potential)
-  std::vector<PartDesc> cparts;     // this rank's cold parts (window-local slots, like hot parts)
-  std::vector<ColdGroup> cgroups;   // k_cold CTAs
-  std::vector<int32_t> cgroup_parts;  // cold part ids grouped by window (cgroups index into it)
   std::vector<int32_t> shard_row0;  // [world+1] internal row ranges of all ranks
   std::vector<int32_t> shard_tile0; // [world+1]
   // statistics (this rank)
   int64_t nnz = 0, n_idx_hot = 0, n_idx_remote = 0, n_slots_hot = 0, n_slots_remote = 0;
-  int64_t n_idx_cold = 0, n_slots_cold = 0;
   int64_t n_dense_blocks = 0, n_sparse_blocks = 0, n_hot_parts = 0;
   int64_t n_window_loads = 0;       // hot windows staged per RHS (all tiles)
 };

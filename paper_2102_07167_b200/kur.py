@@ -52,7 +52,7 @@ class GraphInfo(ctypes.Structure):
                 ("n_slots_remote", _i64), ("n_dense_blocks", _i64), ("n_sparse_blocks", _i64),
                 ("n_tiles", _i64), ("n_hot_parts", _i64), ("n_window_loads", _i64), ("sincos_per_rhs", _i64),
                 ("bytes_per_rhs", _i64), ("bytes_pool", _i64), ("build_seconds", _d), ("remote_pass", _i32),
-                ("peer_exchange", _i32), ("n_idx_cold", _i64), ("n_slots_cold", _i64), ("n_cold_parts", _i64)]
+                ("peer_exchange", _i32)]
 
 
 class AdaptiveCtrl(ctypes.Structure):
@@ -461,7 +461,7 @@ def plan_export(inst, *, rank=0, world=1, sm_count=148, dense_threshold=-1.0, ho
     h = ctypes.c_void_p()
     _check(_lib.kur_plan_build(ctypes.byref(desc), rank, world, sm_count, ctypes.byref(h)))
     try:
-        sz = np.zeros(20, np.int64)
+        sz = np.zeros(16, np.int64)
         _check(_lib.kur_plan_sizes(h, _np_ptr(sz)))
         n, C, nl, rb, ne, nd, nt, rpt_rows, nnz, w = (int(x) for x in sz[:10])
         out = dict(n=n, n_comm=C, n_local=nl, row_begin=rb, n_tiles=nt, rows_per_tile=rpt_rows, nnz=nnz,
@@ -476,8 +476,7 @@ def plan_export(inst, *, rank=0, world=1, sm_count=148, dense_threshold=-1.0, ho
         out["neg"] = out["neg"][:ne]
         _check(_lib.kur_plan_sizes(h, _np_ptr(sz)))
         out.update(conflicts=int(sz[10]), slots_hot=int(sz[11]), idx_hot=int(sz[12]), slots_remote=int(sz[13]),
-                   idx_remote=int(sz[14]), window_loads=int(sz[15]), idx_cold=int(sz[16]), slots_cold=int(sz[17]),
-                   n_cold_parts=int(sz[18]), n_cold_groups=int(sz[19]))
+                   idx_remote=int(sz[14]), window_loads=int(sz[15]))
         tiles = np.zeros((max(nt, 1), 7), np.int32)
         _check(_lib.kur_plan_tiles(h, ctypes.c_void_p(tiles.ctypes.data), None))
         pw = np.zeros(max(int(tiles[:nt, 3].sum()), 1), np.int32)

@@ -241,7 +241,7 @@ def test_library_exports_every_declared_symbol():
 
 
 @pytest.mark.parametrize("world", [1, 3])
-def test_canonical_part_order(world, monkeypatch):
+def test_canonical_part_order(world):
     """per tile, the nown own-community hot windows first (each lying wholly inside
     the tile's community — local at any world size), then the other hot windows, then at most
     one remote part; the order does not depend on the partition into ranks."""
@@ -249,7 +249,6 @@ def test_canonical_part_order(world, monkeypatch):
     inst = kurgen.sbm(sizes, np.array(
         [[0.97, 0.002, 0.6, 0.0, 0.1], [0.002, 0.9, 0.0, 0.001, 0.0], [0.6, 0.0, 0.98, 0.0, 0.0],
          [0.0, 0.001, 0.0, 0.95, 0.02], [0.1, 0.0, 0.0, 0.02, 0.5]]), 31)
-    monkeypatch.setenv("KUR_NO_COLD", "1")  # keep the sparse windows in the remote part
     out = kur.plan_export(inst, world=world, rank=world - 1, tile_rows=512)
     off = np.concatenate([[0], np.cumsum(sizes)])
     k = 0
@@ -347,32 +346,3 @@ def test_split_community_plan_decodes():
                 if q < nloc:
                     assert inside
             assert nloc == nown or not (w[nloc] * 4096 >= rb and (w[nloc] + 1) * 4096 <= re_)
-
-
-def _cold_instance():
-    """4 communities of 2048 in random label order, dense inside (p 0.9), p_out 1e-3: a 256-row tile holds
-    ~1 K entries in the window of the other two communities -- below hot_min, above COLD_MIN: cold parts."""
-    rng = np.random.default_rng(5)
-    n = 8192
-    lab = np.repeat(np.arange(4), 2048)[rng.permutation(n)]
-    P = np.where(lab[:, None] == lab[None, :], 0.9, 0.001)
-    A = (rng.random((n, n)) < P).astype(np.uint8)
-    A = np.triu(A, 1)
-    A = A + A.T
-    return A, kurgen.from_dense(A, lab, kind="auto")
-
-
-def test_cold_parts_decode(monkeypatch):
-    """Cold parts (k_cold) hold the entries of windows with COLD_MIN..hot_min-1 entries of
-    a tile; the exported layout (hot + cold + remote) still decodes to A at world 1 and 2, conflict free,
-    and without cold parts the same entries are remote."""
-    A, inst = _cold_instance()
-    out = kur.plan_export(inst, tile_rows=256)
-    assert out["idx_cold"] > 0 and out["n_cold_parts"] > 0 and out["n_cold_groups"] > 0
-    assert out["conflicts"] == 0
-    check_plan(inst, A, tile_rows=256)
-    check_plan(inst, A, tile_rows=256, world=2)
-    monkeypatch.setenv("KUR_NO_COLD", "1")
-    off = kur.plan_export(inst, tile_rows=256)
-    assert off["idx_cold"] == 0 and off["idx_remote"] == out["idx_cold"] + out["idx_remote"]
-    assert off["idx_hot"] == out["idx_hot"]

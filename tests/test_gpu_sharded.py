@@ -193,50 +193,3 @@ def test_concurrent_inline_remote_bitwise(world, monkeypatch):
         else:
             ok, _ = _group_vs_single(inst, world, steps=4, remote_pass=rp, tile_rows=256)
             assert all(ok), (mode, rp, ok)
-
-
-def _cold_inst():
-    from tests.test_builder_host import _cold_instance
-    A, inst = _cold_instance()
-    inst.K, inst.h = 3.0, 0.01
-    return inst
-
-
-@pytest.mark.parametrize("world", [2, 3])
-def test_cold_parts_world_bitwise(world):
-    """Plans with cold parts (k_cold writes per-(part, row) partials, the finalize adds them in window
-    order): RHS, RK4 and Heun at world 2/3 bitwise equal to world 1 (k_cold runs in phase B)."""
-    inst = _cold_inst()
-    g = kur.graph_build(inst, tile_rows=256)
-    assert g.info["n_cold_parts"] > 0
-    g.close()
-    for method in ("rk4", "heun"):
-        ok, _ = _group_vs_single(inst, world, steps=4, method=method, tile_rows=256)
-        assert all(ok), (world, method, ok)
-
-
-def test_cold_parts_parity_with_oracle(monkeypatch):
-    """Cold and no-cold plans of the same graph both match the oracle (the cold partials change only the
-    order of additions); 10 RK4 steps and r(t)."""
-    inst = _cold_inst()
-    og = oracle.Graph(inst)
-    f_ref = oracle.rhs(og, inst.theta0, inst.omega, inst.K, mode="naive")
-    _, th10, rt_ref = oracle.rk4(og, inst.theta0, inst.omega, inst.K, inst.h, 10, 1, mode="matvec")
-    for cold in (True, False):
-        if cold:
-            monkeypatch.delenv("KUR_NO_COLD", raising=False)
-        else:
-            monkeypatch.setenv("KUR_NO_COLD", "1")
-        g = kur.graph_build(inst, tile_rows=256)
-        assert (g.info["n_cold_parts"] > 0) == cold
-        th = g.to_internal(torch.from_numpy(inst.theta0).cuda())
-        om = g.to_internal(torch.from_numpy(inst.omega).cuda())
-        f = g.to_user(kur.rhs(g, th, om, inst.K)).cpu().numpy()
-        ok, err = close(f, f_ref)
-        assert ok, (cold, err)
-        rt = kur.step(g, th, om, inst.K, inst.h, 10, 1).cpu().numpy()
-        ok, err = close(g.to_user(th).cpu().numpy(), th10)
-        assert ok, (cold, err)
-        d = np.abs(rt[:, 0] * np.exp(1j * rt[:, 1]) - rt_ref[:, 0] * np.exp(1j * rt_ref[:, 1]))
-        assert d.max() <= 1e-9
-        g.close()
