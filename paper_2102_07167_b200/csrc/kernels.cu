@@ -1718,6 +1718,9 @@ size_t persist_smem_bytes(const DevPlan& dp) {
 using PersistKernel = void (*)(const DevPlan, const StageArgs, double2*, unsigned long long*, long long,
                                unsigned long long);
 PersistKernel persist_kernel(const DevPlan& dp) {
+#ifdef KUR_PERSIST_R8
+  return k_persist_rk4<8>;
+#endif
   switch ((dp.rows_per_tile + NTHREADS - 1) / NTHREADS) {
     case 1: return k_persist_rk4<1>;
     case 2: return k_persist_rk4<2>;
