@@ -1717,18 +1717,15 @@ size_t persist_smem_bytes(const DevPlan& dp) {
 
 using PersistKernel = void (*)(const DevPlan, const StageArgs, double2*, unsigned long long*, long long,
                                unsigned long long);
+// R = 1..4 rows per thread compile without spills; above that the kernel spills a few bytes either
+// way and R = 8 measured faster than the exact R = 7 on config 2 (8.06 vs 8.19 us per stage,
+// profiles/r02/notes/persist_r7_r8.log)
 PersistKernel persist_kernel(const DevPlan& dp) {
-#ifdef KUR_PERSIST_R8
-  return k_persist_rk4<8>;
-#endif
   switch ((dp.rows_per_tile + NTHREADS - 1) / NTHREADS) {
     case 1: return k_persist_rk4<1>;
     case 2: return k_persist_rk4<2>;
     case 3: return k_persist_rk4<3>;
     case 4: return k_persist_rk4<4>;
-    case 5: return k_persist_rk4<5>;
-    case 6: return k_persist_rk4<6>;
-    case 7: return k_persist_rk4<7>;
     default: return k_persist_rk4<8>;
   }
 }
