@@ -327,14 +327,15 @@ kur_status kur_plan_tiles(const kur_plan *p, int32_t *tiles, int32_t *part_windo
 
 /* Per-launch timing for measurement (bench.py): while enabled, kur_step
  * records a CUDA event pair around every kernel it launches, on `stream`.
- * kur_timing_read blocks until the last recorded event, writes out[7] =
+ * kur_timing_read blocks until the last recorded event, writes out[9] =
  * {total ms of k_prologue launches, their count, total ms of k_stage (fused
  * RK stage) launches -- or of the single-launch trajectory kernels -- the RHS
  * evaluations they did, total ms of k_remote launches (remote-pass plans; one
- * per RHS evaluation), their count, the number of timed kernel launches} and
- * clears the record.  Enabling also clears it. */
+ * per RHS evaluation), their count, the number of timed kernel launches,
+ * world > 1: total ms of the phase-A k_stage launches (also in out[2]), their
+ * count} and clears the record.  Enabling also clears it. */
 kur_status kur_timing(kur_graph *g, int32_t enable);
-kur_status kur_timing_read(kur_graph *g, double *out /* [7] */);
+kur_status kur_timing_read(kur_graph *g, double *out /* [9] */);
 
 /* Creates a 128-byte NCCL unique id (rank 0), to be broadcast by the caller. */
 kur_status kur_nccl_unique_id(void *id128);

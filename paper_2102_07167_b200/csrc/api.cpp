@@ -82,6 +82,7 @@ struct kur_graph {
   cudaStream_t comm_stream = nullptr;         // NCCL: exchange + unpack + finish, overlapping phase A
   cudaEvent_t ev_b = nullptr, ev_exch = nullptr;
   bool exch_pending = false;                  // comm_stream holds an exchange the next phase B waits for
+  bool remote_on_xs = true;                   // world > 1: k_remote on the exchange stream (KUR_REMOTE_SEQ: A/B)
   // fused peer-store exchange (KUR_DIST_PEER_EXCHANGE)
   bool peer_req = false, peer_on = false;
   unsigned int* d_flag = nullptr;             // this rank's arrival counter (peers increment it)
@@ -278,6 +279,15 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
           (e = cudaMalloc((void**)&g->d_peer_flag, sizeof(unsigned int*) * (size_t)world)) != cudaSuccess)
         return bail(e, "peer exchange buffers");
     }
+    g->remote_on_xs = std::getenv("KUR_REMOTE_SEQ") == nullptr;
+    {
+      int lo = 0, hi = 0;  // the exchange stream gets the highest priority: its few CTAs jump the queue
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if ((e = cudaStreamCreateWithPriority(&g->comm_stream, cudaStreamNonBlocking, hi)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&g->ev_exch, cudaEventDisableTiming)) != cudaSuccess)
+        return bail(e, "exchange stream");
+    }
     if (dist && dist->nccl_id) {
       ncclUniqueId id;
       std::memcpy(&id, dist->nccl_id, sizeof(id));
@@ -286,12 +296,6 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
         delete g;
         return fail(KUR_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(nr));
       }
-      int lo = 0, hi = 0;  // the exchange stream gets the highest priority: its few CTAs jump the queue
-      cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      if ((e = cudaStreamCreateWithPriority(&g->comm_stream, cudaStreamNonBlocking, hi)) != cudaSuccess ||
-          (e = cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming)) != cudaSuccess ||
-          (e = cudaEventCreateWithFlags(&g->ev_exch, cudaEventDisableTiming)) != cudaSuccess)
-        return bail(e, "exchange stream");
       if (g->peer_req) {
         // map every rank's receive buffer and arrival counter into this process: CUDA IPC
         // handles all-gathered over NCCL; any failure keeps the all-gather exchange
@@ -617,11 +621,31 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
       KUR_CUDA(g->mark(s));
       KUR_CUDA(launch_stage(mode, g->dp, a, s));
       KUR_CUDA(g->mark(s));
-      if (g->timing) g->ev_kind.push_back({1, 0});
+      if (g->timing) g->ev_kind.push_back({3, 0});  // phase A (world > 1)
       a.phase = PHASE_B;
     }
+    // the remote pass of this stage needs the other ranks' z of the stage state, which the previous
+    // exchange unpacks on the exchange stream: queue it there too, so it runs concurrently with phase A
+    // (on the SMs phase A leaves free) instead of between phase A and phase B
+    kur_graph* g0 = gs[0];
+    if (g0->comm_stream && g0->remote_on_xs) {
+      bool pre = false;
+      for (size_t r = 0; r < gs.size(); ++r)
+        if (gs[r]->dp.has_remote && !gs[r]->dp.remote_warp) {
+          KUR_CUDA(gs[r]->mark(g0->comm_stream));
+          KUR_CUDA(launch_remote(gs[r]->dp, args[r].zin, g0->comm_stream));
+          KUR_CUDA(gs[r]->mark(g0->comm_stream));
+          if (gs[r]->timing) gs[r]->ev_kind.push_back({2, 1});
+          args[r].no_remote = 1;
+          pre = true;
+        }
+      if (pre) {
+        KUR_CUDA(cudaEventRecord(g0->ev_exch, g0->comm_stream));
+        g0->exch_pending = true;
+      }
+    }
     for (kur_graph* g : gs)
-      if (g->exch_pending) {  // phase B needs the other ranks' z and the new block sums
+      if (g->exch_pending) {  // phase B needs the other ranks' z, the new block sums and Wr
         KUR_CUDA(cudaStreamWaitEvent(s, g->ev_exch, 0));
         g->exch_pending = false;
       }
@@ -629,7 +653,7 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
   for (size_t r = 0; r < gs.size(); ++r) {
     kur_graph* g = gs[r];
     StageArgs& a = args[r];
-    if (g->timing && mode != PH_PROLOGUE && g->dp.has_remote && !g->dp.remote_warp) {  // time k_remote, k_stage apart
+    if (g->timing && mode != PH_PROLOGUE && g->dp.has_remote && !g->dp.remote_warp && !a.no_remote) {  // time apart
       KUR_CUDA(g->mark(s));
       KUR_CUDA(launch_remote(g->dp, a.zin, s));
       KUR_CUDA(g->mark(s));
@@ -644,9 +668,10 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
   }
   if (world == 1 || mode == MODE_RHS) return KUR_OK;
   kur_graph* g0 = gs[0];
-  // NCCL: the exchange, unpack and fixed-order finish run on the exchange stream, so the next
-  // phase A overlaps them; the prologue (no phase A follows it on its own) is joined at once.
-  const bool async = g0->comm != nullptr;
+  // The exchange, unpack and fixed-order finish run on the exchange stream (NCCL ranks and in-process
+  // groups alike), so the next phase A overlaps them; the prologue (no phase A follows it on its own)
+  // is joined at once.
+  const bool async = g0->comm_stream != nullptr;
   cudaStream_t xs = async ? g0->comm_stream : s;
   if (async) {
     KUR_CUDA(cudaEventRecord(g0->ev_b, s));
@@ -1150,8 +1175,8 @@ kur_status kur_timing(kur_graph* g, int32_t enable) {
 kur_status kur_timing_read(kur_graph* g, double* out) {
   if (!g || !out) return fail(KUR_ERR_INVALID_ARG, "NULL argument");
   KUR_CUDA(cudaSetDevice(g->device));
-  double ms[3] = {0.0, 0.0, 0.0};
-  int64_t cnt[3] = {0, 0, 0};
+  double ms[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t cnt[4] = {0, 0, 0, 0};
   for (size_t i = 0; i < g->ev_kind.size(); ++i) {
     float t = 0.f;
     KUR_CUDA(cudaEventSynchronize(g->ev[2 * i + 1]));
@@ -1166,6 +1191,9 @@ kur_status kur_timing_read(kur_graph* g, double* out) {
   out[4] = ms[2];
   out[5] = (double)cnt[2];
   out[6] = (double)g->ev_kind.size();
+  out[7] = ms[3];  // world > 1: phase-A k_stage launches (own-community windows), included in out[2]
+  out[8] = (double)cnt[3];
+  out[2] += ms[3];
   g->ev_used = 0;
   g->ev_kind.clear();
   return KUR_OK;

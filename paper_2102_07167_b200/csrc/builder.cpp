@@ -916,7 +916,10 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   // config 5 (42 M remote slots, 20 K per tile) 1.226 -> 1.181 ms with the pass;
   // config 4 (7.7 M, 7 K per tile) 0.312 -> 0.350 ms and config 3 (4.3 M, 17 K per
   // tile, 44 us stage) 0.044 -> 0.049 ms, so those stay inline.
-  P.split_remote = !P.small && P.n_slots_remote >= (16LL << 20) && nt > 0 && P.n_slots_remote / nt >= 8192;
+  // (the count threshold applies to the whole graph -- this rank's slots x world -- so a sharded config
+  // 5 keeps the pass, which at world > 1 runs on the exchange stream concurrently with phase A; the
+  // per-tile threshold does not depend on the world size.  Either way the bits are the same.)
+  P.split_remote = !P.small && P.n_slots_remote * world >= (16LL << 20) && nt > 0 && P.n_slots_remote / nt >= 8192;
   if (force_split) P.split_remote = !P.small && force_split == 1;
 #pragma omp parallel for schedule(dynamic, 4)
   for (int32_t lt = 0; lt < nt; ++lt) {

@@ -343,10 +343,11 @@ def timing(g: Graph, enable: bool):
 def timing_read(g: Graph):
     """dict(prologue_ms, prologue_n, stage_ms, stage_n, remote_ms, remote_n, launches) of the launches
     recorded since enabling (stage = k_stage or a single-launch trajectory kernel, remote = k_remote)."""
-    out = np.zeros(7, np.float64)
+    out = np.zeros(9, np.float64)
     _check(_lib.kur_timing_read(g._h, _np_ptr(out)))
     return dict(prologue_ms=float(out[0]), prologue_n=int(out[1]), stage_ms=float(out[2]), stage_n=int(out[3]),
-                remote_ms=float(out[4]), remote_n=int(out[5]), launches=int(out[6]))
+                remote_ms=float(out[4]), remote_n=int(out[5]), launches=int(out[6]), phase_a_ms=float(out[7]),
+                phase_a_n=int(out[8]))
 
 
 def _ptr_array(ptrs):
