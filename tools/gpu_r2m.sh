@@ -1,7 +1,7 @@
 # final-state validation: full GPU suite, smoke, bench lines for every config, ncu captures (cfg2 persist,
 # cfg3 k_stage CR variant), launch lists cfg3
-mkdir -p gpurun_out/r2m
-O=gpurun_out/r2m
+mkdir -p gpurun_out/r2w
+O=gpurun_out/r2w
 timeout 2700 python -m pytest tests -q -m gpu > $O/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke=$?; tail -1 $O/smoke.log
 python bench.py --steps 20 --warmup 5 > $O/bench_default.json 2> $O/bench_default.err; echo default=$?
