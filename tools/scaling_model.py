@@ -41,11 +41,12 @@ def main():
     ap.add_argument("--worlds", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--remote-pass", default="auto", choices=["auto", "on", "off"])
+    ap.add_argument("--tile-rows", type=int, default=0)
     args = ap.parse_args()
     rp = {"auto": None, "on": True, "off": False}[args.remote_pass]
     inst = kurgen.config(args.config)
     dev = "cuda:0"
-    g1 = kur.graph_build(inst)
+    g1 = kur.graph_build(inst, tile_rows=args.tile_rows)
     th = g1.to_internal(torch.from_numpy(inst.theta0).to(dev))
     om = g1.to_internal(torch.from_numpy(inst.omega).to(dev))
     a = th.clone()
@@ -58,7 +59,7 @@ def main():
     g1.close()
     out = {"config": inst.name, "T1_stage_ms": T1, "worlds": []}
     for G in args.worlds:
-        gs = kur.group_build(inst, G, remote_pass=rp)
+        gs = kur.group_build(inst, G, remote_pass=rp, tile_rows=args.tile_rows)
         ths = [th[g.row_begin:g.row_end].clone() for g in gs]
         oms = [om[g.row_begin:g.row_end].clone() for g in gs]
         kur.group_step(gs, ths, oms, inst.K, inst.h, 2)
