@@ -101,6 +101,12 @@ struct kur_graph {
   unsigned long long* gbar = nullptr; // persist: monotonic arrival counter
   unsigned long long persist_q = 0;   // persist: publications so far
   int32_t* d_big = nullptr;           // communities of > 64 tiles
+  // deferred block sums (world 1): the inner stages of a step skip the last-CTA reduction, the next
+  // stage forms its T from their tile partials (StageArgs::no_finish / plazy); partial and partialB
+  // alternate as the destination so a stage never overwrites the partials it reads
+  bool lazy_ok = false;
+  double2* partialB = nullptr;
+  const double2* lazy_prev = nullptr;  // partials of the previous stage if it skipped its reduction
   size_t ev_used = 0;
   cudaError_t mark(cudaStream_t s) {  // records the next event of the pool on s
     if (!timing) return cudaSuccess;
@@ -118,7 +124,7 @@ struct kur_graph {
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
                     xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh, d_rchunks, d_rem_lp, d_flag, d_xticket,
-                    d_peer_x, d_peer_flag, theta_ws, omega_ws, pbuf, gbar, d_big};
+                    d_peer_x, d_peer_flag, theta_ws, omega_ws, pbuf, gbar, d_big, partialB};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -243,6 +249,8 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   const int32_t ntiles_all = P.comm_tile0[(size_t)P.C];
   if ((e = cudaMalloc((void**)&g->partial, sizeof(double2) * (size_t)std::max<int32_t>(ntiles_all, 1))) != cudaSuccess)
     return bail(e, "partial");
+  if ((e = cudaMalloc((void**)&g->partialB, sizeof(double2) * (size_t)std::max<int32_t>(ntiles_all, 1))) != cudaSuccess)
+    return bail(e, "partialB");
   if ((e = cudaMalloc((void**)&g->pmax, sizeof(double) * (size_t)std::max<int32_t>(ntiles_all, 1))) != cudaSuccess)
     return bail(e, "pmax");
   if ((e = cudaMalloc((void**)&g->acc, sizeof(double) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess)
@@ -434,6 +442,12 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
     dp.big_comm = g->d_big;
     dp.n_big = (int32_t)big.size();
   }
+  // deferred block sums: world 1 and no block-reduced community (lazy_T_warp sums S_b sequentially);
+  // KUR_LAZY_T=0 keeps the last-CTA reduction after every stage (A/B switch)
+  {
+    const char* lz = std::getenv("KUR_LAZY_T");
+    g->lazy_ok = world == 1 && dp.n_big == 0 && !(lz && lz[0] == '0');
+  }
   dp.shard_row0 = g->d_shard_row0;
   dp.shard_tile0 = g->d_shard_tile0;
   dp.xrows = xrows;
@@ -610,6 +624,19 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
     a.Wh = g->Wh;
     a.xpar = (int)((g->xepoch + 1) & 1u);  // parity of the exchange this phase produces
     a.theta_host = (mode == MODE_S4 || mode == MODE_E1 || mode == MODE_H2) ? g->host_out : nullptr;
+    // deferred block sums (world 1): RK4 S1-S3 and Heun H1 leave the reduction to the next stage,
+    // which reads their partials; the destination alternates so no stage overwrites what it reads
+    if (mode == PH_PROLOGUE || !g->lazy_ok) {
+      g->lazy_prev = nullptr;
+    } else {
+      const bool defer = record == REC_NONE &&
+                         (mode == MODE_S1 || mode == MODE_S2 || mode == MODE_S3 || mode == MODE_H1);
+      const bool takes = mode == MODE_S2 || mode == MODE_S3 || mode == MODE_S4 || mode == MODE_H2;
+      a.plazy = takes ? g->lazy_prev : nullptr;
+      if (defer || a.plazy) a.pout = a.plazy == g->partialB ? g->partial : g->partialB;
+      a.no_finish = defer ? 1 : 0;
+      g->lazy_prev = defer ? a.pout : nullptr;
+    }
   }
   if (world > 1 && mode != PH_PROLOGUE) {
     // phase A: own-community hot parts (local z only) -> Wh, while the previous stage's

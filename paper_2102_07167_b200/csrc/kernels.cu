@@ -636,6 +636,30 @@ __device__ __forceinline__ double2 seq_sum_partials(const double2* v, int t0, in
   return make_double2(x, y);
 }
 
+// Deferred block sums (world 1, plans without communities of > 64 tiles): T_c of community c from
+// the previous stage's tile partials P, by ONE warp, in finish_reduce's exact summation order --
+// S_b = 0 + P[t0] + ... + P[t1-1] (seq_sum_partials, one lane per b in D(c)), then
+// T_c = 0 + S_{D[0]} + S_{D[1]} + ... -- so the bits equal the last-CTA reduction's.
+// Replaces the last CTA's reduction after the inner stages of a step: every CTA forms the one T it
+// needs while its first window is in flight, instead of one CTA reducing all C after all tiles.
+__device__ __forceinline__ void lazy_T_warp(const DevPlan& dp, const double2* P, int c, int lane, double2* out) {
+  const int d0 = dp.D_ptr[c], d1 = dp.D_ptr[c + 1];
+  double tx = 0.0, ty = 0.0;
+  for (int base = d0; base < d1; base += 32) {
+    double2 sb = make_double2(0.0, 0.0);
+    if (base + lane < d1) {
+      const int b = dp.D_idx[base + lane];
+      sb = seq_sum_partials(P, dp.comm_tile0[b], dp.comm_tile0[b + 1]);
+    }
+    const int nb = min(32, d1 - base);
+    for (int i = 0; i < nb; ++i) {
+      tx += __shfl_sync(0xffffffffu, sb.x, i);
+      ty += __shfl_sync(0xffffffffu, sb.y, i);
+    }
+  }
+  if (lane == 0) *out = make_double2(tx, ty);
+}
+
 // Executed by every thread of the LAST CTA of a grid: S_b from the per-tile
 // partials, T_a, the order parameter and its recording.
 // S_sh: shared scratch of >= C entries for the block sums (k_stage's free window buffer), or NULL:
@@ -643,12 +667,13 @@ __device__ __forceinline__ double2 seq_sum_partials(const double2* v, int t0, in
 __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a, double2* S_sh = nullptr) {
   __shared__ double2 fred[NWARPS];
   double2* const Sd = S_sh ? S_sh : dp.S;
+  const double2* const Pt = a.pout ? a.pout : dp.partial;  // this grid's tile partials
   const int tid = threadIdx.x;
   constexpr int BIG = 64;  // communities with more tiles are reduced by the whole CTA
   if (a.v_out) {  // kur_potential: V = sum of the tile partials in tile order (fixed shape)
     double x = 0.0, y = 0.0;
     const int nt = dp.comm_tile0[dp.C];
-    for (int t = tid; t < nt; t += NTHREADS) x += __ldcg(dp.partial + t).x;
+    for (int t = tid; t < nt; t += NTHREADS) x += __ldcg(Pt + t).x;
     block_sum2(x, y, fred);
     if (tid == 0) a.v_out[0] = x;
     return;
@@ -668,14 +693,14 @@ __device__ void finish_reduce(const DevPlan& dp, const StageArgs& a, double2* S_
   for (int c = tid; c < dp.C; c += NTHREADS) {
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
     if (t1 - t0 > BIG) continue;
-    Sd[c] = seq_sum_partials(dp.partial, t0, t1);
+    Sd[c] = seq_sum_partials(Pt, t0, t1);
   }
   for (int i = 0; i < dp.n_big; ++i) {  // communities of > BIG tiles (uniform): fixed-shape block reduction
     const int c = dp.big_comm[i];
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
     double x = 0.0, y = 0.0;
     for (int t = t0 + tid; t < t1; t += NTHREADS) {
-      const double2 v = __ldcg(dp.partial + t);
+      const double2 v = __ldcg(Pt + t);
       x += v.x;
       y += v.y;
     }
@@ -750,7 +775,7 @@ __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const
   }
   block_sum2(x, y, red);
   if (threadIdx.x == 0) {
-    dp.partial[dp.tile_base + lt] = make_double2(x, y);
+    (a.pout ? a.pout : dp.partial)[dp.tile_base + lt] = make_double2(x, y);
     if (a.fp_check) dp.pmax[dp.tile_base + lt] = dmax;
     if (a.xsend) {
       xput(dp, a, dp.xrows + 3 * lt, x);
@@ -758,7 +783,8 @@ __device__ __forceinline__ void tile_partial_and_finish(const DevPlan& dp, const
       xput(dp, a, dp.xrows + 3 * lt + 2, dmax);
     }
     s_last = false;
-    if (dp.world == 1) {  // world > 1: the reduction runs after the exchange
+    if (dp.world == 1 && !a.no_finish) {  // world > 1: the reduction runs after the exchange;
+      // no_finish: the next stage forms its block sums from these partials itself (lazy_T_warp)
       __threadfence();
       const unsigned int t = atomicAdd(&dp.ctrl->ticket, 1u);
       s_last = (t == gridDim.x - 1);
@@ -813,7 +839,7 @@ template <int MODE, bool SMALL, bool RW = false, bool CR = false>
 __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a, const TileDesc& T, double2* zs,
                                            double2* Ws, uint64_t* bar, uint32_t& phase, double& px, double& py,
                                            double& dmax, double2* ring = nullptr, uint64_t* rbar = nullptr,
-                                           const CUtensorMap* tmz = nullptr) {
+                                           const CUtensorMap* tmz = nullptr, double2* s_T = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool parts = dp.has_parts;
   // the remote part of the tile was summed by k_remote into Wr (added in the finalize);
@@ -878,6 +904,8 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
     pending = true;
     if (tid == 0) tma_load_1d(zs, a.zin + (size_t)loaded * WZ, WZ * sizeof(double2), bar);
   }
+  // deferred block sums: warp 0 forms T of the tile's community while the first window is in flight
+  if (!SMALL && a.plazy && warp == 0) lazy_T_warp(dp, a.plazy, T.comm, lane, s_T);
   for (int pi = pbeg; pi < pend_h; ++pi) {
     const int p = T.part0 + pi;
     const PartDesc P = dp.parts[p];
@@ -908,6 +936,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   }
   if (named) __syncthreads();  // joins the remote warp(s)
   }
+  if (!SMALL && a.plazy) __syncthreads();  // s_T visible (tiles without parts have no barrier above)
   if (!SMALL) PROF_T(25);
   if (!SMALL && a.phase == PHASE_A) {  // hand the own-community sums to phase B
     for (int r = tid; r < T.nrows; r += NTHREADS) a.Wh[(T.row0 - dp.row_begin) + r] = Ws[r];
@@ -916,7 +945,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   }
 
   // ---- finalize: k_j = omega_j + (K/N) Im(conj z_j W_j), fused RK4 stage
-  const double2 Tc = __ldcg(a.Tin + T.comm);
+  const double2 Tc = (!SMALL && a.plazy) ? *s_T : __ldcg(a.Tin + T.comm);
   px = 0.0;
   py = 0.0;
   dmax = 0.0;
@@ -1092,6 +1121,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __shared__ __align__(8) uint64_t bar;
   __shared__ __align__(8) uint64_t rbar[RING_SLOTS];
   __shared__ int s_nonfinite;
+  __shared__ double2 s_T;  // deferred block sums: T of the tile's community
   const int tid = threadIdx.x;
   pdl_wait_and_release();
   PROF_G(160);
@@ -1121,7 +1151,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __syncthreads();
   uint32_t phase = 0;
   double px, py, dmax;
-  const bool bad = stage_rows<MODE, false, RW, CR>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax, ring, rbar, &tmz);
+  const bool bad =
+      stage_rows<MODE, false, RW, CR>(dp, a, T, zs, Ws, &bar, phase, px, py, dmax, ring, rbar, &tmz, &s_T);
   if (MODE == MODE_RHS || a.phase == PHASE_A) return;
   constexpr bool FINAL = MODE == MODE_S4 || MODE == MODE_E1 || MODE == MODE_H2;
   if (FINAL && bad) s_nonfinite = 1;

@@ -119,6 +119,13 @@ struct StageArgs {
   double* theta_host;     // final stages (S4, E1, H2): theta_{n+1} also stored here -- the device
                           // mapping of the caller's pinned host buffer (end-to-end path: the
                           // device-to-host copy rides on the stage) -- or NULL
+  // Deferred block sums (world 1, inner stages of a step): a stage launched with no_finish writes
+  // its tile partials to pout and skips the last-CTA reduction; the next stage (plazy = those
+  // partials) forms S_b and T_{c} of its own tile's community at its start, in finish_reduce's
+  // exact summation order, instead of reading Tin.  pout NULL = dp.partial.
+  double2* pout;
+  const double2* plazy;
+  int no_finish;
 };
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
