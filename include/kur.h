@@ -99,12 +99,7 @@ typedef struct {
   int32_t flags;            /* tuning / tests, 0 = automatic: low 16 bits a forced tile size in rows
                                (a multiple of 32 in [32, 2048]); | KUR_FLAG_REMOTE_PASS or
                                | KUR_FLAG_REMOTE_INLINE forces where the remote (global-gather)
-                               entries are summed: a separate pass before each stage, or inline;
-                               | KUR_FLAG_TILE_MODE keeps the tile plan where the cluster-resident
-                               stage would be chosen (world 1, n <= 65536, stored entries: all of z
-                               staged over one 8-CTA cluster) -- that plan sums in
-                               another order, so only tile plans are bitwise equal across world
-                               sizes */
+                               entries are summed: a separate pass before each stage, or inline */
   int32_t scaling;          /* KUR_SCALING_UNIFORM: M_m = N (the north_star model), or
                                KUR_SCALING_DEGREE: M_m = sum_l A_ml (a zero row gives
                                theta_m' = omega_m).  The degree counts the off-diagonal
@@ -114,7 +109,7 @@ typedef struct {
 } kur_graph_desc;
 
 enum { KUR_SCALING_UNIFORM = 0, KUR_SCALING_DEGREE = 1 };
-enum { KUR_FLAG_REMOTE_PASS = 1 << 16, KUR_FLAG_REMOTE_INLINE = 2 << 16, KUR_FLAG_TILE_MODE = 4 << 16 };
+enum { KUR_FLAG_REMOTE_PASS = 1 << 16, KUR_FLAG_REMOTE_INLINE = 2 << 16 };
 
 /* Multi-GPU placement: contiguous ranges of whole communities per rank,
  * balanced by stored-entry count (every rank computes the same split).
@@ -161,9 +156,6 @@ typedef struct {
   int32_t remote_pass;         /* 1: remote entries summed by the separate k_remote pass before each
                                   stage kernel (2 launches per RHS), 0: inline */
   int32_t peer_exchange;       /* world > 1: 1 = fused peer-store exchange active, 0 = all-gather */
-  int32_t cluster_plan;        /* > 0: the cluster-resident stage with this many 8-CTA clusters (world 1,
-                                  n <= 65536, stored entries); 0: tile plan */
-  int32_t reserved_info;
 } kur_graph_info_t;
 
 typedef struct kur_graph kur_graph; /* opaque; owns all device data and workspace */
@@ -322,12 +314,6 @@ kur_status kur_check(kur_graph *g, void *stream);
 typedef struct kur_plan kur_plan;
 kur_status kur_plan_build(const kur_graph_desc *desc, int32_t rank, int32_t world, int32_t sm_count,
                           kur_plan **out);
-/* As kur_plan_build, with the cluster-resident layout when the plan qualifies (world 1,
- * n <= 65536, stored entries, no KUR_FLAG_TILE_MODE): `clusters` 8-CTA clusters (what
- * kur_graph_build uses is kur_graph_info.cluster_plan); 0 = tile plan.  kur_plan_export decodes
- * either layout. */
-kur_status kur_plan_build_cz(const kur_graph_desc *desc, int32_t rank, int32_t world, int32_t sm_count,
-                             int32_t clusters, kur_plan **out);
 kur_status kur_plan_sizes(const kur_plan *p, int64_t *sizes /* [16] */);
 kur_status kur_plan_export(const kur_plan *p, int32_t *perm, int32_t *D_ptr, int32_t *D_idx, int64_t *row_ptr,
                            int32_t *cols, int8_t *neg, int32_t *shard_row0);

@@ -101,8 +101,6 @@ struct kur_graph {
   unsigned long long* gbar = nullptr; // persist: monotonic arrival counter
   unsigned long long persist_q = 0;   // persist: publications so far
   int32_t* d_big = nullptr;           // communities of > 64 tiles
-  CzUnit* d_cz_units = nullptr;       // cluster-resident stage
-  int32_t *d_cz_ft = nullptr, *d_cz_tlro = nullptr;
   // deferred block sums (world 1): the inner stages of a step skip the last-CTA reduction, the next
   // stage forms its T from their tile partials (StageArgs::no_finish / plazy); partial and partialB
   // alternate as the destination so a stage never overwrites the partials it reads
@@ -126,8 +124,7 @@ struct kur_graph {
     void* ptrs[] = {d_tiles, d_order, d_parts, d_chunks, d_pool, d_comm_tile0, d_D_ptr, d_D_idx,
                     d_csize, d_perm, zA, zB, TA, TB, S, partial, acc, ctrl, d_shard_row0, d_shard_tile0,
                     xsend, xrecv, d_rowscale, d_potc, pmax, Wr, Wh, d_rchunks, d_rem_lp, d_flag, d_xticket,
-                    d_peer_x, d_peer_flag, theta_ws, omega_ws, pbuf, gbar, d_big, partialB, d_cz_units,
-                    d_cz_ft, d_cz_tlro};
+                    d_peer_x, d_peer_flag, theta_ws, omega_ws, pbuf, gbar, d_big, partialB};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -193,11 +190,7 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   std::string err;
   kur_status st;
   try {
-    // cluster-resident stage (world 1, small graphs with stored entries): the clusters that fit at
-    // once; KUR_CZ=0 keeps the tile plan (A/B switch)
-    const char* czv = std::getenv("KUR_CZ");
-    const int czc = (world == 1 && !(czv && czv[0] == '0')) ? cz_max_clusters() : 0;
-    st = build_plan(desc, rank, world, sm, P, err, czc);
+    st = build_plan(desc, rank, world, sm, P, err);
   } catch (const std::bad_alloc&) {
     return fail(KUR_ERR_OOM, "host allocation failed in kur_graph_build");
   }
@@ -384,22 +377,6 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
     if (T.nparts > 0) dp.has_parts = 1;
     if (T.nparts > T.nhot && P.split_remote) dp.has_remote = 1;
   }
-  dp.cz = 0;
-  if (P.cz) {  // cluster-resident stage: the parts belong to the cluster units
-    dp.has_parts = 1;
-    if ((e = upload(&g->d_cz_units, P.cz_units)) != cudaSuccess) return bail(e, "cluster units");
-    if ((e = upload(&g->d_cz_ft, P.cz_ft)) != cudaSuccess) return bail(e, "cluster finalize tiles");
-    if ((e = upload(&g->d_cz_tlro, P.cz_tlro)) != cudaSuccess) return bail(e, "cluster tile rows");
-    dp.cz = P.cz;
-    dp.cz_rmax = P.cz_rmax;
-    dp.cz_units = g->d_cz_units;
-    dp.cz_ft = g->d_cz_ft;
-    dp.cz_tlro = g->d_cz_tlro;
-    const char* dbg = std::getenv("KUR_CZ_DBG");
-    dp.cz_dbg = dbg ? std::atoi(dbg) : 0;
-    const char* czt = std::getenv("KUR_CZ_THREADS");
-    dp.cz_threads = (czt && std::atoi(czt) == 1024) ? 1024 : NTHREADS;
-  }
   if (dp.has_remote) {  // rows without remote entries keep Wr = 0 for good
     if ((e = cudaMalloc((void**)&g->Wr, sizeof(double2) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess ||
         (e = cudaMemset(g->Wr, 0, sizeof(double2) * (size_t)std::max<int64_t>(g->n_local, 1))) != cudaSuccess)
@@ -527,7 +504,6 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   I.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   I.remote_pass = dp.has_remote;
   I.peer_exchange = g->peer_on ? 1 : 0;
-  I.cluster_plan = P.cz;
   *out = g;
   return KUR_OK;
 }
@@ -1279,11 +1255,6 @@ extern "C" {
 
 kur_status kur_plan_build(const kur_graph_desc* desc, int32_t rank, int32_t world, int32_t sm_count,
                           kur_plan** out) {
-  return kur_plan_build_cz(desc, rank, world, sm_count, 0, out);
-}
-
-kur_status kur_plan_build_cz(const kur_graph_desc* desc, int32_t rank, int32_t world, int32_t sm_count,
-                             int32_t clusters, kur_plan** out) {
   if (!out) return fail(KUR_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   kur_plan* p = new (std::nothrow) kur_plan();
@@ -1291,7 +1262,7 @@ kur_status kur_plan_build_cz(const kur_graph_desc* desc, int32_t rank, int32_t w
   std::string err;
   kur_status st;
   try {
-    st = build_plan(desc, rank, world, sm_count > 0 ? sm_count : 148, p->P, err, std::max(clusters, 0));
+    st = build_plan(desc, rank, world, sm_count > 0 ? sm_count : 148, p->P, err);
   } catch (const std::bad_alloc&) {
     delete p;
     return fail(KUR_ERR_OOM, "host allocation failed in kur_plan_build");
@@ -1360,43 +1331,7 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
     const uint16_t* t16 = reinterpret_cast<const uint16_t*>(&P.pool[(size_t)cd.ofs + HDR_UNITS + (size_t)G * 32]);
     return t16[(size_t)l * 4 + (pos - 9 * G)];
   };
-  // decode units: the tiles (local row = row - tile row0), or -- cluster-resident plans -- the
-  // cluster units (cluster-local rows: the cluster's tiles in tile order, plan.h CzUnit)
-  struct DU { int32_t part0, nparts, nhot, nrows; std::vector<int32_t> rows; };
-  std::vector<DU> dus;
-  if (P.cz) {
-    std::vector<std::vector<int32_t>> crow((size_t)P.cz);
-    for (size_t t = 0; t < P.tiles.size(); ++t) {
-      std::vector<int32_t>& cr = crow[(size_t)P.cz_tcl[t]];
-      if ((int32_t)cr.size() != P.cz_tlro[t]) return fail(KUR_ERR_INVALID_ARG, "plan: cluster row offsets");
-      for (int32_t r = 0; r < P.tiles[t].nrows; ++r) cr.push_back(P.tiles[t].row0 + r);
-    }
-    for (size_t u = 0; u < P.cz_units.size(); ++u) {
-      const CzUnit& U = P.cz_units[u];
-      if (U.nrows != (int32_t)crow[u / CZ_CL].size()) return fail(KUR_ERR_INVALID_ARG, "plan: cluster rows");
-      for (int q = 0; q < U.nparts; ++q) {
-        const int32_t w = P.parts[(size_t)(U.part0 + q)].window;
-        if (w < 0 || (w != U.w0 && w != U.w1)) return fail(KUR_ERR_INVALID_ARG, "plan: cluster part window");
-      }
-      dus.push_back(DU{U.part0, U.nparts, U.nparts, U.nrows, crow[u / CZ_CL]});
-    }
-    // every tile is finalized by exactly one CTA of its cluster
-    std::vector<int> fin(P.tiles.size(), 0);
-    for (size_t u = 0; u < P.cz_units.size(); ++u)
-      for (int32_t i = 0; i < P.cz_units[u].nft; ++i) {
-        const int32_t t = P.cz_ft[(size_t)(P.cz_units[u].ft0 + i)];
-        if (P.cz_tcl[(size_t)t] != (int32_t)(u / CZ_CL)) return fail(KUR_ERR_INVALID_ARG, "plan: finalize tile");
-        fin[(size_t)t]++;
-      }
-    for (int f : fin)
-      if (f != 1) return fail(KUR_ERR_INVALID_ARG, "plan: finalize tiles");
-  }
   for (const TileDesc& T : P.tiles) {
-    std::vector<int32_t> rows((size_t)T.nrows);
-    for (int32_t r = 0; r < T.nrows; ++r) rows[(size_t)r] = T.row0 + r;
-    if (T.nparts > 0 || !P.cz) dus.push_back(DU{T.part0, T.nparts, T.nhot, T.nrows, std::move(rows)});
-  }
-  for (const DU& T : dus) {
     for (int pi = T.part0; pi < T.part0 + T.nparts; ++pi) {
       const PartDesc& pd = P.parts[(size_t)pi];
       const bool hot = pd.window >= 0;
@@ -1432,7 +1367,7 @@ kur_status kur_plan_export(const kur_plan* p, int32_t* perm, int32_t* D_ptr, int
               }
               if (lr == EMPTY_LANE) return fail(KUR_ERR_INVALID_ARG, "plan: entry in an empty lane");
               if (col < 0 || col >= P.n) return fail(KUR_ERR_INVALID_ARG, "plan: column out of range");
-              ents.push_back(E{(int32_t)(T.rows[lr] - P.row_begin), (int32_t)col, eneg});
+              ents.push_back(E{(int32_t)(T.row0 + lr - P.row_begin), (int32_t)col, eneg});
             }
           }
         }

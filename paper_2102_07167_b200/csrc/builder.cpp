@@ -326,7 +326,7 @@ void schedule_quarter(std::vector<uint16_t> (&lst)[8][8], std::vector<uint32_t>&
 }  // namespace
 
 kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int sm_count,
-                      HostPlan& P, std::string& err, int cz_clusters) {
+                      HostPlan& P, std::string& err) {
   // ------------------------------------------------------------ 1. validate
   if (!d || d->n < 1 || d->n_comm < 1 || !d->community || !d->seg_ptr || !d->idx_ptr) {
     err = "kur_graph_desc: n >= 1, n_comm >= 1 and non-NULL community/seg_ptr/idx_ptr required";
@@ -341,7 +341,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   const int force_rows = d->flags & 0xFFFF;
   const int force_split = (d->flags >> 16) & 3;  // KUR_FLAG_REMOTE_PASS (1) / KUR_FLAG_REMOTE_INLINE (2)
   if ((force_rows != 0 && (force_rows < 32 || force_rows > MAX_TILE_ROWS || force_rows % 32 != 0)) ||
-      (d->flags >> 19) != 0 || force_split == 3) {
+      (d->flags >> 18) != 0 || force_split == 3) {
     err = "flags: 0 or a tile size in rows (multiple of 32 in [32, 2048]), optionally | KUR_FLAG_REMOTE_PASS "
           "or | KUR_FLAG_REMOTE_INLINE";
     return KUR_ERR_INVALID_ARG;
@@ -544,59 +544,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   // 25.7 -> 21.5 us per stage with 2048- instead of 1024-row tiles, see the commit for 4096)
   // Their tile is sized so the tiles fill exactly one wave of 2 CTAs per SM (config 2: 296
   // tiles of 3552 rows instead of 256 of 4096, which left 40 SMs with one CTA).
-  // Cluster-resident stage (plan.h): each community is cut into (at most) one slice per cluster,
-  // cluster k takes one slice of every community (round robin), so the entries of its rows spread
-  // over all windows -- every CTA of the cluster owns ~1/CZ_CL of them.
-  const bool tile_mode = (d->flags >> 18) & 1;  // KUR_FLAG_TILE_MODE
-  std::vector<TileDesc> all;
-  P.comm_tile0.assign((size_t)C + 1, 0);
-  if (cz_clusters > 0 && world == 1 && !P.small && total_len > 0 && n <= CZ_MAX_N && !force_rows && !tile_mode) {
-    const int32_t K = cz_clusters;
-    std::vector<int64_t> crows((size_t)K, 0);
-    std::vector<int32_t> tcl;
-    int32_t base = 0, rmax = 0;
-    for (int32_t c = 0; c < C; ++c) {
-      P.comm_tile0[(size_t)c] = (int32_t)all.size();
-      const int64_t sz = S.csize[(size_t)c];
-      const int64_t ns = sz == 0 ? 0 : std::min<int64_t>(K, std::max<int64_t>(1, sz / 32));
-      for (int64_t i = 0; i < ns; ++i) {
-        TileDesc t{};
-        t.row0 = (int32_t)(S.moff[(size_t)c] + sz * i / ns);
-        t.nrows = (int32_t)(S.moff[(size_t)c] + sz * (i + 1) / ns - t.row0);
-        t.comm = c;
-        const int32_t k = (int32_t)((base + i) % K);
-        crows[(size_t)k] += t.nrows;
-        rmax = std::max(rmax, t.nrows);
-        all.push_back(t);
-        tcl.push_back(k);
-      }
-      base = (int32_t)((base + ns) % K);
-    }
-    P.comm_tile0[(size_t)C] = (int32_t)all.size();
-    const int64_t cmax = *std::max_element(crows.begin(), crows.end());
-    // the cluster's i-th tile is finalized by its CTA i mod CZ_CL: rows and tiles per CTA bounded
-    // (the CTA stages its finalize rows' partials in a window buffer: <= WZ rows)
-    std::vector<int64_t> frows((size_t)K * CZ_CL, 0), ftiles((size_t)K * CZ_CL, 0);
-    std::vector<int32_t> seen((size_t)K, 0);
-    for (size_t t = 0; t < all.size(); ++t) {
-      const int32_t k = tcl[t];
-      const size_t u = (size_t)k * CZ_CL + (size_t)(seen[(size_t)k]++ % CZ_CL);
-      frows[u] += all[t].nrows;
-      ftiles[u] += 1;
-    }
-    const bool fin_ok = *std::max_element(frows.begin(), frows.end()) <= WZ &&
-                        *std::max_element(ftiles.begin(), ftiles.end()) <= CZ_MAX_FT;
-    if (cmax <= CZ_MAX_ROWS && rmax <= MAX_TILE_ROWS_NOPARTS && fin_ok) {
-      P.cz = K;
-      P.cz_tcl = tcl;
-      P.cz_rmax = (int32_t)cmax;
-      P.rows_per_tile = (int32_t)cmax;  // row ids in chunk headers are cluster-local
-    } else {
-      all.clear();
-    }
-  }
   int rows_per_tile = force_rows ? force_rows : tiny ? MAX_TILE_ROWS : 0;
-  if (P.cz) rows_per_tile = P.cz_rmax;
   if (!rows_per_tile && total_len == 0) {
     const int64_t per = (n + 2LL * sm_count - 1) / (2LL * sm_count);
     rows_per_tile = (int)std::min<int64_t>(MAX_TILE_ROWS_NOPARTS, std::max<int64_t>(256, (per + 31) / 32 * 32));
@@ -608,7 +556,9 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   }
   P.rows_per_tile = rows_per_tile;
   std::vector<int32_t> crt((size_t)C, rows_per_tile);
-  for (int32_t c = 0; c < C && !P.cz; ++c) {
+  std::vector<TileDesc> all;
+  P.comm_tile0.assign((size_t)C + 1, 0);
+  for (int32_t c = 0; c < C; ++c) {
     P.comm_tile0[(size_t)c] = (int32_t)all.size();
     const int RT = crt[(size_t)c];
     for (int64_t r0 = S.moff[(size_t)c]; r0 < S.moff[(size_t)c + 1]; r0 += RT) {
@@ -619,7 +569,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
       all.push_back(t);
     }
   }
-  if (!P.cz) P.comm_tile0[(size_t)C] = (int32_t)all.size();
+  P.comm_tile0[(size_t)C] = (int32_t)all.size();
   const int64_t ntiles_all = (int64_t)all.size();
   // per-tile work estimate (entries), then shards of whole communities
   std::vector<int64_t> twork((size_t)ntiles_all, 0);
@@ -693,204 +643,17 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     int32_t nhot = 0, nown = 0, nloc = 0;
     int64_t hot = 0, rem = 0, shot = 0, srem = 0, loads = 0;
   };
-  const int32_t ncz = P.cz * CZ_CL;  // cluster-resident units (after the tiles in outs)
-  std::vector<TileOut> outs((size_t)nt + (size_t)ncz);
-  std::vector<std::array<int32_t, 2>> cz_win((size_t)ncz, std::array<int32_t, 2>{-1, -1});
-  std::vector<int32_t> cz_nrows((size_t)ncz, 0);
-  if (P.cz) {  // cluster-local row of each tile's row 0 (tiles of a cluster in tile order)
-    P.cz_tlro.assign((size_t)nt, 0);
-    std::vector<int32_t> acc((size_t)P.cz, 0);
-    for (int32_t t = 0; t < nt; ++t) {
-      const int32_t k = P.cz_tcl[(size_t)t];
-      P.cz_tlro[(size_t)t] = acc[(size_t)k];
-      acc[(size_t)k] += all[(size_t)t].nrows;
-    }
-  }
+  std::vector<TileOut> outs((size_t)nt);
 #pragma omp parallel
   {
     std::vector<uint64_t> keys, remk;
     std::vector<int32_t> rows, rb, cnt, rl;
     std::vector<uint32_t> pos;  // arranged positions of one quarter: 8 slots each
     std::vector<uint16_t> lst[8][8];
-    // emit_part's target and key format: tiles (local row in bits 32..42, 2^11 rows) or
-    // cluster units (bits 32..46); the row-piece rule sizes pieces for `pthreads` lanes
-    TileOut* Op = nullptr;
-    uint64_t rmask = 0x7FF;
-    size_t pthreads = NTHREADS;
-    // one part = entries src[k0..k1) of one (window|remote, sign), sorted by (row, column)
-    auto emit_part = [&](int32_t window, int32_t neg, const uint64_t* src, size_t k0, size_t k1) {
-      const bool hot = window >= 0;
-      PartDesc pd{window, neg, (uint32_t)Op->chunks.size(), 0};
-      // rows with entries, longest first
-      rows.clear();
-      rb.clear();
-      cnt.clear();
-      for (size_t k = k0; k < k1;) {
-        const int32_t lr = (int32_t)((src[k] >> 32) & rmask);
-        size_t j = k;
-        while (j < k1 && (int32_t)((src[j] >> 32) & rmask) == lr) ++j;
-        rows.push_back((int32_t)rows.size());
-        rb.push_back((int32_t)(k - k0));
-        cnt.push_back((int32_t)(j - k));
-        k = j;
-      }
-      std::vector<int32_t> ord(rows.size());
-      std::iota(ord.begin(), ord.end(), 0);
-      std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return cnt[(size_t)x] > cnt[(size_t)y]; });
-      rl.resize(rows.size());
-      for (size_t i = 0; i < rows.size(); ++i) rl[i] = (int32_t)((src[k0 + (size_t)rb[i]] >> 32) & rmask);
-      // ROW PIECES: few long rows -> split each row over an aligned group of lp lanes (combined by
-      // a warp butterfly in the kernel) so the part still has ~16 chunks for the 16 warps
-      int lp = 0;
-      {
-        const size_t nr = rows.size(), ne = k1 - k0;
-        while (lp < 5 && nr * ((size_t)2 << lp) <= pthreads && ne / (nr * ((size_t)2 << lp)) >= 16) ++lp;
-      }
-      // hot parts with pieces of <= 8 lanes: pack whole rows (items of 2^lp aligned lanes) into
-      // residue-balanced quarters first, in the row-level numbering (ord / cnt / rb / rl by row)
-      std::vector<std::array<int32_t, 32>> lanes;
-      const bool pooled = hot && lp <= 3;
-      if (pooled) {
-        const int w = 1 << lp;
-        std::vector<int32_t> lane_len(cnt.size());
-        for (size_t i = 0; i < cnt.size(); ++i) lane_len[i] = (cnt[i] + w - 1) / w;  // longest piece
-        std::vector<int32_t> pos_of(cnt.size());
-        for (size_t p = 0; p < ord.size(); ++p) pos_of[(size_t)ord[p]] = (int32_t)p;  // row -> ord position
-        plan_pools(ord, lane_len, lanes, [&](int32_t ri, int* cv) {
-          for (int e = 0; e < cnt[(size_t)ri]; ++e) cv[(src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) & 7]++;
-        }, w);
-        if (lp > 0)  // expand items to pieces: the pieces of the row at ord position p are p*w .. p*w+w-1
-          for (auto& a : lanes)
-            for (int l = 0; l < 32; l += w)
-              if (a[(size_t)l] >= 0) {
-                const int32_t p = pos_of[(size_t)a[(size_t)l]];
-                for (int i = 0; i < w; ++i) a[(size_t)(l + i)] = p * w + i;
-              }
-      }
-      if (lp > 0) {
-        const int pcs = 1 << lp;
-        std::vector<int32_t> vrb, vcnt, vrl;
-        for (int32_t ri : ord)
-          for (int i = 0; i < pcs; ++i) {
-            const int32_t b0 = (int32_t)((int64_t)cnt[(size_t)ri] * i / pcs);
-            const int32_t b1 = (int32_t)((int64_t)cnt[(size_t)ri] * (i + 1) / pcs);
-            vrb.push_back(rb[(size_t)ri] + b0);
-            vcnt.push_back(b1 - b0);
-            vrl.push_back(rl[(size_t)ri]);
-          }
-        rb.swap(vrb);
-        cnt.swap(vcnt);
-        rl.swap(vrl);
-        ord.resize(rb.size());
-        std::iota(ord.begin(), ord.end(), 0);  // units stay contiguous and lp-aligned
-        pd.neg |= lp << 8;
-      }
-      auto slot_of = [&](int32_t ri, int e) -> uint32_t {
-        return (uint32_t)((src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) - (uint64_t)window * WZ);
-      };
-      // chunks (lane -> row or piece); hot parts: residue-balanced quarter-warps (above)
-      if (!pooled) {
-        for (size_t c0 = 0; c0 < ord.size(); c0 += 32) {
-          std::array<int32_t, 32> a;
-          for (int l = 0; l < 32; ++l) a[(size_t)l] = c0 + (size_t)l < ord.size() ? ord[c0 + (size_t)l] : -1;
-          lanes.push_back(a);
-        }
-      }
-      for (const std::array<int32_t, 32>& lane_row : lanes) {
-        ChunkDesc cd{(uint32_t)Op->units.size(), 0};
-        Unit hdr[HDR_UNITS];
-        uint16_t* h16 = reinterpret_cast<uint16_t*>(hdr);
-        for (int l = 0; l < 32; ++l)
-          h16[l] = lane_row[(size_t)l] >= 0 ? (uint16_t)rl[(size_t)lane_row[(size_t)l]] : EMPTY_LANE;
-        Op->units.insert(Op->units.end(), hdr, hdr + HDR_UNITS);
-        const size_t gbase = Op->units.size();
-        if (hot) {
-          // bank-conflict-free schedule, one quarter-warp (8 lanes) at a time
-          std::vector<std::vector<uint32_t>> qpos(4);
-          size_t L = 0;
-          for (int q = 0; q < 4; ++q) {
-            for (int l = 0; l < 8; ++l)
-              for (int r = 0; r < 8; ++r) lst[l][r].clear();
-            for (int l = 0; l < 8; ++l) {
-              const int32_t ri = lane_row[(size_t)(q * 8 + l)];
-              if (ri < 0) continue;
-              for (int e = 0; e < cnt[(size_t)ri]; ++e) {
-                const uint32_t slot = slot_of(ri, e);
-                lst[l][slot & 7].push_back((uint16_t)slot);
-              }
-            }
-            schedule_quarter(lst, qpos[(size_t)q]);
-            L = std::max(L, qpos[(size_t)q].size() / 8);
-          }
-          // H half-groups of 4 positions: H/2 full groups of 8 slots (uint4 per lane), then one
-          // trailing half-group (uint2 per lane) when H is odd
-          // G full groups of 9 positions (13-bit slots packed in 16 bytes per lane), then an
-          // optional tail of 4 positions (16-bit slots, 8 bytes per lane): L rounded up to 9G or 9G + 4
-          uint32_t G = (uint32_t)(L / 9), tail = 0;
-          const size_t rem = L - (size_t)G * 9;
-          if (rem > 4) ++G;
-          else if (rem > 0) tail = 1;
-          cd.ng = (G << 1) | tail;
-          Op->units.resize(gbase + (size_t)G * 32 + tail * 16);
-          auto slot_at = [&](int lane, size_t p) -> uint32_t {
-            const std::vector<uint32_t>& P8 = qpos[(size_t)(lane / 8)];
-            return p < P8.size() / 8 ? P8[p * 8 + (size_t)(lane & 7)] : HOT_SENT + (uint32_t)(lane & 7);
-          };
-          for (uint32_t g = 0; g < G; ++g)
-            for (int lane = 0; lane < 32; ++lane) {
-              uint64_t lo = 0, hi = 0;
-              for (int e = 0; e < 9; ++e) {
-                const uint64_t v = slot_at(lane, (size_t)g * 9 + (size_t)e);
-                const int off = 13 * e;
-                if (off + 13 <= 64) lo |= v << off;
-                else if (off >= 64) hi |= v << (off - 64);
-                else {
-                  lo |= v << off;
-                  hi |= v >> (64 - off);
-                }
-              }
-              std::memcpy(Op->units[gbase + (size_t)g * 32 + (size_t)lane].w, &lo, 8);
-              std::memcpy(Op->units[gbase + (size_t)g * 32 + (size_t)lane].w + 2, &hi, 8);
-            }
-          if (tail) {
-            uint16_t* t16 = reinterpret_cast<uint16_t*>(Op->units.data() + gbase + (size_t)G * 32);
-            for (int lane = 0; lane < 32; ++lane)
-              for (int e = 0; e < 4; ++e) t16[(size_t)lane * 4 + (size_t)e] = (uint16_t)slot_at(lane, (size_t)G * 9 + (size_t)e);
-          }
-          Op->shot += (int64_t)(9 * G + 4 * tail) * 32;
-        } else {
-          int mx = 0;
-          for (int l = 0; l < 32; ++l)
-            if (lane_row[(size_t)l] >= 0) mx = std::max(mx, cnt[(size_t)lane_row[(size_t)l]]);
-          const uint32_t ng = (uint32_t)((mx + 3) / 4);
-          cd.ng = ng;
-          Op->units.resize(gbase + (size_t)ng * 32);
-          for (uint32_t g = 0; g < ng; ++g)
-            for (int lane = 0; lane < 32; ++lane) {
-              Unit& U = Op->units[gbase + (size_t)g * 32 + (size_t)lane];
-              for (int e = 0; e < 4; ++e) {
-                const int p = (int)g * 4 + e;
-                uint32_t v = SENT_REMOTE;
-                const int32_t ri = lane_row[(size_t)lane];
-                // remote entries keep their sign in bit 31 (1 = complement entry, subtracted)
-                if (ri >= 0 && p < cnt[(size_t)ri]) v = (uint32_t)(src[k0 + (size_t)rb[(size_t)ri] + (size_t)p] & 0xFFFFFFFFULL);
-                U.w[e] = v;
-              }
-            }
-          Op->srem += (int64_t)ng * 128;
-        }
-        Op->chunks.push_back(cd);
-        pd.nchunks++;
-      }
-      Op->parts.push_back(pd);
-      if (hot) Op->hot += (int64_t)(k1 - k0); else Op->rem += (int64_t)(k1 - k0);
-    };
 #pragma omp for schedule(dynamic, 1)
     for (int32_t lt = 0; lt < nt; ++lt) {
-      if (P.cz) continue;  // cluster-resident plans: tiles only finalize, the units below hold the parts
       const TileDesc& T = all[(size_t)(P.tile_begin + lt)];
       TileOut& O = outs[(size_t)lt];
-      Op = &O;
       keys.clear();
       for (int32_t lr = 0; lr < T.nrows; ++lr) {
         const int32_t u = P.perm[(size_t)(T.row0 + lr)];
@@ -900,6 +663,174 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
         });
       }
       std::sort(keys.begin(), keys.end());
+      // one part = entries src[k0..k1) of one (window|remote, sign), sorted by (row, column)
+      auto emit_part = [&](int32_t window, int32_t neg, const uint64_t* src, size_t k0, size_t k1) {
+        const bool hot = window >= 0;
+        PartDesc pd{window, neg, (uint32_t)O.chunks.size(), 0};
+        // rows with entries, longest first
+        rows.clear();
+        rb.clear();
+        cnt.clear();
+        for (size_t k = k0; k < k1;) {
+          const int32_t lr = (int32_t)((src[k] >> 32) & 0x7FF);
+          size_t j = k;
+          while (j < k1 && (int32_t)((src[j] >> 32) & 0x7FF) == lr) ++j;
+          rows.push_back((int32_t)rows.size());
+          rb.push_back((int32_t)(k - k0));
+          cnt.push_back((int32_t)(j - k));
+          k = j;
+        }
+        std::vector<int32_t> ord(rows.size());
+        std::iota(ord.begin(), ord.end(), 0);
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return cnt[(size_t)x] > cnt[(size_t)y]; });
+        rl.resize(rows.size());
+        for (size_t i = 0; i < rows.size(); ++i) rl[i] = (int32_t)((src[k0 + (size_t)rb[i]] >> 32) & 0x7FF);
+        // ROW PIECES: few long rows -> split each row over an aligned group of lp lanes (combined by
+        // a warp butterfly in the kernel) so the part still has ~16 chunks for the 16 warps
+        int lp = 0;
+        {
+          const size_t nr = rows.size(), ne = k1 - k0;
+          while (lp < 5 && nr * ((size_t)2 << lp) <= (size_t)NTHREADS && ne / (nr * ((size_t)2 << lp)) >= 16) ++lp;
+        }
+        // hot parts with pieces of <= 8 lanes: pack whole rows (items of 2^lp aligned lanes) into
+        // residue-balanced quarters first, in the row-level numbering (ord / cnt / rb / rl by row)
+        std::vector<std::array<int32_t, 32>> lanes;
+        const bool pooled = hot && lp <= 3;
+        if (pooled) {
+          const int w = 1 << lp;
+          std::vector<int32_t> lane_len(cnt.size());
+          for (size_t i = 0; i < cnt.size(); ++i) lane_len[i] = (cnt[i] + w - 1) / w;  // longest piece
+          std::vector<int32_t> pos_of(cnt.size());
+          for (size_t p = 0; p < ord.size(); ++p) pos_of[(size_t)ord[p]] = (int32_t)p;  // row -> ord position
+          plan_pools(ord, lane_len, lanes, [&](int32_t ri, int* cv) {
+            for (int e = 0; e < cnt[(size_t)ri]; ++e) cv[(src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) & 7]++;
+          }, w);
+          if (lp > 0)  // expand items to pieces: the pieces of the row at ord position p are p*w .. p*w+w-1
+            for (auto& a : lanes)
+              for (int l = 0; l < 32; l += w)
+                if (a[(size_t)l] >= 0) {
+                  const int32_t p = pos_of[(size_t)a[(size_t)l]];
+                  for (int i = 0; i < w; ++i) a[(size_t)(l + i)] = p * w + i;
+                }
+        }
+        if (lp > 0) {
+          const int pcs = 1 << lp;
+          std::vector<int32_t> vrb, vcnt, vrl;
+          for (int32_t ri : ord)
+            for (int i = 0; i < pcs; ++i) {
+              const int32_t b0 = (int32_t)((int64_t)cnt[(size_t)ri] * i / pcs);
+              const int32_t b1 = (int32_t)((int64_t)cnt[(size_t)ri] * (i + 1) / pcs);
+              vrb.push_back(rb[(size_t)ri] + b0);
+              vcnt.push_back(b1 - b0);
+              vrl.push_back(rl[(size_t)ri]);
+            }
+          rb.swap(vrb);
+          cnt.swap(vcnt);
+          rl.swap(vrl);
+          ord.resize(rb.size());
+          std::iota(ord.begin(), ord.end(), 0);  // units stay contiguous and lp-aligned
+          pd.neg |= lp << 8;
+        }
+        auto slot_of = [&](int32_t ri, int e) -> uint32_t {
+          return (uint32_t)((src[k0 + (size_t)rb[(size_t)ri] + (size_t)e] & COLM) - (uint64_t)window * WZ);
+        };
+        // chunks (lane -> row or piece); hot parts: residue-balanced quarter-warps (above)
+        if (!pooled) {
+          for (size_t c0 = 0; c0 < ord.size(); c0 += 32) {
+            std::array<int32_t, 32> a;
+            for (int l = 0; l < 32; ++l) a[(size_t)l] = c0 + (size_t)l < ord.size() ? ord[c0 + (size_t)l] : -1;
+            lanes.push_back(a);
+          }
+        }
+        for (const std::array<int32_t, 32>& lane_row : lanes) {
+          ChunkDesc cd{(uint32_t)O.units.size(), 0};
+          Unit hdr[HDR_UNITS];
+          uint16_t* h16 = reinterpret_cast<uint16_t*>(hdr);
+          for (int l = 0; l < 32; ++l)
+            h16[l] = lane_row[(size_t)l] >= 0 ? (uint16_t)rl[(size_t)lane_row[(size_t)l]] : EMPTY_LANE;
+          O.units.insert(O.units.end(), hdr, hdr + HDR_UNITS);
+          const size_t gbase = O.units.size();
+          if (hot) {
+            // bank-conflict-free schedule, one quarter-warp (8 lanes) at a time
+            std::vector<std::vector<uint32_t>> qpos(4);
+            size_t L = 0;
+            for (int q = 0; q < 4; ++q) {
+              for (int l = 0; l < 8; ++l)
+                for (int r = 0; r < 8; ++r) lst[l][r].clear();
+              for (int l = 0; l < 8; ++l) {
+                const int32_t ri = lane_row[(size_t)(q * 8 + l)];
+                if (ri < 0) continue;
+                for (int e = 0; e < cnt[(size_t)ri]; ++e) {
+                  const uint32_t slot = slot_of(ri, e);
+                  lst[l][slot & 7].push_back((uint16_t)slot);
+                }
+              }
+              schedule_quarter(lst, qpos[(size_t)q]);
+              L = std::max(L, qpos[(size_t)q].size() / 8);
+            }
+            // H half-groups of 4 positions: H/2 full groups of 8 slots (uint4 per lane), then one
+            // trailing half-group (uint2 per lane) when H is odd
+            // G full groups of 9 positions (13-bit slots packed in 16 bytes per lane), then an
+            // optional tail of 4 positions (16-bit slots, 8 bytes per lane): L rounded up to 9G or 9G + 4
+            uint32_t G = (uint32_t)(L / 9), tail = 0;
+            const size_t rem = L - (size_t)G * 9;
+            if (rem > 4) ++G;
+            else if (rem > 0) tail = 1;
+            cd.ng = (G << 1) | tail;
+            O.units.resize(gbase + (size_t)G * 32 + tail * 16);
+            auto slot_at = [&](int lane, size_t p) -> uint32_t {
+              const std::vector<uint32_t>& P8 = qpos[(size_t)(lane / 8)];
+              return p < P8.size() / 8 ? P8[p * 8 + (size_t)(lane & 7)] : HOT_SENT + (uint32_t)(lane & 7);
+            };
+            for (uint32_t g = 0; g < G; ++g)
+              for (int lane = 0; lane < 32; ++lane) {
+                uint64_t lo = 0, hi = 0;
+                for (int e = 0; e < 9; ++e) {
+                  const uint64_t v = slot_at(lane, (size_t)g * 9 + (size_t)e);
+                  const int off = 13 * e;
+                  if (off + 13 <= 64) lo |= v << off;
+                  else if (off >= 64) hi |= v << (off - 64);
+                  else {
+                    lo |= v << off;
+                    hi |= v >> (64 - off);
+                  }
+                }
+                std::memcpy(O.units[gbase + (size_t)g * 32 + (size_t)lane].w, &lo, 8);
+                std::memcpy(O.units[gbase + (size_t)g * 32 + (size_t)lane].w + 2, &hi, 8);
+              }
+            if (tail) {
+              uint16_t* t16 = reinterpret_cast<uint16_t*>(O.units.data() + gbase + (size_t)G * 32);
+              for (int lane = 0; lane < 32; ++lane)
+                for (int e = 0; e < 4; ++e) t16[(size_t)lane * 4 + (size_t)e] = (uint16_t)slot_at(lane, (size_t)G * 9 + (size_t)e);
+            }
+            O.shot += (int64_t)(9 * G + 4 * tail) * 32;
+          } else {
+            int mx = 0;
+            for (int l = 0; l < 32; ++l)
+              if (lane_row[(size_t)l] >= 0) mx = std::max(mx, cnt[(size_t)lane_row[(size_t)l]]);
+            const uint32_t ng = (uint32_t)((mx + 3) / 4);
+            cd.ng = ng;
+            O.units.resize(gbase + (size_t)ng * 32);
+            for (uint32_t g = 0; g < ng; ++g)
+              for (int lane = 0; lane < 32; ++lane) {
+                Unit& U = O.units[gbase + (size_t)g * 32 + (size_t)lane];
+                for (int e = 0; e < 4; ++e) {
+                  const int p = (int)g * 4 + e;
+                  uint32_t v = SENT_REMOTE;
+                  const int32_t ri = lane_row[(size_t)lane];
+                  // remote entries keep their sign in bit 31 (1 = complement entry, subtracted)
+                  if (ri >= 0 && p < cnt[(size_t)ri]) v = (uint32_t)(src[k0 + (size_t)rb[(size_t)ri] + (size_t)p] & 0xFFFFFFFFULL);
+                  U.w[e] = v;
+                }
+              }
+            O.srem += (int64_t)ng * 128;
+          }
+          O.chunks.push_back(cd);
+          pd.nchunks++;
+        }
+        O.parts.push_back(pd);
+        if (hot) O.hot += (int64_t)(k1 - k0); else O.rem += (int64_t)(k1 - k0);
+      };
       remk.clear();
       size_t i = 0;
       int32_t last_w = -1;
@@ -940,72 +871,11 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
         emit_part(-1, 0, remk.data(), 0, remk.size());
       }
     }
-    // cluster-resident units: cluster k's rows (its tiles in tile order, cluster-local ids), every
-    // entry keyed window<<48 | neg<<47 | local_row<<32 | internal column; the windows go to the
-    // cluster's CTAs largest first, each onto the least loaded CTA with a free window slot; a CTA's
-    // parts are its windows in column order, non-zero entries before complement entries
-#pragma omp for schedule(dynamic, 1)
-    for (int32_t k = 0; k < P.cz; ++k) {
-      keys.clear();
-      int32_t nrows = 0;
-      for (int32_t t = 0; t < nt; ++t) {
-        if (P.cz_tcl[(size_t)t] != k) continue;
-        const TileDesc& T = all[(size_t)t];
-        for (int32_t r = 0; r < T.nrows; ++r) {
-          const uint64_t lr = (uint64_t)(P.cz_tlro[(size_t)t] + r);
-          enumerate_row(S, P.D_ptr, P.D_idx, P.perm[(size_t)(T.row0 + r)], [&](int32_t kc, int neg) {
-            const uint64_t c = (uint64_t)(uint32_t)inv[(size_t)kc];
-            keys.push_back(((c >> WZ_SHIFT) << 48) | ((uint64_t)neg << 47) | (lr << 32) | c);
-          });
-        }
-        nrows += T.nrows;
-      }
-      std::sort(keys.begin(), keys.end());
-      const int32_t nwin = (int32_t)((n + WZ - 1) / WZ);
-      std::vector<size_t> wbeg((size_t)nwin + 1, keys.size());
-      for (int32_t w = 0, i = 0; w < nwin; ++w) {
-        wbeg[(size_t)w] = (size_t)i;
-        while ((size_t)i < keys.size() && (int32_t)(keys[(size_t)i] >> 48) == w) ++i;
-      }
-      std::vector<int32_t> word((size_t)nwin);
-      std::iota(word.begin(), word.end(), 0);
-      std::stable_sort(word.begin(), word.end(), [&](int32_t x, int32_t y) {
-        return wbeg[(size_t)x + 1] - wbeg[(size_t)x] > wbeg[(size_t)y + 1] - wbeg[(size_t)y];
-      });
-      std::array<int64_t, CZ_CL> load{};
-      std::array<std::vector<int32_t>, CZ_CL> wins;
-      for (int32_t w : word) {
-        const size_t ne = wbeg[(size_t)w + 1] - wbeg[(size_t)w];
-        if (ne == 0) continue;
-        int best = -1;
-        for (int c = 0; c < CZ_CL; ++c)
-          if ((int)wins[(size_t)c].size() < CZ_MAX_WIN && (best < 0 || load[(size_t)c] < load[(size_t)best])) best = c;
-        wins[(size_t)best].push_back(w);
-        load[(size_t)best] += (int64_t)ne;
-      }
-      for (int c = 0; c < CZ_CL; ++c) {
-        const int32_t u = k * CZ_CL + c;
-        std::sort(wins[(size_t)c].begin(), wins[(size_t)c].end());
-        Op = &outs[(size_t)nt + (size_t)u];
-        rmask = 0x7FFF;
-        for (size_t i = 0; i < wins[(size_t)c].size(); ++i) {
-          const int32_t w = wins[(size_t)c][i];
-          cz_win[(size_t)u][i] = w;
-          const size_t i0 = wbeg[(size_t)w], i1 = wbeg[(size_t)w + 1];
-          size_t m = i0;
-          while (m < i1 && !((keys[m] >> 47) & 1)) ++m;
-          if (m > i0) { emit_part(w, 0, keys.data(), i0, m); Op->nhot++; }
-          if (i1 > m) { emit_part(w, 1, keys.data(), m, i1); Op->nhot++; }
-          Op->loads++;
-        }
-        cz_nrows[(size_t)u] = nrows;
-      }
-    }
   }
   // ------------------------------------------------------------ 6. concatenate
   P.tiles.resize((size_t)nt);
   int64_t units = 0, nparts = 0, nchunks = 0;
-  for (int32_t lt = 0; lt < nt + ncz; ++lt) {
+  for (int32_t lt = 0; lt < nt; ++lt) {
     units += (int64_t)outs[(size_t)lt].units.size();
     nparts += (int64_t)outs[(size_t)lt].parts.size();
     nchunks += (int64_t)outs[(size_t)lt].chunks.size();
@@ -1016,36 +886,12 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   P.chunks.assign((size_t)std::max<int64_t>(nchunks, 1), ChunkDesc{0, 0});
   int64_t uo = 0, po = 0, co = 0;
   P.n_idx_hot = P.n_idx_remote = P.n_slots_hot = P.n_slots_remote = P.n_hot_parts = P.n_window_loads = 0;
-  std::vector<int64_t> uofs((size_t)(nt + ncz)), pofs((size_t)(nt + ncz)), cofs((size_t)(nt + ncz));
-  P.cz_units.assign((size_t)ncz, CzUnit{});
-  P.cz_ft.clear();
-  for (int32_t lt = 0; lt < nt + ncz; ++lt) {
+  std::vector<int64_t> uofs((size_t)nt), pofs((size_t)nt), cofs((size_t)nt);
+  for (int32_t lt = 0; lt < nt; ++lt) {
     uofs[(size_t)lt] = uo;
     pofs[(size_t)lt] = po;
     cofs[(size_t)lt] = co;
     const TileOut& O = outs[(size_t)lt];
-    if (lt >= nt) {  // cluster-resident unit u: its parts, windows, and the tiles it finalizes
-      const int32_t u = lt - nt, k = u / CZ_CL, c = u % CZ_CL;
-      CzUnit& U = P.cz_units[(size_t)u];
-      U.part0 = (int32_t)po;
-      U.nparts = (int32_t)O.parts.size();
-      U.w0 = cz_win[(size_t)u][0];
-      U.w1 = cz_win[(size_t)u][1];
-      U.nrows = cz_nrows[(size_t)u];
-      U.ft0 = (int32_t)P.cz_ft.size();
-      for (int32_t t = 0, i = 0; t < nt; ++t)  // the cluster's i-th tile is finalized by CTA i mod CZ_CL
-        if (P.cz_tcl[(size_t)t] == k && (i++ % CZ_CL) == c) P.cz_ft.push_back(t);
-      U.nft = (int32_t)P.cz_ft.size() - U.ft0;
-      if (U.nft > CZ_MAX_FT) { err = "cluster plan: too many tiles per CTA"; return KUR_ERR_UNSUPPORTED; }
-      uo += (int64_t)O.units.size();
-      po += (int64_t)O.parts.size();
-      co += (int64_t)O.chunks.size();
-      P.n_idx_hot += O.hot;
-      P.n_slots_hot += O.shot;
-      P.n_hot_parts += O.nhot;
-      P.n_window_loads += O.loads;
-      continue;
-    }
     TileDesc T = all[(size_t)(P.tile_begin + lt)];
     T.part0 = (int32_t)po;
     T.nparts = (int32_t)O.parts.size();
@@ -1076,7 +922,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   P.split_remote = !P.small && P.n_slots_remote * world >= (16LL << 20) && nt > 0 && P.n_slots_remote / nt >= 8192;
   if (force_split) P.split_remote = !P.small && force_split == 1;
 #pragma omp parallel for schedule(dynamic, 4)
-  for (int32_t lt = 0; lt < nt + ncz; ++lt) {
+  for (int32_t lt = 0; lt < nt; ++lt) {
     TileOut& O = outs[(size_t)lt];
     if (!O.units.empty()) std::memcpy(P.pool.data() + uofs[(size_t)lt], O.units.data(), O.units.size() * sizeof(Unit));
     for (size_t p = 0; p < O.parts.size(); ++p) {

@@ -25,7 +25,6 @@
 //               straight into the peers' receive buffers.
 // All reductions are fixed-shape (no floating-point atomics): bitwise
 // reproducible run to run and across world sizes.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -73,14 +72,6 @@ namespace {
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
-// Cluster-resident stage: the whole index pool of such a plan (<= a few tens of MB) stays in the
-// 126 MB L2 across stages -> evict last instead.
-__device__ __forceinline__ uint64_t evict_last_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
 
@@ -840,71 +831,6 @@ __device__ __forceinline__ void prologue_rows(const DevPlan& dp, const StageArgs
   }
 }
 
-// a4 + a5 for one row (k_stage's finalize, the cluster kernel's too): k_j = omega_j + (K/M_j) Im(conj z_j W_j)
-// with W_j = (wx, wy), then the fused integrator stage, the next z and its contribution (px, py) to
-// the tile partial; returns whether theta_{n+1} became non-finite (final stages).
-template <int MODE, bool SMALL>
-__device__ __forceinline__ bool finalize_row(const DevPlan& dp, const StageArgs& a, int row, int li, double wx,
-                                             double wy, double& px, double& py, double& dmax) {
-  bool bad = false;
-  const double2 zj = SMALL ? __ldcg(a.zin + row) : a.zin[row];
-  // K/M_m: uniform K/N, or K/deg_m for the degree scaling
-  const double kn = dp.rowscale ? a.K * dp.rowscale[li] : a.KN;
-  if (MODE == MODE_POT) {  // -omega_m theta_m + (K/2)(1/M_m)(sum_l A_ml - Re(conj z_m W_m))
-    const double sm = dp.rowscale ? dp.rowscale[li] : a.KN / a.K;
-    px += -a.omega[li] * a.theta[li] + 0.5 * a.K * sm * (dp.potc[li] - (zj.x * wx + zj.y * wy));
-    return false;
-  }
-  const double k = rhs_k(a.omega[li], kn, zj.x, zj.y, wx, wy);
-  if (MODE == MODE_RHS) {
-    a.out[li] = k;
-  } else {
-    const double thn = a.theta[li];
-    double ts;
-    if (MODE == MODE_S1) {
-      a.acc[li] = k;
-      ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
-    } else if (MODE == MODE_S2) {
-      a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
-      ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
-    } else if (MODE == MODE_S3) {
-      a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
-      ts = __dadd_rn(thn, __dmul_rn(a.h, k));
-    } else if (MODE == MODE_S4) {  // theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
-      ts = __dadd_rn(thn, __dmul_rn(a.h / 6.0, __dadd_rn(a.acc[li], k)));
-      a.theta[li] = ts;
-      if (a.theta_host) a.theta_host[li] = ts;
-      bad |= !isfinite(ts);
-    } else if (MODE == MODE_E1) {  // explicit Euler: theta_{n+1} = theta_n + h k
-      ts = __dadd_rn(thn, __dmul_rn(a.h, k));
-      a.theta[li] = ts;
-      if (a.theta_host) a.theta_host[li] = ts;
-      bad |= !isfinite(ts);
-    } else if (MODE == MODE_H1) {  // Heun: k1, stage state theta_n + h k1
-      a.acc[li] = k;
-      ts = __dadd_rn(thn, __dmul_rn(a.h, k));
-    } else if (MODE == MODE_H2) {  // theta_{n+1} = theta_n + (h/2)(k1 + k2)
-      ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, __dadd_rn(a.acc[li], k)));
-      a.theta[li] = ts;
-      if (a.theta_host) a.theta_host[li] = ts;
-      bad |= !isfinite(ts);
-    } else {  // MODE_M0 / MODE_MI: implicit midpoint fixed point on tp (kept in acc)
-      const double nv = __dadd_rn(thn, __dmul_rn(a.h, k));
-      if (MODE == MODE_MI) dmax = fmax(dmax, fabs(__dadd_rn(nv, -a.acc[li])));
-      a.acc[li] = nv;
-      ts = __dadd_rn(thn, nv) / 2.0;
-      if (MODE == MODE_MI && !(fabs(nv) <= 1.79e308)) dmax = __longlong_as_double(0x7ff0000000000000ll);
-    }
-    double s, c;
-    sincos(ts, &s, &c);
-    a.zout[row] = make_double2(c, s);
-    if (a.xsend) xput(dp, a, li, ts);
-    px += c;
-    py += s;
-  }
-  return bad;
-}
-
 // a3-a5 for one tile (all threads of the CTA call it; contains barriers).
 // zs: [WZ + 8] window + zero sentinels, Ws: [rows_per_tile] row sums (both
 // unused when the plan has no parts).  Returns the thread's partial sums of
@@ -1039,7 +965,61 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
       w.y += r.y;
     }
     const double wx = Tc.x + w.x, wy = Tc.y + w.y;
-    if (finalize_row<MODE, SMALL>(dp, a, row, li, wx, wy, px, py, dmax)) bad = true;
+    const double2 zj = SMALL ? __ldcg(a.zin + row) : a.zin[row];
+    // K/M_m: uniform K/N, or K/deg_m for the degree scaling
+    const double kn = dp.rowscale ? a.K * dp.rowscale[li] : a.KN;
+    if (MODE == MODE_POT) {  // -omega_m theta_m + (K/2)(1/M_m)(sum_l A_ml - Re(conj z_m W_m))
+      const double sm = dp.rowscale ? dp.rowscale[li] : a.KN / a.K;
+      px += -a.omega[li] * a.theta[li] + 0.5 * a.K * sm * (dp.potc[li] - (zj.x * wx + zj.y * wy));
+      continue;
+    }
+    const double k = rhs_k(a.omega[li], kn, zj.x, zj.y, wx, wy);
+    if (MODE == MODE_RHS) {
+      a.out[li] = k;
+    } else {
+      const double thn = a.theta[li];
+      double ts;
+      if (MODE == MODE_S1) {
+        a.acc[li] = k;
+        ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
+      } else if (MODE == MODE_S2) {
+        a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
+        ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, k));
+      } else if (MODE == MODE_S3) {
+        a.acc[li] = __dadd_rn(a.acc[li], __dmul_rn(2.0, k));
+        ts = __dadd_rn(thn, __dmul_rn(a.h, k));
+      } else if (MODE == MODE_S4) {  // theta_{n+1} = theta_n + (h/6)(k1 + 2k2 + 2k3 + k4)
+        ts = __dadd_rn(thn, __dmul_rn(a.h / 6.0, __dadd_rn(a.acc[li], k)));
+        a.theta[li] = ts;
+        if (a.theta_host) a.theta_host[li] = ts;
+        bad |= !isfinite(ts);
+      } else if (MODE == MODE_E1) {  // explicit Euler: theta_{n+1} = theta_n + h k
+        ts = __dadd_rn(thn, __dmul_rn(a.h, k));
+        a.theta[li] = ts;
+        if (a.theta_host) a.theta_host[li] = ts;
+        bad |= !isfinite(ts);
+      } else if (MODE == MODE_H1) {  // Heun: k1, stage state theta_n + h k1
+        a.acc[li] = k;
+        ts = __dadd_rn(thn, __dmul_rn(a.h, k));
+      } else if (MODE == MODE_H2) {  // theta_{n+1} = theta_n + (h/2)(k1 + k2)
+        ts = __dadd_rn(thn, __dmul_rn(a.h / 2.0, __dadd_rn(a.acc[li], k)));
+        a.theta[li] = ts;
+        if (a.theta_host) a.theta_host[li] = ts;
+        bad |= !isfinite(ts);
+      } else {  // MODE_M0 / MODE_MI: implicit midpoint fixed point on tp (kept in acc)
+        const double nv = __dadd_rn(thn, __dmul_rn(a.h, k));
+        if (MODE == MODE_MI) dmax = fmax(dmax, fabs(__dadd_rn(nv, -a.acc[li])));
+        a.acc[li] = nv;
+        ts = __dadd_rn(thn, nv) / 2.0;
+        if (MODE == MODE_MI && !(fabs(nv) <= 1.79e308)) dmax = __longlong_as_double(0x7ff0000000000000ll);
+      }
+      double s, c;
+      sincos(ts, &s, &c);
+      a.zout[row] = make_double2(c, s);
+      if (a.xsend) xput(dp, a, li, ts);
+      px += c;
+      py += s;
+    }
   }
   return bad;
 }
@@ -1183,250 +1163,6 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   // the window buffer is free now: the last CTA keeps the block sums in it (WZ >= C)
   tile_partial_and_finish(dp, a, lt, px, py, red, dmax, (dp.has_parts && dp.C <= WZ) ? zs : nullptr);
   if (dp.peer_x && a.xsend) peer_arrive(dp);
-}
-
-// Hot part for the cluster-resident stage, whose parts are mostly many SHORT chunks (a row has ~4
-// entries per foreign window): the chunk loop is software-pipelined across chunks -- the next
-// chunk's header, first two index units and tail are requested (and the descriptor after it)
-// before the current chunk is gathered -- so a warp does not pay one DRAM round trip per chunk.
-// Within a chunk: groups 0 and 1 from the prefetched units, later groups two ahead; the tail last.
-template <int NW>
-__device__ __forceinline__ void run_part_cz(const DevPlan& dp, const PartDesc& P, const double2* zs, double2* Ws,
-                                            uint64_t pol, int warp, int lane) {
-  const uint32_t nch = P.nchunks;
-  uint32_t c = warp;
-  if (c >= nch) return;
-  const uint2* ch = dp.chunks + P.chunk0;
-  auto nxt = [&](uint32_t r) { return (r + 1) * NW + (((r + 1) & 1) ? (NW - 1 - warp) : warp); };
-  const uint4 z4 = make_uint4(0, 0, 0, 0);
-  const int lp = P.neg >> 8;
-  uint2 cd = __ldg(ch + c);
-  const uint4* q = dp.pool + cd.x;
-  uint16_t row = reinterpret_cast<const uint16_t*>(q)[lane];
-  uint4 b0 = (cd.y >> 1) > 0 ? ldg_stream(q + HDR_UNITS + lane, pol) : z4;
-  uint4 b1 = (cd.y >> 1) > 1 ? ldg_stream(q + HDR_UNITS + lane + 32, pol) : z4;
-  uint2 tl = (cd.y & 1) ? ldg_stream2(reinterpret_cast<const uint2*>(q + HDR_UNITS + (size_t)(cd.y >> 1) * 32) + lane, pol)
-                        : make_uint2(0, 0);
-  uint32_t cn = nxt(0);
-  uint2 cdn = cn < nch ? __ldg(ch + cn) : make_uint2(0, 0);
-  for (uint32_t r = 0;; ++r) {
-    const bool more = cn < nch;
-    const uint4* qn = dp.pool + cdn.x;
-    uint16_t rown = EMPTY_LANE;
-    uint4 n0 = z4, n1 = z4;
-    uint2 tn = make_uint2(0, 0);
-    if (more) {
-      rown = reinterpret_cast<const uint16_t*>(qn)[lane];
-      if ((cdn.y >> 1) > 0) n0 = ldg_stream(qn + HDR_UNITS + lane, pol);
-      if ((cdn.y >> 1) > 1) n1 = ldg_stream(qn + HDR_UNITS + lane + 32, pol);
-      if (cdn.y & 1) tn = ldg_stream2(reinterpret_cast<const uint2*>(qn + HDR_UNITS + (size_t)(cdn.y >> 1) * 32) + lane, pol);
-    }
-    const uint32_t cnn = nxt(r + 1);
-    const uint2 cdnn = cnn < nch ? __ldg(ch + cnn) : make_uint2(0, 0);
-    // the current chunk
-    const uint32_t ng = cd.y >> 1;
-    const uint4* qg = q + HDR_UNITS + lane;
-    uint4 b2 = ng > 2 ? ldg_stream(qg + 64, pol) : z4;
-    uint4 b3 = ng > 3 ? ldg_stream(qg + 96, pol) : z4;
-    uint4 b4 = ng > 4 ? ldg_stream(qg + 128, pol) : z4;
-    uint4 b5 = ng > 5 ? ldg_stream(qg + 160, pol) : z4;
-    double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
-    if (ng > 0) hot9(b0, zs, x0, y0, x1, y1);
-    if (ng > 1) hot9(b1, zs, x0, y0, x1, y1);
-    for (uint32_t g = 2; g < ng; g += 4) {  // four groups in flight
-      const uint4 u0 = b2, u1 = b3, u2 = b4, u3 = b5;
-      if (g + 4 < ng) b2 = ldg_stream(qg + (size_t)(g + 4) * 32, pol);
-      if (g + 5 < ng) b3 = ldg_stream(qg + (size_t)(g + 5) * 32, pol);
-      if (g + 6 < ng) b4 = ldg_stream(qg + (size_t)(g + 6) * 32, pol);
-      if (g + 7 < ng) b5 = ldg_stream(qg + (size_t)(g + 7) * 32, pol);
-      hot9(u0, zs, x0, y0, x1, y1);
-      if (g + 1 < ng) hot9(u1, zs, x0, y0, x1, y1);
-      if (g + 2 < ng) hot9(u2, zs, x0, y0, x1, y1);
-      if (g + 3 < ng) hot9(u3, zs, x0, y0, x1, y1);
-    }
-    if (cd.y & 1) hot4(tl, zs, x0, y0, x1, y1);
-    double sx = x0 + x1, sy = y0 + y1;
-    for (int o = 1; o < (1 << lp); o <<= 1) {
-      sx += __shfl_xor_sync(0xffffffffu, sx, o);
-      sy += __shfl_xor_sync(0xffffffffu, sy, o);
-    }
-    if (row != EMPTY_LANE && (lane & ((1 << lp) - 1)) == 0) {
-      KUR_ASSERT(row < dp.rows_per_tile);
-      double2 w = Ws[row];
-      if (P.neg & 1) {
-        w.x -= sx;
-        w.y -= sy;
-      } else {
-        w.x += sx;
-        w.y += sy;
-      }
-      Ws[row] = w;
-    }
-    if (!more) break;
-    cd = cdn;
-    q = qn;
-    row = rown;
-    b0 = n0;
-    b1 = n1;
-    tl = tn;
-    cn = cnn;
-    cdn = cdnn;
-  }
-}
-
-// ---- cluster-resident stage (world 1, n <= CZ_MAX_N; plan.h CzUnit).  One cluster
-// of CZ_CL CTAs per slice set of the communities; each CTA stages its (<= 2) windows of z ONCE and
-// gathers every entry of the cluster's rows that falls in them from shared memory (13-bit slots,
-// conflict-free, the tile path's run_part) into its row sums Pw; after a cluster barrier each CTA
-// finalizes its tiles with W_j = T_c + sum over the cluster's CTAs (rank order) of Pw[j], read
-// through distributed shared memory.  No global-memory gather is left: the tile path's remote
-// entries (one L1 wavefront each) become 1/8-wavefront shared-memory gathers.
-template <int MODE, int CZT>
-__global__ void __launch_bounds__(CZT, 1) k_stage_cz(const DevPlan dp, const StageArgs a) {
-  constexpr int CZW = CZT / 32;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* zs0 = reinterpret_cast<double2*>(smem_raw);  // [WZ + 8]: window w0 + 8 zero sentinels
-  double2* zs1 = zs0 + (WZ + 8);                         // [WZ + 8]: window w1
-  double2* Pw = zs1 + (WZ + 8);                          // [cluster rows]: this CTA's row sums
-  __shared__ double2 red[CZW];
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ double2 s_T[CZ_MAX_FT];
-  __shared__ int s_toff[CZ_MAX_FT + 1];
-  __shared__ int s_nonfinite;
-  __shared__ bool s_last;
-  cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // implicit midpoint after convergence: no-op (every CTA reads the same flag, so whole clusters leave)
-  if (MODE == MODE_MI && *(volatile const int*)&dp.ctrl->fp_done) return;
-  const CzUnit U = dp.cz_units[blockIdx.x];
-  if (tid < 8) {
-    zs0[WZ + tid] = make_double2(0.0, 0.0);
-    zs1[WZ + tid] = make_double2(0.0, 0.0);
-  }
-  for (int r = tid; r < ((dp.cz_dbg & 128) ? 0 : U.nrows); r += CZT) Pw[r] = make_double2(0.0, 0.0);
-  if (tid == 0) {
-    s_nonfinite = 0;
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-  }
-  __syncthreads();
-  if (tid == 0 && !(dp.cz_dbg & 64)) {
-    if (U.w0 >= 0) tma_load_1d(zs0, a.zin + (size_t)U.w0 * WZ, WZ * sizeof(double2), &bar[0]);
-    if (U.w1 >= 0) tma_load_1d(zs1, a.zin + (size_t)U.w1 * WZ, WZ * sizeof(double2), &bar[1]);
-  } else if (tid == 32 && U.nparts > 0) {  // this CTA's index units are contiguous: pull them into L2
-    const PartDesc P0 = dp.parts[U.part0], PL = dp.parts[U.part0 + U.nparts - 1];
-    const uint2 c0 = __ldg(dp.chunks + P0.chunk0), cl = __ldg(dp.chunks + PL.chunk0 + PL.nchunks - 1);
-    const uint32_t u0 = c0.x, u1 = cl.x + HDR_UNITS + (cl.y >> 1) * 32 + (cl.y & 1) * 16;
-    for (uint32_t u = u0; u < u1; u += 4096) {
-      const uint32_t nb = min(4096u, u1 - u) * 16u;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(dp.pool + u), "r"(nb) : "memory");
-    }
-  }
-  // row offsets of the finalize tiles; T of each finalize tile's community while the windows are in
-  // flight: the deferred block sums (one warp per tile, the last warps: the first ones start the
-  // parts) or the previous reduction's Tin
-  if (tid == CZT - 1) {
-    int o = 0;
-    for (int i = 0; i < U.nft; ++i) {
-      s_toff[i] = o;
-      o += dp.tiles[dp.cz_ft[U.ft0 + i]].nrows;
-    }
-    s_toff[U.nft] = o;
-  }
-  for (int i = CZW - 1 - warp; i >= 0 && i < ((dp.cz_dbg & 8) ? 0 : U.nft); i += CZW) {
-    const int comm = dp.tiles[dp.cz_ft[U.ft0 + i]].comm;
-    if (a.plazy) lazy_T_warp(dp, a.plazy, comm, lane, &s_T[i]);
-    else if (lane == 0) s_T[i] = __ldcg(a.Tin + comm);
-  }
-  // a3: the parts of this CTA's windows (by window, non-zero entries then complement entries)
-  const uint64_t pol = evict_last_policy();
-  bool got0 = false, got1 = false;
-  for (int p = U.part0; p < U.part0 + ((dp.cz_dbg & 1) ? 0 : U.nparts); ++p) {
-    const PartDesc P = dp.parts[p];
-    const bool second = P.window == U.w1;
-    if (!second && !got0) {
-      mbar_wait(&bar[0], 0);
-      got0 = true;
-    }
-    if (second && !got1) {
-      mbar_wait(&bar[1], 0);
-      got1 = true;
-    }
-    run_part_cz<CZW>(dp, P, second ? zs1 : zs0, Pw, pol, warp, lane);
-    if (!(dp.cz_dbg & 4)) __syncthreads();  // the next part may add into the same rows
-  }
-  if (dp.cz_dbg & 32) __syncthreads();
-  else cl.sync();  // every row sum of the cluster is complete (release / acquire at cluster scope)
-  // a4 + a5 for this CTA's tiles, all their rows at once (one per thread):
-  // W_j = T_c + (0 + Pw_0[j] + ... + Pw_{CZ_CL-1}[j]); the windows are free now and hold each row's
-  // contribution to its tile partial, summed per tile by one warp in row order afterwards
-  double2* sp = zs0;                                  // [finalize rows] (px, py)
-  double* sd = reinterpret_cast<double*>(zs1);        // [finalize rows] max |update| (implicit midpoint)
-  bool bad = false;
-  const int nfin = (dp.cz_dbg & 16) ? 0 : s_toff[U.nft];
-  for (int f = tid; f < nfin; f += CZT) {
-    int i = 0;
-    while (f >= s_toff[i + 1]) ++i;
-    const int lt = dp.cz_ft[U.ft0 + i];
-    const int lr = f - s_toff[i];
-    const int row = dp.tiles[lt].row0 + lr;
-    const int cr = dp.cz_tlro[lt] + lr;
-    double2 v[CZ_CL];
-#pragma unroll
-    for (int c = 0; c < CZ_CL; ++c) v[c] = (dp.cz_dbg & 2) ? Pw[cr] : *cl.map_shared_rank(Pw + cr, c);
-    double wx = 0.0, wy = 0.0;
-#pragma unroll
-    for (int c = 0; c < CZ_CL; ++c) {
-      wx += v[c].x;
-      wy += v[c].y;
-    }
-    const double2 Tc = s_T[i];
-    double px = 0.0, py = 0.0, dmax = 0.0;
-    if (finalize_row<MODE, false>(dp, a, row, row - dp.row_begin, Tc.x + wx, Tc.y + wy, px, py, dmax)) bad = true;
-    sp[f] = make_double2(px, py);
-    sd[f] = dmax;
-  }
-  __syncthreads();
-  if (MODE != MODE_RHS) {  // tile partials (and max |update|): fixed shape, one warp per tile
-    for (int i = warp; i < U.nft; i += CZW) {
-      double x = 0.0, y = 0.0, d = 0.0;
-      for (int f = s_toff[i] + lane; f < s_toff[i + 1]; f += 32) {
-        x += sp[f].x;
-        y += sp[f].y;
-        d = fmax(d, sd[f]);
-      }
-      warp_sum2(x, y);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
-      if (lane == 0) {
-        const int lt = dp.cz_ft[U.ft0 + i];
-        (a.pout ? a.pout : dp.partial)[lt] = make_double2(x, y);
-        if (a.fp_check) dp.pmax[lt] = d;
-      }
-    }
-  }
-  if (dp.cz_dbg & 32) __syncthreads();
-  else cl.sync();  // no CTA leaves while the others may still read its row sums
-  if (MODE == MODE_RHS) return;
-  constexpr bool FINAL = MODE == MODE_S4 || MODE == MODE_E1 || MODE == MODE_H2;
-  if (FINAL && bad) s_nonfinite = 1;
-  __syncthreads();
-  if (FINAL && tid == 0 && s_nonfinite) dp.ctrl->nonfinite = 1;
-  if (tid == 0) {
-    s_last = false;
-    if (!a.no_finish && CZT == NTHREADS) {  // CZT != NTHREADS: the launcher follows with k_finish
-      __threadfence();
-      const unsigned int t = atomicAdd(&dp.ctrl->ticket, 1u);
-      s_last = (t == gridDim.x - 1);
-    }
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  if (CZT == NTHREADS) {
-    finish_reduce(dp, a, dp.C <= WZ ? zs0 : nullptr);
-    if (tid == 0) dp.ctrl->ticket = 0;
-  }
 }
 
 // ---- single-CTA trajectory kernel for tiny graphs (world == 1): the whole
@@ -1916,42 +1652,6 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
   return launch_maybe_pdl(dp.pdl != 0, k_stage<MODE, RW, CR>, dim3(dp.ntiles), dim3(NTHREADS), dyn, s, dp, a, tm);
 }
 
-size_t cz_smem_bytes(int rows) { return sizeof(double2) * (size_t)(2 * (WZ + 8) + rows); }
-
-template <int MODE, int CZT>
-cudaError_t launch_stage_cz_t(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
-  static std::atomic<uint64_t> attr_set{0};  // one bit per device (the attribute is per device context)
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!((attr_set.load() >> (dev & 63)) & 1)) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage_cz<MODE, CZT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)cz_smem_bytes(CZ_MAX_ROWS));
-    if (e != cudaSuccess) return e;
-    attr_set.fetch_or(1ull << (dev & 63));
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(dp.cz * CZ_CL);
-  cfg.blockDim = dim3(CZT);
-  cfg.dynamicSmemBytes = cz_smem_bytes(dp.cz_rmax);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CZ_CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_stage_cz<MODE, CZT>, dp, a);
-  if (e != cudaSuccess || CZT == NTHREADS || MODE == MODE_RHS || a.no_finish) return e;
-  k_finish<<<1, NTHREADS, 0, s>>>(dp, a);  // the block-sum reduction (512 threads, fixed shape)
-  return cudaGetLastError();
-}
-
-template <int MODE>
-cudaError_t launch_stage_cz(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
-  return dp.cz_threads == 1024 ? launch_stage_cz_t<MODE, 1024>(dp, a, s) : launch_stage_cz_t<MODE, NTHREADS>(dp, a, s);
-}
-
 template <int MODE>
 cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
   if (dp.remote_warp) return launch_stage_m<MODE, true, false>(dp, a, s);
@@ -1988,31 +1688,6 @@ cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s)
 
 size_t stage_smem_bytes(int rows_per_tile) { return sizeof(double2) * (size_t)(WZ + 8 + rows_per_tile); }
 
-int cz_max_clusters() {
-  const size_t smem = cz_smem_bytes(CZ_MAX_ROWS);
-  if (cudaFuncSetAttribute(k_stage_cz<MODE_S1, NTHREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(CZ_CL * 64);
-  cfg.blockDim = dim3(NTHREADS);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CZ_CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_stage_cz<MODE_S1, NTHREADS>, &cfg) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  return n;
-}
-
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s) {
   if (dp.ntiles <= 0) {
     if (dp.peer_x && a.xsend) k_arrive<<<1, 1, 0, s>>>(dp);
@@ -2031,22 +1706,6 @@ cudaError_t launch_stage(int mode, const DevPlan& dp, const StageArgs& a, cudaSt
   if (dp.ntiles <= 0) {  // no rows here; a fused exchange still counts this rank's arrival
     if (dp.peer_x && a.xsend && mode != MODE_RHS && a.phase != PHASE_A) k_arrive<<<1, 1, 0, s>>>(dp);
     return cudaGetLastError();
-  }
-  if (dp.cz) {  // cluster-resident stage (world 1)
-    switch (mode) {
-      case MODE_RHS: return launch_stage_cz<MODE_RHS>(dp, a, s);
-      case MODE_S1: return launch_stage_cz<MODE_S1>(dp, a, s);
-      case MODE_S2: return launch_stage_cz<MODE_S2>(dp, a, s);
-      case MODE_S3: return launch_stage_cz<MODE_S3>(dp, a, s);
-      case MODE_S4: return launch_stage_cz<MODE_S4>(dp, a, s);
-      case MODE_POT: return launch_stage_cz<MODE_POT>(dp, a, s);
-      case MODE_E1: return launch_stage_cz<MODE_E1>(dp, a, s);
-      case MODE_H1: return launch_stage_cz<MODE_H1>(dp, a, s);
-      case MODE_H2: return launch_stage_cz<MODE_H2>(dp, a, s);
-      case MODE_M0: return launch_stage_cz<MODE_M0>(dp, a, s);
-      case MODE_MI: return launch_stage_cz<MODE_MI>(dp, a, s);
-      default: return cudaErrorInvalidValue;
-    }
   }
   switch (mode) {
     case MODE_RHS: return launch_stage_m<MODE_RHS>(dp, a, s);

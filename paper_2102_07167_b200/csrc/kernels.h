@@ -72,16 +72,6 @@ struct DevPlan {
   int32_t n_rchunks;
   double2* S;                 // [C] block sums S_b of the last reduction
   Ctrl* ctrl;
-  // cluster-resident stage (plan.h; world 1): k_stage_cz replaces k_stage
-  int32_t cz;                 // clusters of CZ_CL CTAs (0 = tile mode)
-  int32_t cz_rmax;            // max rows of a cluster
-  const CzUnit* cz_units;     // [cz * CZ_CL] per CTA: parts, staged windows, finalize tiles
-  const int32_t* cz_ft;       // finalize tiles (local ids) of every unit
-  const int32_t* cz_tlro;     // [ntiles] cluster-local row of each tile's row 0
-  int32_t cz_threads;         // threads per CTA of k_stage_cz (512, or 1024: KUR_CZ_THREADS, A/B)
-  int32_t cz_dbg;             // tooling (KUR_CZ_DBG, timing breakdown only; results invalid): bit 0 skip the
-                              // parts, bit 1 skip the cluster row-sum reads, bit 2 no barrier between parts, bit 3 no T,
-                              // bit 4 no finalize rows, bit 5 block instead of cluster barriers
 };
 
 // Stage epilogues (k = RHS of the stage state, theta_n = a.theta, acc = a.acc):
@@ -163,8 +153,6 @@ cudaError_t launch_set_ctrl(Ctrl* c, int record_every, int nrec_cap, double* r_t
 cudaError_t launch_permute(const int32_t* perm, int64_t n, const double* in, double* out, int dir,
                            cudaStream_t s);
 size_t stage_smem_bytes(int rows_per_tile);
-// cluster-resident stage: clusters of CZ_CL CTAs that can be co-resident on this device (0: none)
-int cz_max_clusters();
 // remote warp (remote_warp == 1): RING_SLOTS groups of 32 lanes x 4 entries x 16 bytes in flight
 constexpr int RING_SLOTS = 6;
 constexpr size_t RING_BYTES = (size_t)RING_SLOTS * 128 * 16;

@@ -81,28 +81,6 @@ struct Unit {       // 16 bytes of the pool
   uint32_t w[4];
 };
 
-// Cluster-resident stage (world 1, n <= CZ_MAX_N, plans with stored entries): the
-// column space (all of z) is split over the CZ_CL CTAs of a thread-block cluster, at most
-// CZ_MAX_WIN windows each, staged once per stage; every entry of the cluster's rows is then a
-// hot shared-memory gather in the CTA owning its column, the per-CTA row sums are added over
-// the cluster through distributed shared memory.  A cluster's rows are one slice of every
-// community (tiles), so each CTA's columns carry ~1/CZ_CL of the cluster's entries.
-constexpr int CZ_CL = 8;
-constexpr int CZ_MAX_WIN = 2;
-constexpr int64_t CZ_MAX_N = (int64_t)CZ_CL * CZ_MAX_WIN * WZ;
-constexpr int CZ_MAX_ROWS = 6144;  // rows of one cluster (row sums in shared memory, 16 B each)
-constexpr int CZ_MAX_FT = 32;      // tiles one CTA finalizes
-
-struct CzUnit {     // 32 bytes; device array [clusters * CZ_CL], unit = cluster * CZ_CL + CTA rank
-  int32_t part0;    // first part (hot, by window then sign) of this CTA
-  int32_t nparts;
-  int32_t w0, w1;   // windows staged (-1: none); parts of w0 first
-  int32_t nrows;    // rows of the cluster (cluster-local row ids 0..nrows-1 in the chunk headers)
-  int32_t ft0;      // first entry in the finalize-tile list
-  int32_t nft;      // tiles this CTA finalizes (their rows' sums are gathered over the cluster)
-  int32_t pad;
-};
-
 struct HostPlan {
   int64_t n = 0;
   int32_t C = 0;
@@ -128,13 +106,6 @@ struct HostPlan {
   std::vector<double> potc;         // [local rows] off-diagonal ones + [z_m inside W_m] (kur_potential)
   std::vector<int32_t> shard_row0;  // [world+1] internal row ranges of all ranks
   std::vector<int32_t> shard_tile0; // [world+1]
-  // cluster-resident stage (0 = tile mode)
-  int32_t cz = 0;                   // clusters
-  int32_t cz_rmax = 0;              // max rows of a cluster
-  std::vector<CzUnit> cz_units;     // [cz * CZ_CL]
-  std::vector<int32_t> cz_ft;       // finalize tiles (local tile ids) of every unit
-  std::vector<int32_t> cz_tlro;     // [tiles] cluster-local row of each tile's row 0
-  std::vector<int32_t> cz_tcl;      // [tiles] cluster of each tile
   // statistics (this rank)
   int64_t nnz = 0, n_idx_hot = 0, n_idx_remote = 0, n_slots_hot = 0, n_slots_remote = 0;
   int64_t n_dense_blocks = 0, n_sparse_blocks = 0, n_hot_parts = 0;
@@ -142,10 +113,7 @@ struct HostPlan {
 };
 
 // Builds the plan on the host.  `sm_count` steers the tile size choice.
-// cz_clusters > 0: thread-block clusters of CZ_CL CTAs that can be co-resident; the builder then
-// lays out the cluster-resident stage when the plan qualifies (world 1, n <= CZ_MAX_N, stored
-// entries, not KUR_FLAG_TILE_MODE / a forced tile size).
 kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int sm_count,
-                      HostPlan& P, std::string& err, int cz_clusters = 0);
+                      HostPlan& P, std::string& err);
 
 }  // namespace kur

@@ -52,7 +52,7 @@ class GraphInfo(ctypes.Structure):
                 ("n_slots_remote", _i64), ("n_dense_blocks", _i64), ("n_sparse_blocks", _i64),
                 ("n_tiles", _i64), ("n_hot_parts", _i64), ("n_window_loads", _i64), ("sincos_per_rhs", _i64),
                 ("bytes_per_rhs", _i64), ("bytes_pool", _i64), ("build_seconds", _d), ("remote_pass", _i32),
-                ("peer_exchange", _i32), ("cluster_plan", _i32), ("reserved_info", _i32)]
+                ("peer_exchange", _i32)]
 
 
 class AdaptiveCtrl(ctypes.Structure):
@@ -202,21 +202,19 @@ class Graph:
         return x_internal_full[self.row_begin:self.row_end]
 
 
-FLAG_REMOTE_PASS, FLAG_REMOTE_INLINE, FLAG_TILE_MODE = 1 << 16, 2 << 16, 4 << 16
+FLAG_REMOTE_PASS, FLAG_REMOTE_INLINE = 1 << 16, 2 << 16
 
 
-def _flags(tile_rows, remote_pass, tile_mode=False):
-    return (int(tile_rows) | (0 if remote_pass is None else (FLAG_REMOTE_PASS if remote_pass else FLAG_REMOTE_INLINE))
-            | (FLAG_TILE_MODE if tile_mode else 0))
+def _flags(tile_rows, remote_pass):
+    return int(tile_rows) | (0 if remote_pass is None else (FLAG_REMOTE_PASS if remote_pass else FLAG_REMOTE_INLINE))
 
 
 def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, remote_pass=None, scaling=None,
-                device=None, dist=None, tile_mode=False, **arrays):
+                device=None, dist=None, **arrays):
     """kur_graph_build from a kurgen.Instance (or the same arrays as keywords).
 
     scaling: 0 = uniform K/N (default, or inst.scaling), 1 = degree K/deg_m.
-    remote_pass: None = automatic, True/False = force the separate remote-gather pass / inline.
-    tile_mode: keep the tile plan where the cluster-resident stage would be chosen (kur.h)."""
+    remote_pass: None = automatic, True/False = force the separate remote-gather pass / inline."""
     src = arrays if inst is None else dict(
         n=inst.n, n_comm=inst.n_comm, community=inst.community, seg_ptr=inst.seg_ptr,
         seg_comm=inst.seg_comm, seg_kind=inst.seg_kind, idx_ptr=inst.idx_ptr, idx=inst.idx)
@@ -234,7 +232,7 @@ def graph_build(inst=None, *, dense_threshold=-1.0, hot_min=0, tile_rows=0, remo
                      seg_comm=_np_ptr(keep["seg_comm"]), seg_kind=_np_ptr(keep["seg_kind"]),
                      idx_ptr=_np_ptr(keep["idx_ptr"]), idx=_np_ptr(keep["idx"]),
                      dense_threshold=float(dense_threshold), hot_min=int(hot_min),
-                     flags=_flags(tile_rows, remote_pass, tile_mode), scaling=int(scaling), reserved=0)
+                     flags=_flags(tile_rows, remote_pass), scaling=int(scaling), reserved=0)
     if device is None:
         device = torch.cuda.current_device()
     dd = None
@@ -432,17 +430,16 @@ def order_parameter(g: Graph, theta, local=False, stream=None):
 
 # ------------------------------------------------------------------ host-only plan introspection
 _lib.kur_plan_build.argtypes = [ctypes.POINTER(GraphDesc), _i32, _i32, _i32, ctypes.POINTER(_p)]
-_lib.kur_plan_build_cz.argtypes = [ctypes.POINTER(GraphDesc), _i32, _i32, _i32, _i32, ctypes.POINTER(_p)]
 _lib.kur_plan_sizes.argtypes = [_p, _p]
 _lib.kur_plan_export.argtypes = [_p] + [_p] * 7
 _lib.kur_plan_destroy.argtypes = [_p]
 _lib.kur_plan_tiles.argtypes = [_p, _p, _p]
-for _f in ("kur_plan_build", "kur_plan_build_cz", "kur_plan_sizes", "kur_plan_export", "kur_plan_destroy", "kur_plan_tiles"):
+for _f in ("kur_plan_build", "kur_plan_sizes", "kur_plan_export", "kur_plan_destroy", "kur_plan_tiles"):
     getattr(_lib, _f).restype = ctypes.c_int
-EXPORTED = EXPORTED + ("kur_plan_build", "kur_plan_build_cz", "kur_plan_sizes", "kur_plan_export", "kur_plan_destroy", "kur_plan_tiles")
+EXPORTED = EXPORTED + ("kur_plan_build", "kur_plan_sizes", "kur_plan_export", "kur_plan_destroy", "kur_plan_tiles")
 
 
-def _desc_from(inst, dense_threshold=-1.0, hot_min=0, tile_rows=0, tile_mode=False):
+def _desc_from(inst, dense_threshold=-1.0, hot_min=0, tile_rows=0):
     keep = dict(
         community=np.ascontiguousarray(inst.community, np.int32),
         seg_ptr=np.ascontiguousarray(inst.seg_ptr, np.int64),
@@ -454,19 +451,16 @@ def _desc_from(inst, dense_threshold=-1.0, hot_min=0, tile_rows=0, tile_mode=Fal
                      seg_ptr=_np_ptr(keep["seg_ptr"]), seg_comm=_np_ptr(keep["seg_comm"]),
                      seg_kind=_np_ptr(keep["seg_kind"]), idx_ptr=_np_ptr(keep["idx_ptr"]),
                      idx=_np_ptr(keep["idx"]), dense_threshold=float(dense_threshold),
-                     hot_min=int(hot_min), flags=_flags(tile_rows, None, tile_mode),
-                     scaling=int(getattr(inst, "scaling", 0)),
+                     hot_min=int(hot_min), flags=int(tile_rows), scaling=int(getattr(inst, "scaling", 0)),
                      reserved=0)
     return desc, keep
 
 
-def plan_export(inst, *, rank=0, world=1, sm_count=148, dense_threshold=-1.0, hot_min=0, tile_rows=0, clusters=0,
-                tile_mode=False):
-    """Host-only: build the block plan and decode its stored layout (see kur.h).
-    clusters > 0: the cluster-resident layout with that many 8-CTA clusters when the plan qualifies."""
-    desc, keep = _desc_from(inst, dense_threshold, hot_min, tile_rows, tile_mode)
+def plan_export(inst, *, rank=0, world=1, sm_count=148, dense_threshold=-1.0, hot_min=0, tile_rows=0):
+    """Host-only: build the block plan and decode its stored layout (see kur.h)."""
+    desc, keep = _desc_from(inst, dense_threshold, hot_min, tile_rows)
     h = ctypes.c_void_p()
-    _check(_lib.kur_plan_build_cz(ctypes.byref(desc), rank, world, sm_count, clusters, ctypes.byref(h)))
+    _check(_lib.kur_plan_build(ctypes.byref(desc), rank, world, sm_count, ctypes.byref(h)))
     try:
         sz = np.zeros(16, np.int64)
         _check(_lib.kur_plan_sizes(h, _np_ptr(sz)))

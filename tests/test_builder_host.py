@@ -346,56 +346,3 @@ def test_split_community_plan_decodes():
                 if q < nloc:
                     assert inside
             assert nloc == nown or not (w[nloc] * 4096 >= rb and (w[nloc] + 1) * 4096 <= re_)
-
-
-def _cz_inst():
-    """A graph the cluster-resident stage takes (world 1, 8192 < n <= 65536, stored entries): dense
-    and sparse diagonal blocks, a dense off-diagonal pair, an empty and a 7-node community; labels
-    permuted (n = 15207: 4 windows)."""
-    P = np.array([[0.95, 0.002, 0.9, 0.0, 0.0, 0.001],
-                  [0.002, 0.3, 0.0, 0.0, 0.0, 0.0],
-                  [0.9, 0.0, 0.97, 0.001, 0.0, 0.0],
-                  [0.0, 0.0, 0.001, 0.05, 0.0, 0.0],
-                  [0.0, 0.0, 0.0, 0.0, 0.5, 0.0],
-                  [0.001, 0.0, 0.0, 0.0, 0.0, 0.6]])
-    return kurgen.sbm([5000, 3000, 4000, 1200, 7, 2000], P, 20210215, K=2.0, h=0.01)
-
-
-def _rows_of(plan):
-    out = []
-    for lj in range(plan["n_local"]):
-        s, e = plan["row_ptr"][lj], plan["row_ptr"][lj + 1]
-        out.append(sorted(zip(plan["cols"][s:e].tolist(), plan["neg"][s:e].tolist())))
-    return out
-
-
-@pytest.mark.parametrize("clusters", [3, 16])
-def test_cluster_plan_decodes_to_the_tile_plan(clusters):
-    """The cluster-resident layout (plan.h CzUnit: every entry a window-local slot of the CTA owning
-    its column, cluster-local row ids) decodes to exactly the tile plan's lists, row by row, with
-    conflict-free hot gathers; every tile is finalized by one CTA of its cluster (checked by the
-    decoder); each community is cut into min(clusters, size/32) slices."""
-    inst = _cz_inst()
-    a = kur.plan_export(inst, clusters=clusters)
-    b = kur.plan_export(inst, clusters=clusters, tile_mode=True)
-    sizes = np.bincount(inst.community, minlength=inst.n_comm)
-    assert a["n_tiles"] == sum(min(clusters, max(1, s // 32)) for s in sizes if s > 0)
-    assert b["n_tiles"] != a["n_tiles"]
-    assert a["conflicts"] == 0
-    assert a["idx_remote"] == 0 and a["idx_hot"] == b["idx_hot"] + b["idx_remote"]
-    assert np.array_equal(a["perm"], b["perm"]) and np.array_equal(a["D_idx"], b["D_idx"])
-    assert _rows_of(a) == _rows_of(b)
-
-
-def test_cluster_plan_only_where_it_applies():
-    """Tile plans for world > 1, n > 65536, a forced tile size, KUR_FLAG_TILE_MODE, no clusters, or
-    clusters whose rows would not fit the shared row sums (CZ_MAX_ROWS: one cluster for 15207 rows)."""
-    inst = _cz_inst()
-    tile = kur.plan_export(inst, tile_mode=True)["n_tiles"]
-    assert kur.plan_export(inst, clusters=0)["n_tiles"] == tile
-    assert kur.plan_export(inst, clusters=1)["n_tiles"] == tile
-    assert kur.plan_export(inst, clusters=16, tile_rows=256)["n_tiles"] == kur.plan_export(inst, tile_rows=256)["n_tiles"]
-    w2 = kur.plan_export(inst, clusters=16, world=2)
-    assert w2["n_tiles"] + kur.plan_export(inst, clusters=16, world=2, rank=1)["n_tiles"] == tile
-    big = kurgen.sbm([40000, 30000], np.array([[0.001, 0.0], [0.0, 0.001]]), 5, K=1.0)
-    assert (kur.plan_export(big, clusters=16)["n_tiles"] == kur.plan_export(big, tile_mode=True)["n_tiles"])

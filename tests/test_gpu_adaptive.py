@@ -78,7 +78,7 @@ def test_adaptive_group_bitwise(peer):
     inst = kurgen.sbm([3000, 500, 2000, 77], np.array(
         [[0.95, 0.01, 0.0, 0.6], [0.01, 0.3, 0.02, 0.0], [0.0, 0.02, 0.97, 0.1], [0.6, 0.0, 0.1, 0.5]]), 29,
         K=3.0)
-    g1 = kur.graph_build(inst, tile_mode=True)  # the tile plan: bitwise world-invariant (kur.h)
+    g1 = kur.graph_build(inst)
     full = g1.to_internal(torch.from_numpy(inst.theta0).cuda())
     omf = g1.to_internal(torch.from_numpy(inst.omega).cuda())
     th1 = full.clone()

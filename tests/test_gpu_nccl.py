@@ -65,7 +65,7 @@ def _worker(rank, port, peer, q):
         for k, v in (("f", f), ("rk", th_rk), ("he", th_he), ("host", th_host)):
             dist.all_gather_object(parts[k], v.cpu().numpy())
         if rank == 0:  # world 1 on this GPU
-            g1 = kur.graph_build(inst, device=0, tile_mode=True)
+            g1 = kur.graph_build(inst, device=0)
             t1 = g1.to_internal(torch.from_numpy(inst.theta0).to(dev))
             o1 = g1.to_internal(torch.from_numpy(inst.omega).to(dev))
             f1 = kur.rhs(g1, t1, o1, inst.K).cpu().numpy()

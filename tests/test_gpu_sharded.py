@@ -26,7 +26,7 @@ def _instances():
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_group_bitwise_equals_single(world, remote_pass, peer):
     for name, inst in _instances():
-        g1 = kur.graph_build(inst, remote_pass=remote_pass, tile_mode=True)
+        g1 = kur.graph_build(inst, remote_pass=remote_pass)
         dev = "cuda:0"
         th_full = g1.to_internal(torch.from_numpy(inst.theta0).to(dev))
         om_full = g1.to_internal(torch.from_numpy(inst.omega).to(dev))
@@ -85,7 +85,7 @@ def test_group_handle_alone_is_refused():
 
 def _group_vs_single(inst, world, steps=4, method="rk4", **kw):
     """world-rank group (one device) against world 1: RHS, `steps` steps and r(t), bitwise."""
-    g1 = kur.graph_build(inst, tile_mode=True, **kw)  # world 1 with the tile plan (kur.h)
+    g1 = kur.graph_build(inst, **kw)
     dev = "cuda:0"
     th_full = g1.to_internal(torch.from_numpy(inst.theta0).to(dev))
     om_full = g1.to_internal(torch.from_numpy(inst.omega).to(dev))
