@@ -554,6 +554,26 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
     for (int32_t c = 0; c < C; ++c) nt += (S.csize[(size_t)c] + r - 1) / r;
     if (nt >= 4LL * sm_count || r == 256) rows_per_tile = r;
   }
+  // One partial wave: when even 256-row tiles give fewer tiles than one wave of 2 CTAs per SM
+  // (config 3: 256 tiles for 296 slots, so 108 SMs ran two tiles and 40 ran one), each community
+  // is cut into floor(2 SMs x size / N) tiles of equal size instead (config 3: 18 tiles of 227-228
+  // rows, 288 tiles, every SM at most 2 x 228 rows instead of 2 x 256); never fewer tiles than
+  // the 256-row rule, never more than one wave.
+  std::vector<int32_t> ctiles((size_t)C, 0);  // > 0: balanced split into that many tiles
+  if (!force_rows && !tiny && total_len > 0 && rows_per_tile == 256) {
+    const int64_t T = 2LL * sm_count;
+    int64_t nt256 = 0, ntb = 0;
+    for (int32_t c = 0; c < C; ++c) nt256 += (S.csize[(size_t)c] + 255) / 256;
+    if (nt256 < T) {
+      for (int32_t c = 0; c < C; ++c) {
+        const int64_t sz = S.csize[(size_t)c];
+        if (sz == 0) continue;
+        ctiles[(size_t)c] = (int32_t)std::max<int64_t>((sz + 255) / 256, T * sz / n);
+        ntb += ctiles[(size_t)c];
+      }
+      if (ntb > T) std::fill(ctiles.begin(), ctiles.end(), 0);
+    }
+  }
   P.rows_per_tile = rows_per_tile;
   std::vector<int32_t> crt((size_t)C, rows_per_tile);
   std::vector<TileDesc> all;
@@ -561,6 +581,17 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   for (int32_t c = 0; c < C; ++c) {
     P.comm_tile0[(size_t)c] = (int32_t)all.size();
     const int RT = crt[(size_t)c];
+    if (ctiles[(size_t)c] > 0) {  // balanced split
+      const int64_t sz = S.csize[(size_t)c], k = ctiles[(size_t)c];
+      for (int64_t i = 0; i < k; ++i) {
+        TileDesc t{};
+        t.row0 = (int32_t)(S.moff[(size_t)c] + sz * i / k);
+        t.nrows = (int32_t)(S.moff[(size_t)c] + sz * (i + 1) / k - t.row0);
+        t.comm = c;
+        all.push_back(t);
+      }
+      continue;
+    }
     for (int64_t r0 = S.moff[(size_t)c]; r0 < S.moff[(size_t)c + 1]; r0 += RT) {
       TileDesc t{};
       t.row0 = (int32_t)r0;
