@@ -425,6 +425,10 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   // (profiles/r02/notes/pdl_ab.log): no gain on configs 3/4, config 5 4.41 -> 5.17 ms per RK4 step
   // (the early-resident k_remote / k_stage CTAs of the next stage only wait), so off by default.
   dp.pdl = (world == 1 && std::getenv("KUR_PDL") != nullptr) ? 1 : 0;
+  {
+    const char* ro = std::getenv("KUR_REMOTE_OVERLAP");  // k_remote CTAs per SM while k_stage overlaps it
+    dp.rov = (world == 1 && ro) ? std::max(0, std::min(3, std::atoi(ro))) : 0;
+  }
   dp.Wr = g->Wr;
   dp.peer_x = g->peer_on ? g->d_peer_x : nullptr;
   dp.peer_flag = g->d_peer_flag;

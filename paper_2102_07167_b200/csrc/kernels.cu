@@ -945,6 +945,7 @@ __device__ __forceinline__ bool stage_rows(const DevPlan& dp, const StageArgs& a
   }
 
   // ---- finalize: k_j = omega_j + (K/N) Im(conj z_j W_j), fused RK4 stage
+  if (!SMALL && a.rov_wait) asm volatile("griddepcontrol.wait;" ::: "memory");  // k_remote done: Wr complete
   const double2 Tc = (!SMALL && a.plazy) ? *s_T : __ldcg(a.Tin + T.comm);
   px = 0.0;
   py = 0.0;
@@ -1123,7 +1124,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
   __shared__ int s_nonfinite;
   __shared__ double2 s_T;  // deferred block sums: T of the tile's community
   const int tid = threadIdx.x;
-  pdl_wait_and_release();
+  if (!a.rov_wait) pdl_wait_and_release();  // rov_wait: only Wr depends on k_remote (waited for before the finalize)
   PROF_G(160);
   // implicit midpoint: iterations after convergence are no-ops (uniform: every CTA reads the same flag)
   // (phase A never skips: it may run before the finish that sets or clears the flag, and
@@ -1639,9 +1640,11 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(1ull << (dev & 63));
   }
+  bool rov = false;
   if (dp.has_remote && !dp.remote_warp && !a.no_remote && a.phase != PHASE_A) {
     cudaError_t e = launch_remote(dp, a.zin, s);
     if (e != cudaSuccess) return e;
+    rov = dp.rov > 0 && dp.world == 1 && a.phase == PHASE_FULL;
   }
   const size_t dyn = dp.has_parts ? stage_smem_bytes(dp.rows_per_tile) +
                                          ((dp.remote_warp == 1 || dp.remote_warp == 3) ? RING_BYTES : 0) +
@@ -1649,6 +1652,11 @@ cudaError_t launch_stage_m(const DevPlan& dp, const StageArgs& a, cudaStream_t s
   CUtensorMap tm;  // remote_warp 3: the tensor map of the stage's input z (zA or zB)
   if (dp.tmaps) tm = dp.tmaps[a.zin == dp.zbuf[0] ? 0 : 1];
   else memset(&tm, 0, sizeof(tm));
+  if (rov) {  // programmatic dependent of the k_remote just launched (it releases us at its start)
+    StageArgs b = a;
+    b.rov_wait = 1;
+    return launch_maybe_pdl(true, k_stage<MODE, RW, CR>, dim3(dp.ntiles), dim3(NTHREADS), dyn, s, dp, b, tm);
+  }
   return launch_maybe_pdl(dp.pdl != 0, k_stage<MODE, RW, CR>, dim3(dp.ntiles), dim3(NTHREADS), dyn, s, dp, a, tm);
 }
 
@@ -1681,7 +1689,8 @@ cudaError_t launch_remote(const DevPlan& dp, const double2* zin, cudaStream_t s)
     if (e != cudaSuccess) return e;
     dev_cached = dev;
   }
-  const long long need = (dp.n_rchunks + wpb - 1) / wpb, full = (long long)KREM_CTAS_PER_SM * sms;
+  const long long need = (dp.n_rchunks + wpb - 1) / wpb,
+                  full = (long long)(dp.rov > 0 ? dp.rov : KREM_CTAS_PER_SM) * sms;
   return launch_maybe_pdl(dp.pdl != 0, k_remote, dim3((unsigned)(need < full ? need : full)), dim3(KREM_THREADS), 0, s,
                           dp, zin);
 }

@@ -33,6 +33,10 @@ struct DevPlan {
   int32_t world;
   int32_t has_parts;          // any tile has stored entries (else no shared memory is needed)
   int32_t pdl;                // world 1: k_prologue / k_remote / k_stage launched as programmatic dependents
+  int32_t rov;                // > 0: k_stage overlaps the k_remote pass before it (KUR_REMOTE_OVERLAP = k_remote
+                              // CTAs per SM): launched as its programmatic dependent, it stages windows and
+                              // gathers the hot parts while k_remote runs and waits for it only before the
+                              // finalize, the first reader of Wr
   int32_t has_remote;         // any tile has remote parts summed out of line into Wr (see remote_warp)
   int32_t remote_warp;        // has_remote: 0 = the k_remote pass before each k_stage; inside k_stage, one
                               // warp of each tile sums its remote part while the others gather the hot
@@ -126,6 +130,7 @@ struct StageArgs {
   double2* pout;
   const double2* plazy;
   int no_finish;
+  int rov_wait;           // k_stage launched as the programmatic dependent of k_remote: wait before the finalize
 };
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
