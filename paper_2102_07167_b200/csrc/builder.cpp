@@ -558,7 +558,7 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   // (config 3: 256 tiles for 296 slots, so 108 SMs ran two tiles and 40 ran one), each community
   // is cut into floor(2 SMs x size / N) tiles of equal size instead (config 3: 18 tiles of 227-228
   // rows, 288 tiles, every SM at most 2 x 228 rows instead of 2 x 256); never fewer tiles than
-  // the 256-row rule, never more than one wave.
+  // the 256-row rule, never more than one wave, never below 192 rows per tile.
   std::vector<int32_t> ctiles((size_t)C, 0);  // > 0: balanced split into that many tiles
   if (!force_rows && !tiny && total_len > 0 && rows_per_tile == 256) {
     const int64_t T = 2LL * sm_count;
@@ -568,7 +568,8 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
       for (int32_t c = 0; c < C; ++c) {
         const int64_t sz = S.csize[(size_t)c];
         if (sz == 0) continue;
-        ctiles[(size_t)c] = (int32_t)std::max<int64_t>((sz + 255) / 256, T * sz / n);
+        // (tiles of >= 192 rows: a graph far smaller than one wave keeps ~256-row tiles, only balanced)
+        ctiles[(size_t)c] = (int32_t)std::max<int64_t>((sz + 255) / 256, std::min<int64_t>(T * sz / n, sz / 192));
         ntb += ctiles[(size_t)c];
       }
       if (ntb > T) std::fill(ctiles.begin(), ctiles.end(), 0);
