@@ -44,13 +44,7 @@ debug: $(KUR_SRCS) $(KUR_HDRS)
 	  -Xcompiler -fPIC,-fopenmp,-O3 -shared -o $(PKG)/libkur_debug.so $(KUR_SRCS) \
 	  -L$(NCCL_LIB) -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_LIB) -lgomp
 
-# tooling: A/B build with random z gathers not allocated in L1 (KUR_LIB=$(PKG)/libkur_na.so)
-na: $(KUR_SRCS) $(KUR_HDRS)
-	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -DKUR_Z_NOALLOC -Iinclude -I$(NCCL_INC) \
-	  -Xcompiler -fPIC,-fopenmp,-O3 -shared -o $(PKG)/libkur_na.so $(KUR_SRCS) \
-	  -L$(NCCL_LIB) -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_LIB) -lgomp
-
 clean:
 	rm -f kurgen/libkurgen.so oracle/liboracle.so $(PKG)/libkur.so $(PKG)/ptxas.log
 
-.PHONY: all clean prof debug na
+.PHONY: all clean prof debug

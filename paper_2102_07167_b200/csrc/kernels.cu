@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 
@@ -240,13 +241,6 @@ __device__ __forceinline__ void hot4(const uint2 v, const double2* zs, double& x
 // kernel) -> read through L2 (ld.global.cg) instead of the non-coherent path.
 template <bool COHERENT>
 __device__ __forceinline__ double2 ldz(const double2* p) {
-#ifdef KUR_Z_NOALLOC  // A/B build: random z gathers without an L1 allocation
-  if (!COHERENT) {
-    double2 r;
-    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
-    return r;
-  }
-#endif
   return COHERENT ? __ldcg(p) : __ldg(p);
 }
 
