@@ -426,8 +426,12 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   // (the early-resident k_remote / k_stage CTAs of the next stage only wait), so off by default.
   dp.pdl = (world == 1 && std::getenv("KUR_PDL") != nullptr) ? 1 : 0;
   {
-    const char* ro = std::getenv("KUR_REMOTE_OVERLAP");  // k_remote CTAs per SM while k_stage overlaps it
-    dp.rov = (world == 1 && ro) ? std::max(0, std::min(3, std::atoi(ro))) : 0;
+    // world 1: k_stage overlaps the tail of the k_remote pass (programmatic dependent launch, waiting for
+    // it only before the finalize); KUR_REMOTE_OVERLAP = k_remote CTAs per SM meanwhile (default 3, the
+    // pass's own occupancy; 0 = off).  Config 5 892.6 -> 897.6 RHS/s, config 3 (which then takes the
+    // pass) 29.05 K -> 29.7 K (profiles/r02/notes/remote_overlap_pdl_ab.log)
+    const char* ro = std::getenv("KUR_REMOTE_OVERLAP");
+    dp.rov = world == 1 ? (ro ? std::max(0, std::min(3, std::atoi(ro))) : 3) : 0;
   }
   dp.Wr = g->Wr;
   dp.peer_x = g->peer_on ? g->d_peer_x : nullptr;
@@ -684,7 +688,9 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
   for (size_t r = 0; r < gs.size(); ++r) {
     kur_graph* g = gs[r];
     StageArgs& a = args[r];
-    if (g->timing && mode != PH_PROLOGUE && g->dp.has_remote && !g->dp.remote_warp && !a.no_remote) {  // time apart
+    // time k_remote apart -- unless k_stage overlaps it (then one event pair spans both: an event between
+    // them would serialise the programmatic dependent launch)
+    if (g->timing && mode != PH_PROLOGUE && g->dp.has_remote && !g->dp.remote_warp && !a.no_remote && !g->dp.rov) {
       KUR_CUDA(g->mark(s));
       KUR_CUDA(launch_remote(g->dp, a.zin, s));
       KUR_CUDA(g->mark(s));

@@ -952,6 +952,17 @@ kur_status build_plan(const kur_graph_desc* d, int32_t rank, int32_t world, int 
   // 5 keeps the pass, which at world > 1 runs on the exchange stream concurrently with phase A; the
   // per-tile threshold does not depend on the world size.  Either way the bits are the same.)
   P.split_remote = !P.small && P.n_slots_remote * world >= (16LL << 20) && nt > 0 && P.n_slots_remote / nt >= 8192;
+  // World 1 with the overlapped pass (k_stage launched as k_remote's programmatic dependent, api.cpp /
+  // kernels.cu, on unless KUR_REMOTE_OVERLAP=0): plans whose inline remote part would otherwise run
+  // concurrently inside k_stage (small tiles, remote wavefronts >= half the hot ones: config 3) take
+  // the pass instead -- config 3 29.05 K -> 29.7 K RHS/s (profiles/r02/notes/remote_overlap_pdl_ab.log).
+  {
+    const char* ro = std::getenv("KUR_REMOTE_OVERLAP");
+    const bool overlap = world == 1 && !(ro && ro[0] == '0');
+    if (overlap && !P.small && P.n_slots_remote > 0 && P.rows_per_tile <= 512 &&
+        2 * P.n_slots_remote * 8 >= P.n_slots_hot)
+      P.split_remote = true;
+  }
   if (force_split) P.split_remote = !P.small && force_split == 1;
 #pragma omp parallel for schedule(dynamic, 4)
   for (int32_t lt = 0; lt < nt; ++lt) {
