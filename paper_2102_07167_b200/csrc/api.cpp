@@ -107,6 +107,9 @@ struct kur_graph {
   bool lazy_ok = false;
   double2* partialB = nullptr;
   const double2* lazy_prev = nullptr;  // partials of the previous stage if it skipped its reduction
+  bool defer_rec_ok = false;           // kur_step RK4, not the last step: S4 may defer its record too
+  bool lazy_rec_ok = true;             // KUR_LAZY_REC=0: every S4 reduces itself (A/B switch)
+  bool rec_pending = false;            // the previous stage (S4) deferred its record to this one
   size_t ev_used = 0;
   cudaError_t mark(cudaStream_t s) {  // records the next event of the pool on s
     if (!timing) return cudaSuccess;
@@ -455,6 +458,8 @@ kur_status kur_graph_build(const kur_graph_desc* desc, const kur_dist_desc* dist
   {
     const char* lz = std::getenv("KUR_LAZY_T");
     g->lazy_ok = world == 1 && dp.n_big == 0 && !(lz && lz[0] == '0');
+    const char* lr = std::getenv("KUR_LAZY_REC");
+    g->lazy_rec_ok = !(lr && lr[0] == '0');
   }
   dp.shard_row0 = g->d_shard_row0;
   dp.shard_tile0 = g->d_shard_tile0;
@@ -634,16 +639,24 @@ kur_status run_phase(const std::vector<kur_graph*>& gs, int mode, const std::vec
     a.theta_host = (mode == MODE_S4 || mode == MODE_E1 || mode == MODE_H2) ? g->host_out : nullptr;
     // deferred block sums (world 1): RK4 S1-S3 and Heun H1 leave the reduction to the next stage,
     // which reads their partials; the destination alternates so no stage overwrites what it reads
+    // RK4 S4 of a step that is not the call's last defers its reduction AND its step record: the next
+    // S1's last CTA runs the reduction (finish_reduce on S4's partials: r(t), ctrl->rpsi, the step
+    // counter) while the other CTAs form their T lazily
     if (mode == PH_PROLOGUE || !g->lazy_ok) {
       g->lazy_prev = nullptr;
+      g->rec_pending = false;
     } else {
-      const bool defer = record == REC_NONE &&
-                         (mode == MODE_S1 || mode == MODE_S2 || mode == MODE_S3 || mode == MODE_H1);
-      const bool takes = mode == MODE_S2 || mode == MODE_S3 || mode == MODE_S4 || mode == MODE_H2;
+      const bool s4_defer = mode == MODE_S4 && record == REC_STEP && g->defer_rec_ok && !g->host_out;
+      const bool defer = s4_defer || (record == REC_NONE && (mode == MODE_S1 || mode == MODE_S2 ||
+                                                             mode == MODE_S3 || mode == MODE_H1));
+      const bool takes = mode == MODE_S1 || mode == MODE_S2 || mode == MODE_S3 || mode == MODE_S4 ||
+                         mode == MODE_H2;
       a.plazy = takes ? g->lazy_prev : nullptr;
+      a.lazy_rec = (a.plazy && g->rec_pending) ? 1 : 0;
       if (defer || a.plazy) a.pout = a.plazy == g->partialB ? g->partial : g->partialB;
       a.no_finish = defer ? 1 : 0;
       g->lazy_prev = defer ? a.pout : nullptr;
+      g->rec_pending = s4_defer;
     }
   }
   if (world > 1 && mode != PH_PROLOGUE) {
@@ -855,7 +868,9 @@ kur_status step_impl(const std::vector<kur_graph*>& gs, const std::vector<RankIO
     if (host_out && n + 1 == nsteps) gs[0]->host_out = host_out;  // the last step's final stage stores it
     switch (method) {
       case KUR_RK4:
+        for (kur_graph* g : gs) g->defer_rec_ok = n + 1 < nsteps && g->lazy_rec_ok;  // the last S4 reduces itself
         for (int m = MODE_S1; m <= MODE_S4 && st == KUR_OK; ++m) st = stage(m, m == MODE_S4 ? REC_STEP : REC_NONE);
+        for (kur_graph* g : gs) g->defer_rec_ok = false;
         break;
       case KUR_EULER:
         st = stage(MODE_E1, REC_STEP);

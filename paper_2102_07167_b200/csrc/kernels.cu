@@ -1140,6 +1140,15 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_stage(const DevPlan dp, const S
     }
     return;
   }
+  if (a.lazy_rec && blockIdx.x == gridDim.x - 1) {  // the deferred S4 reduction + step record, by the
+    StageArgs ra = a;                                 // last-launched (lightest) tile's CTA, in
+    ra.pout = const_cast<double2*>(a.plazy);          // finish_reduce's order (same bits)
+    ra.record = REC_STEP;
+    ra.op_rpsi = ra.op_local = ra.v_out = nullptr;
+    ra.fp_reset = ra.fp_check = 0;
+    finish_reduce(dp, ra, nullptr);
+    __syncthreads();
+  }
   const int lt = dp.order[blockIdx.x];
   const TileDesc T = dp.tiles[lt];
   if (a.phase == PHASE_A && T.nloc == 0) return;  // nothing local to pre-sum (phase B starts from 0)

@@ -131,6 +131,8 @@ struct StageArgs {
   const double2* plazy;
   int no_finish;
   int rov_wait;           // k_stage launched as the programmatic dependent of k_remote: wait before the finalize
+  int lazy_rec;           // the previous stage (RK4 S4) deferred its step record too: the last CTA of this
+                          // grid runs finish_reduce on plazy at its start (r(t), ctrl->rpsi, step counter)
 };
 
 cudaError_t launch_prologue(const DevPlan& dp, const StageArgs& a, cudaStream_t s);
