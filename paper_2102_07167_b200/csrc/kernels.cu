@@ -1386,6 +1386,7 @@ __device__ __forceinline__ void local_reduce(const DevPlan& dp, const double2* p
     S_sh[c] = seq_sum_partials(src, t0, t1);
   }
   for (int i = 0; i < dp.n_big; ++i) {
+    if (i > 0) __syncthreads();  // red is reused: warp 0 has read the previous iteration's
     const int c = dp.big_comm[i];
     const int t0 = dp.comm_tile0[c], t1 = dp.comm_tile0[c + 1];
     double x = 0.0, y = 0.0;
@@ -1394,11 +1395,10 @@ __device__ __forceinline__ void local_reduce(const DevPlan& dp, const double2* p
       x += v.x;
       y += v.y;
     }
-    block_sum2(x, y, red);
+    block_sum2(x, y, red);  // its barrier also orders the small communities' S_sh before thread 0's reads
     if (tid == 0) S_sh[c] = make_double2(x, y);
-    __syncthreads();
   }
-  __syncthreads();
+  if (dp.n_big == 0) __syncthreads();
   if (tid == 0) {  // T of this tile's community = sum over its dense column communities
     double x = 0.0, y = 0.0;
     for (int i = dp.D_ptr[c_own]; i < dp.D_ptr[c_own + 1]; ++i) {
@@ -1409,6 +1409,7 @@ __device__ __forceinline__ void local_reduce(const DevPlan& dp, const double2* p
     *sT = make_double2(x, y);
   }
   if (want_rpsi) {  // uniform branch
+    __syncthreads();          // thread 0's S_sh entries visible; red free
     double x = 0.0, y = 0.0;  // r e^{i psi} = (1/N) sum_b S_b
     for (int c = tid; c < dp.C; c += NTHREADS) {
       const double2 v = S_sh[c];
