@@ -16,3 +16,10 @@ for c in 5 3; do
   ncu --set full --clock-control none --import-source on -k regex:k_remote -s 6 -c 1 -o $O/cfg${c}_k_remote $CMD > $O/ncu_r$c.log 2>&1; echo full_remote$c=$?
 done
 ls -la $O
+# the four reports together exceed gpurun's 64 MiB return limit: summarise them on the box, keep the text
+for c in 5 3; do for k in k_stage k_remote; do
+  python tools/ncu_summary.py $O/cfg${c}_$k.ncu-rep > $O/cfg${c}_${k}_ncu_full.txt 2>&1
+  python tools/ncu_stalls.py $O/cfg${c}_$k.ncu-rep > $O/cfg${c}_${k}_stalls.txt 2>&1
+  rm -f $O/cfg${c}_$k.ncu-rep
+done; python tools/launch_summary.py $O/launches_cfg$c.csv > $O/launches_cfg${c}_summary.txt 2>&1; done
+du -sh $O
