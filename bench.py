@@ -375,6 +375,9 @@ def main():
                 "kernel_bytes_frac": kernel_bytes / (stage_ms / 1e3) / 1e9 / peak,
                 "traffic_gbs": None if traffic is None else traffic / (stage_ms / 1e3) / 1e9}
     if int(info["n_idx"]) == 0:  # entry-free plan (complete graph): no index stream at all
+        if world == 1 and tm["launches"] <= 1:  # the whole K-step call was one launch
+            roofline["kernel"] = ("single-launch trajectory kernel (k_persist_rk4, or k_small_dense for tiny graphs): "
+                                  "avg_launch_ms is its time per RK4 stage = one RHS evaluation")
         roofline["note"] = ("entry-free plan: the SURVEY bytes are nominal -- the persistent trajectory kernel keeps "
                             "theta_n, acc, z and omega on chip for the whole kur_step, so per stage it moves only "
                             "its tile partials; it is bound by fp64 issue (sincos) and the per-stage grid "
